@@ -1,0 +1,508 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Each test names what fixes the expected value: a worked example the paper/SPEC prints (tests/golden),
+a closed form, a brute force on tiny inputs, an independent algorithm, or a library routine.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import workload
+from oracle import luffy_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rows(name):
+    with open(os.path.join(GOLD, name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                yield line
+
+
+# ---------------------------------------------------------------- Eq. (1), Eq. (2)
+
+def test_eq1_worked_values():
+    for line in _rows("eq1_attention_cost.txt"):
+        B, L, d, P, exp = map(int, line.split())
+        assert O.attention_cost(B, L, d, P) == exp
+
+
+def _count_attention_macs(B, L, d):
+    """Brute force: walk the loops of a naive single-head attention and count multiply-adds
+    (Q,K,V projections, QK^T, AV) -- P:314's operation count, counted rather than retyped."""
+    n = 0
+    for _b in range(B):
+        for _proj in range(3):
+            for _t in range(L):
+                for _o in range(d):
+                    for _i in range(d):
+                        n += 1
+        for _q in range(L):
+            for _k in range(L):
+                for _i in range(d):
+                    n += 1          # QK^T
+        for _q in range(L):
+            for _k in range(L):
+                for _i in range(d):
+                    n += 1          # AV
+    return n
+
+
+@pytest.mark.parametrize("B,L,d", [(1, 1, 1), (2, 3, 4), (3, 5, 2), (1, 7, 3)])
+def test_eq1_equals_counted_operations(B, L, d):
+    assert O.attention_cost(B, L, d) == _count_attention_macs(B, L, d)
+
+
+def test_eq1_scaling_laws():
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        B, L, d = (int(x) for x in rng.integers(1, 50, 3))
+        assert O.attention_cost(2 * B, L, d) == 2 * O.attention_cost(B, L, d)
+        assert O.attention_cost(B, L, d, P=2) == O.attention_cost(B, L, d) / 2
+
+
+def test_eq2_worked_values():
+    for line in _rows("eq2_adaptive_threshold.txt"):
+        li, lp, exp = map(float, line.split())
+        assert abs(O.adaptive_threshold(li, lp) - exp) < 5e-6
+    xs = [O.adaptive_threshold(10.0, lp) for lp in np.linspace(10, 0, 21)]
+    assert all(a > b for a, b in zip(xs, xs[1:]))     # strictly decreasing in l_norm
+
+
+# ---------------------------------------------------------------- similarity
+
+def test_normalized_cosine_closed_forms():
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal(17)
+    v = rng.standard_normal(17)
+    v -= (v @ u) / (u @ u) * u
+    assert O.normalized_cosine(u, u) == pytest.approx(1.0, abs=1e-15)
+    assert O.normalized_cosine(u, -u) == pytest.approx(0.0, abs=1e-15)
+    assert O.normalized_cosine(u, v) == pytest.approx(0.5, abs=1e-15)
+    assert math.isnan(O.normalized_cosine(u, np.zeros(17)))
+
+
+def test_similarity_matrix_matches_pairwise_definition():
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((9, 5))
+    X[3] = 0.0
+    s = O.similarity_matrix(X)
+    for i in range(9):
+        for j in range(9):
+            ref = O.normalized_cosine(X[i], X[j])
+            if math.isnan(ref):
+                assert math.isnan(s[i, j])
+            else:
+                assert s[i, j] == pytest.approx(ref, abs=1e-14)
+    adj = O.threshold_graph(s, 0.5)
+    assert not adj[3].any() and not adj[:, 3].any() and not adj.diagonal().any()
+
+
+# ---------------------------------------------------------------- routing
+
+def test_route_matches_torch_topk_and_softmax():
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((64, 16))
+    Wg = rng.standard_normal((8, 16))
+    for k, renorm in [(1, False), (2, True), (3, True), (2, False)]:
+        r = O.route(X, Wg, k, renorm)
+        lt = torch.from_numpy(X) @ torch.from_numpy(Wg).T
+        vals, idx = torch.topk(lt, k, dim=1)
+        assert np.array_equal(r.idx, idx.numpy())
+        if renorm:
+            w = torch.softmax(vals, dim=1).numpy()
+            assert np.allclose(r.w.sum(1), 1.0, atol=1e-12)
+        else:
+            w = torch.gather(torch.softmax(lt, dim=1), 1, idx).numpy()
+        assert np.allclose(r.w, w, atol=1e-14)
+
+
+def test_route_brute_force_small_E_and_ties():
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        E = int(rng.integers(2, 5))
+        k = int(rng.integers(1, E + 1))
+        logits = rng.integers(-2, 3, size=E).astype(np.float64)   # many exact ties
+        X = logits[None, :]
+        Wg = np.eye(E)
+        r = O.route(X, Wg, k, k > 1)
+        # brute force: lexicographically smallest sequence of ids among orderings sorted by logit desc
+        best = min(itertools.permutations(range(E)),
+                   key=lambda p: tuple((-logits[e], e) for e in p))
+        assert list(r.idx[0]) == list(best[:k])
+        ties = any(logits[best[i]] == logits[best[i + 1]] for i in range(min(k, E - 1)))
+        assert bool(r.near_tie[0]) == ties
+
+
+# ---------------------------------------------------------------- greedy representative selection
+
+def _graph(n, edges):
+    adj = np.zeros((n, n), bool)
+    for a, b in edges:
+        adj[a, b] = adj[b, a] = True
+    return adj
+
+
+def test_greedy_worked_examples():
+    for line in _rows("condense_examples.txt"):
+        name, n, edges, exp = (p.strip() for p in line.split("|"))
+        es = [tuple(map(int, e.split("-"))) for e in edges.split(",") if e]
+        rep = O.greedy_condense(_graph(int(n), es))
+        assert list(rep) == [int(x) for x in exp.split(",")], name
+
+
+def _rounds_greedy(adj):
+    """Independent algorithm: parallel 2-hop local-maximum rounds (SURVEY §8c A8 proof): every alive
+    node whose (residual degree, -id) is the strict max of its alive 2-hop ball is selected in the
+    same round together with its alive neighbours.  Equal to the sequential greedy by the theorem."""
+    n = adj.shape[0]
+    nbr = [set(np.nonzero(adj[i])[0].tolist()) for i in range(n)]
+    alive = set(range(n))
+    rep = [-1] * n
+    while alive:
+        key = {u: (len(nbr[u] & alive), -u) for u in alive}
+        m1 = {u: max([key[u]] + [key[v] for v in nbr[u] & alive]) for u in alive}
+        m2 = {u: max([m1[u]] + [m1[v] for v in nbr[u] & alive]) for u in alive}
+        win = [u for u in alive if m2[u] == key[u]]
+        claimed = set()
+        for u in win:
+            rep[u] = u
+            for v in nbr[u] & alive:
+                rep[v] = u
+                claimed.add(v)
+        alive -= set(win) | claimed
+    return np.array(rep)
+
+
+def _brute_greedy(adj):
+    """Independent formulation with Python sets: literally 'take the highest-degree token, condense
+    its neighbours, repeat' on an explicit shrinking edge list."""
+    n = adj.shape[0]
+    edges = {(a, b) for a in range(n) for b in range(n) if adj[a, b]}
+    nodes = set(range(n))
+    rep = [-1] * n
+    while nodes:
+        deg = {u: sum(1 for (a, b) in edges if a == u) for u in nodes}
+        u = sorted(nodes, key=lambda x: (-deg[x], x))[0]
+        nb = {b for (a, b) in edges if a == u}
+        rep[u] = u
+        for v in nb:
+            rep[v] = u
+        gone = nb | {u}
+        nodes -= gone
+        edges = {(a, b) for (a, b) in edges if a not in gone and b not in gone}
+    return np.array(rep)
+
+
+def test_greedy_equals_brute_force_and_rounds_on_random_graphs():
+    rng = np.random.default_rng(5)
+    for trial in range(600):
+        n = int(rng.integers(1, 14))
+        p = rng.uniform(0.05, 0.7)
+        a = np.triu(rng.random((n, n)) < p, 1)
+        adj = a | a.T
+        rep = O.greedy_condense(adj)
+        assert np.array_equal(rep, _brute_greedy(adj)), trial
+        assert np.array_equal(rep, _rounds_greedy(adj)), trial
+
+
+def test_greedy_rounds_on_clustered_graphs():
+    rng = np.random.default_rng(6)
+    for trial in range(40):
+        n = int(rng.integers(20, 120))
+        pts = rng.standard_normal((n, 2)) + rng.integers(0, 4, size=(n, 1)) * 3.0
+        dist = np.linalg.norm(pts[:, None] - pts[None], axis=-1)
+        adj = dist < rng.uniform(0.5, 1.5)
+        np.fill_diagonal(adj, False)
+        assert np.array_equal(O.greedy_condense(adj), _rounds_greedy(adj)), trial
+
+
+def test_greedy_invariants():
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        n = int(rng.integers(1, 40))
+        a = np.triu(rng.random((n, n)) < rng.uniform(0, 0.5), 1)
+        adj = a | a.T
+        rep = O.greedy_condense(adj)
+        assert (rep >= 0).all()                                   # coverage
+        assert np.array_equal(rep[rep], rep)                      # idempotence
+        for i in range(n):                                        # soundness
+            assert rep[i] == i or adj[i, rep[i]]
+        reps = np.unique(rep)
+        assert not adj[np.ix_(reps, reps)].any()                  # representatives are independent
+    clique = ~np.eye(7, dtype=bool)
+    assert (O.greedy_condense(clique) == 0).all()                 # one representative per clique
+
+
+def test_condense_duplicates_and_threshold_above_one():
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((40, 32))
+    X[10] = X[3]
+    X[20] = X[3]
+    X[31] = X[7]
+    idx = np.zeros((40, 1), np.int64)
+    c = O.condense(X, idx, 1, 1.0 - 1e-5)
+    assert c.rep[10, 0] == c.rep[3, 0] == c.rep[20, 0]             # exact duplicates condensed
+    assert c.rep[31, 0] == c.rep[7, 0]
+    c2 = O.condense(X, idx, 1, 1.01)
+    assert np.array_equal(c2.rep[:, 0], np.arange(40))            # h > 1: identity (R4)
+
+
+# ---------------------------------------------------------------- pack / layout
+
+def test_pack_conservation_and_stable_order():
+    cfg = workload.CONFIGS["C1"]
+    X, _, _ = workload.make_tokens(cfg, rank=1, num_seqs=2, seq_len=32)
+    Wg = workload.make_gate(cfg)
+    r = O.route(X, Wg, cfg.top_k, True)
+    c = O.condense(X, r.idx, cfg.num_experts, 0.9)
+    pk = O.pack(r.idx, c.rep, cfg.num_experts)
+    T, k = r.idx.shape
+    n_cond = int((c.rep != np.arange(T)[:, None]).sum())
+    assert pk.perm.size == pk.counts.sum() == T * k - n_cond      # conservation
+    brute = sorted((int(r.idx[t, j]), t) for t in range(T) for j in range(k) if c.rep[t, j] == t)
+    assert [(int(e), int(t)) for e, t in zip(pk.slot_expert, pk.perm)] == brute
+    assert np.array_equal(pk.perm[pk.pos], c.rep)
+    assert np.array_equal(pk.slot_expert[pk.pos], r.idx)
+
+
+def test_recv_layout_conserves_rows():
+    rng = np.random.default_rng(9)
+    P, E = 4, 8
+    cnt = rng.integers(0, 50, size=(P, E))
+    total = 0
+    for rank in range(P):
+        blocks, off = O.recv_layout(cnt, rank, E, P)
+        assert off[-1] == sum(b[3] for b in blocks)
+        assert [b[1] for b in blocks] == sorted(b[1] for b in blocks)
+        total += off[-1]
+    assert total == cnt.sum()
+
+
+# ---------------------------------------------------------------- expert + layer vs torch fp64 autograd
+
+def _torch_dense_moe(X, Wg, W1, W2, W3, k, act, rep=None):
+    """Looped dense top-k MoE in torch fp64: every copy runs its own expert on x_{rep(t,k)}."""
+    X = torch.tensor(X, dtype=torch.float64, requires_grad=True)
+    Wg = torch.tensor(Wg, dtype=torch.float64, requires_grad=True)
+    W1 = torch.tensor(W1, dtype=torch.float64, requires_grad=True)
+    W2 = torch.tensor(W2, dtype=torch.float64, requires_grad=True)
+    W3t = None if W3 is None else torch.tensor(W3, dtype=torch.float64, requires_grad=True)
+    logits = X @ Wg.T
+    vals, idx = torch.topk(logits, k, dim=1)
+    w = torch.softmax(vals, 1) if k > 1 else torch.gather(torch.softmax(logits, 1), 1, idx)
+    ys = []
+    for t in range(X.shape[0]):
+        y = 0
+        for j in range(k):
+            e = int(idx[t, j])
+            src = t if rep is None else int(rep[t, j])
+            pre = W1[e] @ X[src]
+            if act == "gelu":
+                a = torch.nn.functional.gelu(pre)
+            else:
+                a = torch.nn.functional.silu(pre) * (W3t[e] @ X[src])
+            y = y + w[t, j] * (W2[e] @ a)
+        ys.append(y)
+    Y = torch.stack(ys)
+    return X, Wg, W1, W2, W3t, Y, idx
+
+
+@pytest.mark.parametrize("act,k", [("gelu", 2), ("gelu", 1), ("swiglu", 2)])
+def test_plain_layer_matches_torch_autograd(act, k):
+    rng = np.random.default_rng(10)
+    T, d, f, E = 12, 8, 16, 4
+    X = rng.standard_normal((T, d))
+    Wg = rng.standard_normal((E, d))
+    W1 = rng.standard_normal((E, f, d)) * 0.3
+    W2 = rng.standard_normal((E, d, f)) * 0.3
+    W3 = rng.standard_normal((E, f, d)) * 0.3 if act == "swiglu" else None
+    dY = rng.standard_normal((T, d))
+    st = O.layer_forward(X, Wg, W1, W2, W3, k, h=1.01, act=act)
+    g = O.layer_backward(st, X, Wg, W1, W2, W3, dY, act=act)
+    Xt, Wgt, W1t, W2t, W3t, Y, idx = _torch_dense_moe(X, Wg, W1, W2, W3, k, act)
+    assert np.array_equal(st.routing.idx, idx.numpy())
+    assert np.allclose(st.Y, Y.detach().numpy(), atol=1e-12)
+    Y.backward(torch.from_numpy(dY))
+    assert np.allclose(g.dX, Xt.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dWg, Wgt.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dW1, W1t.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dW2, W2t.grad.numpy(), atol=1e-11)
+    if act == "swiglu":
+        assert np.allclose(g.dW3, W3t.grad.numpy(), atol=1e-11)
+
+
+def _clustered(rng, T, d, n_centres=3, tau=0.05):
+    c = rng.standard_normal((n_centres, d))
+    return c[rng.integers(0, n_centres, T)] + tau * rng.standard_normal((T, d))
+
+
+@pytest.mark.parametrize("act", ["gelu", "swiglu"])
+def test_condensed_layer_matches_frozen_map_autograd(act):
+    rng = np.random.default_rng(11)
+    T, d, f, E, k = 24, 8, 16, 3, 2
+    X = _clustered(rng, T, d)
+    Wg = rng.standard_normal((E, d))
+    W1 = rng.standard_normal((E, f, d)) * 0.3
+    W2 = rng.standard_normal((E, d, f)) * 0.3
+    W3 = rng.standard_normal((E, f, d)) * 0.3 if act == "swiglu" else None
+    dY = rng.standard_normal((T, d))
+    st = O.layer_forward(X, Wg, W1, W2, W3, k, h=0.95, act=act)
+    assert (st.cond.rep != np.arange(T)[:, None]).sum() > 5     # something was condensed
+    g = O.layer_backward(st, X, Wg, W1, W2, W3, dY, act=act)
+    Xt, Wgt, W1t, W2t, W3t, Y, idx = _torch_dense_moe(X, Wg, W1, W2, W3, k, act, rep=st.cond.rep)
+    assert np.allclose(st.Y, Y.detach().numpy(), atol=1e-12)
+    Y.backward(torch.from_numpy(dY))
+    assert np.allclose(g.dX, Xt.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dWg, Wgt.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dW1, W1t.grad.numpy(), atol=1e-11)
+    assert np.allclose(g.dW2, W2t.grad.numpy(), atol=1e-11)
+
+
+def test_condensed_backward_finite_differences():
+    rng = np.random.default_rng(12)
+    T, d, f, E, k = 16, 6, 10, 3, 2
+    X = _clustered(rng, T, d)
+    Wg = rng.standard_normal((E, d))
+    W1 = rng.standard_normal((E, f, d)) * 0.3
+    W2 = rng.standard_normal((E, d, f)) * 0.3
+    dY = rng.standard_normal((T, d))
+    st = O.layer_forward(X, Wg, W1, W2, None, k, h=0.95)
+    g = O.layer_backward(st, X, Wg, W1, W2, None, dY)
+
+    def loss(Xp, Wgp, W1p):
+        s2 = O.layer_forward(Xp, Wgp, W1p, W2, None, k, h=0.95, rep=st.cond.rep,
+                             routing=O.route(Xp, Wgp, k, True))
+        return float((s2.Y * dY).sum())
+    eps = 1e-6
+    for _ in range(6):
+        for which in range(3):
+            D = [np.zeros_like(X), np.zeros_like(Wg), np.zeros_like(W1)]
+            D[which] = rng.standard_normal(D[which].shape)
+            args_p = [X + eps * D[0], Wg + eps * D[1], W1 + eps * D[2]]
+            args_m = [X - eps * D[0], Wg - eps * D[1], W1 - eps * D[2]]
+            fd = (loss(*args_p) - loss(*args_m)) / (2 * eps)
+            an = float((g.dX * D[0]).sum() + (g.dWg * D[1]).sum() + (g.dW1 * D[2]).sum())
+            assert fd == pytest.approx(an, rel=1e-6, abs=1e-8)
+
+
+def test_exact_duplicate_equivalence():
+    """If every condensed member is a bitwise copy of its representative, Y equals the plain layer
+    and dW1/dW2 equal the plain ones (SURVEY §8c 'Whole layer' pin)."""
+    rng = np.random.default_rng(13)
+    T, d, f, E, k = 20, 8, 12, 3, 2
+    base = rng.standard_normal((6, d))
+    X = base[rng.integers(0, 6, T)]
+    Wg = rng.standard_normal((E, d))
+    W1 = rng.standard_normal((E, f, d)) * 0.3
+    W2 = rng.standard_normal((E, d, f)) * 0.3
+    dY = rng.standard_normal((T, d))
+    sc = O.layer_forward(X, Wg, W1, W2, None, k, h=1.0 - 1e-9)
+    sp = O.layer_forward(X, Wg, W1, W2, None, k, h=1.01)
+    assert sc.pk.perm.size < sp.pk.perm.size
+    assert np.allclose(sc.Y, sp.Y, atol=1e-13)
+    gc = O.layer_backward(sc, X, Wg, W1, W2, None, dY)
+    gp = O.layer_backward(sp, X, Wg, W1, W2, None, dY)
+    assert np.allclose(gc.dW1, gp.dW1, atol=1e-12)
+    assert np.allclose(gc.dW2, gp.dW2, atol=1e-12)
+    assert np.allclose(gc.dWg, gp.dWg, atol=1e-12)
+    # expert-path input gradient moves to the representative: totals per distinct row agree
+    assert np.allclose(gc.dX.sum(0), gp.dX.sum(0), atol=1e-11)
+
+
+def test_expert_ffn_matches_torch():
+    rng = np.random.default_rng(14)
+    x = rng.standard_normal((5, 8))
+    W1 = rng.standard_normal((12, 8))
+    W2 = rng.standard_normal((8, 12))
+    W3 = rng.standard_normal((12, 8))
+    o, _ = O.expert_ffn(x, W1, W2, None, "gelu")
+    ref = torch.nn.functional.gelu(torch.from_numpy(x) @ torch.from_numpy(W1).T) @ torch.from_numpy(W2).T
+    assert np.allclose(o, ref.numpy(), atol=1e-12)
+    o, _ = O.expert_ffn(x, W1, W2, W3, "swiglu")
+    xt = torch.from_numpy(x)
+    ref = (torch.nn.functional.silu(xt @ torch.from_numpy(W1).T) * (xt @ torch.from_numpy(W3).T)) @ torch.from_numpy(W2).T
+    assert np.allclose(o, ref.numpy(), atol=1e-12)
+
+
+# ---------------------------------------------------------------- sequence migration (Alg. 1)
+
+def test_alg1_worked_values():
+    for line in _rows("alg1_cost_growth.txt"):
+        Bj, Lj, ln, d, exp = map(int, line.split())
+        assert O.cost_growth(Bj, Lj, ln, d) == exp
+    for line in _rows("alg1_candidate_set.txt"):
+        f, q, exp = line.split()
+        assert O.candidate_set(np.array([int(x) for x in f.split(",")]), int(q)) == [int(x) for x in exp.split(",")]
+    for line in _rows("alg1_combine_traffic.txt"):
+        ra, rb, exp = line.split()
+        f = O.combine_traffic(np.array([int(x) for x in ra.split(",")]), int(rb))
+        assert list(f) == [int(x) for x in exp.split(",")]
+
+
+def test_alg1_paper_example_padding_and_formula():
+    rows = list(_rows("alg1_paper_example.txt"))
+    for line in rows:
+        gpu, lens, new, pads = line.split()
+        lens = [int(x) for x in lens.split(",")]
+        L = max(lens + [int(new)])
+        assert sum(L - x for x in lens + [int(new)]) == int(pads)   # "10 padded zeros" either way
+    g1 = O.cost_growth(1, 1, 11, 8)
+    g2 = O.cost_growth(2, 6, 11, 8)
+    assert (g1, g2) == (7888, 8688) and g1 < g2
+
+
+def _random_problem(rng, S, P):
+    seq_len = rng.integers(1, 20, size=S)
+    rows_at = rng.integers(0, 10, size=(S, P))
+    return seq_len, rows_at
+
+
+def test_alg1_single_sequence_exhaustive():
+    rng = np.random.default_rng(15)
+    for _ in range(200):
+        P = int(rng.integers(1, 6))
+        seq_len, rows_at = _random_problem(rng, 1, P)
+        dest, _ = O.plan_migration(seq_len, rows_at, q=P, row_bytes=8, d=4, capacity=10 ** 9)
+        f = O.combine_traffic(rows_at[0], 8)
+        # all GPUs empty: growth ties, so the traffic tie-break decides -> exhaustive argmin (f, id)
+        best = min(range(P), key=lambda j: (O.cost_growth(0, 0, int(seq_len[0]), 4), int(f[j]), j))
+        assert dest[0] == best
+
+
+def test_alg1_q1_is_argmin_traffic_and_properties():
+    rng = np.random.default_rng(16)
+    for _ in range(300):
+        S, P = int(rng.integers(1, 7)), int(rng.integers(1, 6))
+        seq_len, rows_at = _random_problem(rng, S, P)
+        rb = 16
+        dest, comb = O.plan_migration(seq_len, rows_at, q=1, row_bytes=rb, d=4, capacity=10 ** 9)
+        for i in range(S):
+            assert dest[i] == O.candidate_set(O.combine_traffic(rows_at[i], rb), 1)[0]
+        # total predicted combine bytes <= stay-at-home policy
+        home = np.arange(S) % P
+        home_bytes = sum(O.combine_traffic(rows_at[i], rb)[home[i]] for i in range(S))
+        assert comb.sum() <= home_bytes
+        q = int(rng.integers(1, P + 1))
+        cap = max(int(np.ceil(1.5 * seq_len.sum() / P)), int(seq_len.max()))
+        dest, comb = O.plan_migration(seq_len, rows_at, q=q, row_bytes=rb, d=4, capacity=0)
+        load = np.bincount(dest, weights=seq_len, minlength=P)
+        assert (load <= cap).all()
+        for i in range(S):
+            f = O.combine_traffic(rows_at[i], rb)
+            H = O.candidate_set(f, q)
+            if dest[i] in H:   # candidates dominate non-candidates on traffic
+                assert all(f[dest[i]] <= f[j] for j in range(P) if j not in H)
+        d2, c2 = O.plan_migration(seq_len, rows_at, q=q, row_bytes=rb, d=4, capacity=cap)
+        assert np.array_equal(dest, d2) and np.array_equal(comb, c2)   # deterministic
+
+
+def test_alg1_capacity_error():
+    with pytest.raises(O.PlanningError):
+        O.plan_migration([10, 10], np.ones((2, 2), np.int64), q=2, row_bytes=1, d=1, capacity=5)

@@ -1,0 +1,235 @@
+/* luffy.h -- C ABI of libluffy: the token-condensed expert-parallel MoE layer of Luffy
+ * (arXiv 2411.15419, "Communication-Efficient Sparsely-Activated Model Training via Sequence Migration
+ * and Token Condensation"), forward and backward, hand-written CUDA for sm_100a (B200).
+ *
+ * Citations: P:n = PAPER.md line n (LaTeX source of the paper).  Readings Rn = DESIGN.md section 2.
+ *
+ * ---------------------------------------------------------------------------------------------------
+ * General conventions
+ *  - Every device pointer is caller-owned (e.g. allocated by PyTorch).  The library never allocates
+ *    device memory after luffy_layer_create; all scratch lives in the caller's workspace.
+ *  - Calls taking `stream` (a cudaStream_t passed as void*) are stream-ordered and asynchronous unless
+ *    marked [sync].  Host pointers are marked (host); all other pointers are device pointers.
+ *  - Row-major, rows 16-byte aligned: d_model % 8 == 0 and d_ffn % 8 == 0 (bf16) / % 4 (fp32).
+ *    Element type of activations/weights = luffy_config.dtype (bf16 or fp32); gate weights, gate
+ *    outputs and weight gradients are fp32.
+ *  - Weights use the nn.Linear layout (out x in): W_g [E, d]; W1, W3 [E_l, f, d]; W2 [E_l, d, f],
+ *    where E_l = E / world local experts on this rank (contiguous placement, R14: expert e lives on
+ *    rank e / E_l).
+ *  - ROW LAYOUT ("slot" space).  Per-row expert buffers are expert-major and every expert segment is
+ *    padded to a multiple of LUFFY_ROW_ALIGN rows; padding rows are zero in every buffer the library
+ *    writes.  On the source side a slot is the padded position of a representative in its send
+ *    layout (expert asc, then token asc, R15).  On the expert side (recv / expert_out) the segment of
+ *    local expert e holds source rank 0's rows, then rank 1's, ... then zero padding.  With world == 1
+ *    the two layouts coincide: recv == send, expert_out == gathered.
+ *  - Errors: arguments are validated on the host before anything is enqueued; on failure a status is
+ *    returned, nothing is launched and luffy_last_error() describes the problem.  CUDA / NCCL failures
+ *    map to LUFFY_E_CUDA / LUFFY_E_NCCL.  Calling out of order returns LUFFY_E_STATE.
+ *  - Determinism: identical inputs give bitwise-identical outputs (no floating-point atomics).
+ *  - Thread-compatibility: one thread at a time per luffy_ctx.
+ * ------------------------------------------------------------------------------------------------- */
+#ifndef LUFFY_H_
+#define LUFFY_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define LUFFY_API __attribute__((visibility("default")))
+#else
+#define LUFFY_API
+#endif
+
+#define LUFFY_ROW_ALIGN 128
+#define LUFFY_MAX_EXPERTS 256
+
+typedef enum {
+  LUFFY_OK = 0,
+  LUFFY_E_INVALID = 1,      /* bad argument (shape, alignment, null pointer, range) */
+  LUFFY_E_CUDA = 2,         /* a CUDA runtime call failed */
+  LUFFY_E_NCCL = 3,         /* an NCCL call failed or NCCL could not be loaded */
+  LUFFY_E_CAPACITY = 4,     /* a receive / migration capacity would be exceeded (checked before any transfer) */
+  LUFFY_E_UNSUPPORTED = 5,  /* configuration not supported by this build (e.g. no sm_100a device) */
+  LUFFY_E_STATE = 6         /* call order violated (e.g. combine before dispatch) */
+} luffy_status;
+
+typedef enum { LUFFY_FP32 = 0, LUFFY_BF16 = 1 } luffy_dtype;
+typedef enum { LUFFY_GELU = 0, LUFFY_SWIGLU = 1 } luffy_act;
+
+typedef struct {
+  int32_t world;          /* ranks of the expert-parallel group (1 = single GPU) */
+  int32_t rank;           /* this rank, 0 <= rank < world */
+  int32_t num_experts;    /* E, E % world == 0, E <= LUFFY_MAX_EXPERTS */
+  int32_t top_k;          /* k, 1 <= k <= E ("top-2 gating") */
+  int32_t d_model;        /* d */
+  int32_t d_ffn;          /* f */
+  int32_t dtype;          /* luffy_dtype of activations and expert weights */
+  int32_t act;            /* luffy_act of the expert FFN (R12) */
+  int32_t renormalize;    /* 1: gate weights renormalized over the k selected experts; 0: raw softmax
+                             probability; -1: default (top_k > 1), R1 */
+  int32_t max_tokens;     /* T capacity per rank */
+  int32_t max_recv_rows;  /* expert-side row capacity incl. padding; 0: world*max_tokens*top_k + E_l*LUFFY_ROW_ALIGN */
+} luffy_config;
+
+typedef struct luffy_ctx luffy_ctx;     /* per rank: config, NCCL communicator, pinned host buffers */
+typedef struct luffy_layer luffy_layer; /* per MoE layer call chain: saved routing/condensation/layout */
+
+typedef struct {
+  int64_t copies;                 /* T * k token copies */
+  int64_t reps;                   /* representatives R (rows that are dispatched and run by experts) */
+  int32_t rounds;                 /* parallel selection rounds used */
+  int32_t reps_per_expert[LUFFY_MAX_EXPERTS];
+  int32_t copies_per_expert[LUFFY_MAX_EXPERTS];
+} luffy_condense_stats;
+
+/* ---- lifetime ---------------------------------------------------------------------------------- */
+
+/* NCCL unique id for world > 1, produced on rank 0 and broadcast by the caller.  [sync] */
+LUFFY_API luffy_status luffy_get_unique_id(uint8_t id[128]);
+
+/* Validates cfg, selects the current CUDA device, and (world > 1) creates the NCCL communicator with
+ * ncclCommInitRank(world, id, rank).  `nccl_id` (host, 128 bytes) may be NULL when world == 1.  [sync] */
+LUFFY_API luffy_status luffy_create(const luffy_config* cfg, const uint8_t* nccl_id, luffy_ctx** out);
+LUFFY_API void luffy_destroy(luffy_ctx* ctx);
+
+/* Bytes of device workspace one layer needs (saved state + scratch), a function of cfg only. */
+LUFFY_API size_t luffy_layer_workspace_bytes(const luffy_config* cfg);
+
+/* Binds a layer to `dev_workspace` (device, >= luffy_layer_workspace_bytes, 256-byte aligned). */
+LUFFY_API luffy_status luffy_layer_create(luffy_ctx* ctx, void* dev_workspace, size_t bytes, luffy_layer** out);
+LUFFY_API void luffy_layer_destroy(luffy_layer* layer);
+
+/* Thread-local description of the last failure. */
+LUFFY_API const char* luffy_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process (for the bench's gpu_launches). */
+LUFFY_API int64_t luffy_launch_count(void);
+
+/* Padded row counts after the forward calls (host, valid after luffy_dispatch returned):
+ * send_rows = padded rows of this rank's send layout; recv_rows = padded rows of its expert layout. */
+LUFFY_API luffy_status luffy_layer_rows(const luffy_layer* layer, int64_t* send_rows, int64_t* recv_rows);
+
+/* ---- forward (P:256-259 workflow: gate -> condensation -> dispatch -> experts -> combine) -------- */
+
+/* Top-k gate, P:152/P:434 and R1/R2.  x [T, d] (dtype), w_gate [E, d] fp32.
+ * logits = x W_g^T in fp32 with a fixed summation order; experts ordered by (logit desc, id asc);
+ * topk_w = renormalized softmax over the k selected logits, or the softmax probability (R1).
+ * Outputs topk_idx [T, k] int32 and topk_w [T, k] fp32 (device); the layer keeps copies for backward.
+ * Starts a new forward on the layer.  0 < T <= max_tokens. */
+LUFFY_API luffy_status luffy_route(luffy_layer* layer, const void* x, const float* w_gate, int32_t T,
+                         int32_t* topk_idx, float* topk_w, void* stream);
+
+/* Token condensation, P:358 (group = tokens routed to the same expert), P:373 (cosine similarity of the
+ * remaining pairs), P:378 (threshold, then keep the highest-degree token and condense its neighbours,
+ * repeat), P:405 (token_to_token map).  Normalized cosine s = (1 + cos)/2 (R4); edge iff s >= h;
+ * zero vectors have no edges (R7); greedy on the dynamic residual degree with ties to the lowest token
+ * (R8), computed exactly by parallel 2-hop rounds.  h > 1 disables condensation (identity map).
+ * Output rep [T, k] int32: the token whose copy represents copy (t, j) in expert topk_idx[t, j]
+ * (rep[rep] == rep).  `stats` (host, nullable) is filled synchronously when non-NULL ([sync] then). */
+LUFFY_API luffy_status luffy_condense(luffy_layer* layer, const void* x, float h, int32_t* rep,
+                            luffy_condense_stats* stats, void* stream);
+
+/* Dispatch phase: packs only the representatives into the send layout and, for
+ * world > 1, exchanges counts (ncclAllGather) and rows (grouped ncclSend/ncclRecv) so that `recv`
+ * [max_recv_rows, d] holds this rank's local-expert rows in the expert layout.  world == 1: `recv`
+ * receives the packed rows directly (no communication).  *recv_rows (host) = padded rows written.
+ * [sync] for world > 1 (the all-gathered counts are copied to the host to post the receives).
+ * LUFFY_E_CAPACITY if the padded rows exceed max_recv_rows (checked before any transfer). */
+LUFFY_API luffy_status luffy_dispatch(luffy_layer* layer, const void* x, void* recv, int64_t* recv_rows, void* stream);
+
+/* Expert FFN ("expert networks that are essentially FFNs"; R12):
+ * GELU:   pre = recv W1_e^T, act = GeLU_erf(pre), out = act W2_e^T;
+ * SWIGLU: pre = [recv W1_e^T | recv W3_e^T] (saved_pre is [rows, 2f]), act = silu(pre1) * pre3.
+ * bf16: tcgen05 grouped GEMMs, fp32 accumulation, bf16 outputs.  fp32: SIMT FFMA.
+ * saved_pre [rows, f or 2f] and saved_act [rows, f] are written for the backward. w3 NULL for GELU. */
+LUFFY_API luffy_status luffy_expert_ffn(luffy_layer* layer, const void* recv, const void* w1, const void* w2,
+                              const void* w3, void* out, void* saved_pre, void* saved_act, void* stream);
+
+/* Combine phase: returns expert outputs to the source ranks so that `gathered` [send rows, d]
+ * is in this rank's send layout.  world == 1: gathered may alias expert_out (no-op) or is a copy. */
+LUFFY_API luffy_status luffy_combine(luffy_layer* layer, const void* expert_out, void* gathered, void* stream);
+
+/* Output reuse, "use the expert output of token j to replace it" (R10):
+ * y[t] = sum_j topk_w[t, j] * gathered[slot of rep(t, j)], fp32 accumulation, y [T, d] (dtype). */
+LUFFY_API luffy_status luffy_uncondense(luffy_layer* layer, const void* gathered, void* y, void* stream);
+
+/* ---- backward: exact autograd of the forward with routing and rep as constants (R11) ------------- */
+
+/* d_gathered[slot] = sum over copies (t, j) represented by the slot (token order) of w[t,j] * dy[t];
+ * padding slots are zeroed.  d_topk_w [T, k] fp32 = <dy[t], gathered[slot(t, j)]>. */
+LUFFY_API luffy_status luffy_uncondense_bwd(luffy_layer* layer, const void* dy, const void* gathered,
+                                  void* d_gathered, float* d_topk_w, void* stream);
+
+/* Mirror of luffy_combine: d_expert_out (expert layout) <- d_gathered (send layout). */
+LUFFY_API luffy_status luffy_combine_bwd(luffy_layer* layer, const void* d_gathered, void* d_expert_out, void* stream);
+
+/* FFN backward: d_act = d_out W2; d_pre = d_act * act'(pre); d_recv = d_pre W1 (+ d_pre3 W3);
+ * dw2 = d_out^T act; dw1 = d_pre^T recv (dw3 = d_pre3^T recv).  dw* fp32, overwritten.
+ * `scratch_dpre` [rows, f or 2f] (dtype) receives d_pre.  dw3 / w3 NULL for GELU. */
+LUFFY_API luffy_status luffy_expert_ffn_bwd(luffy_layer* layer, const void* d_out, const void* recv, const void* w1,
+                                  const void* w2, const void* w3, const void* saved_pre,
+                                  const void* saved_act, void* scratch_dpre, void* d_recv,
+                                  float* dw1, float* dw2, float* dw3, void* stream);
+
+/* Mirror of luffy_dispatch: d_send (send layout, internal for world > 1) <- d_recv (expert layout),
+ * then dx[t] = sum over j with rep(t, j) == t of d_send[slot(t, j)] (dx overwritten, dtype). */
+LUFFY_API luffy_status luffy_dispatch_bwd(luffy_layer* layer, const void* d_recv, void* dx, void* stream);
+
+/* Gate backward: renormalized: dl_j = w_j (dw_j - sum_i w_i dw_i) on the top-k; raw softmax:
+ * dl = p * (g - <p, g>); dw_gate [E, d] fp32 = dl^T x (overwritten); dx += dl W_g (accumulated). */
+LUFFY_API luffy_status luffy_route_bwd(luffy_layer* layer, const void* x, const float* w_gate, const float* d_topk_w,
+                             void* dx, float* dw_gate, void* stream);
+
+/* ---- debug export (tests) ----------------------------------------------------------------------- */
+
+typedef enum {
+  LUFFY_DBG_GCNT = 0,      /* int32 [E]     copies per expert group */
+  LUFFY_DBG_GOFF = 1,      /* int32 [E+1]   padded group-row offsets */
+  LUFFY_DBG_GTOK = 2,      /* int32 [goff[E]] token of each group row (-1 padding) */
+  LUFFY_DBG_ADJOFF = 3,    /* int64 [E+1]   word offsets of the group adjacency bit matrices */
+  LUFFY_DBG_ADJ = 4,       /* uint32 [adjoff[E]] adjacency bits (row r of group e: adjoff[e] + r * npad_e/32) */
+  LUFFY_DBG_REP_LOCAL = 5, /* int32 [goff[E]] group row of each row's representative */
+  LUFFY_DBG_SOFF = 6,      /* int32 [E+1]   padded send offsets */
+  LUFFY_DBG_PERM = 7,      /* int32 [soff[E]] slot -> token (-1 padding) */
+  LUFFY_DBG_POS = 8,       /* int32 [T, k]  slot of the representative of copy (t, j) */
+  LUFFY_DBG_NREP = 9,      /* int32 [E]     representatives per expert */
+  LUFFY_DBG_ROUNDS = 10    /* uint32 [1]    greedy rounds of the last condense */
+} luffy_debug_item;
+
+/* Synchronously copies an internal array of the layer's current forward to host memory `dst` (host).
+ * *bytes (in: capacity of dst, out: bytes of the item).  [sync] */
+LUFFY_API luffy_status luffy_debug_copy(luffy_layer* layer, int32_t item, void* dst, size_t* bytes, void* stream);
+
+/* ---- sequence migration placement (CPU, host memory, synchronous, reentrant, deterministic) ------ */
+
+typedef struct {
+  int32_t num_seqs;          /* S */
+  int32_t num_ranks;         /* P */
+  int32_t q;                 /* candidate-set size, Alg. 1 line 2 */
+  int32_t objective;         /* 0: minimum cost growth (default, R16); 1: maximum as printed */
+  const int32_t* seq_len;    /* [S] sequence lengths l_i */
+  const int64_t* rows_at;    /* [S][P] expert-output rows of sequence i located on rank j */
+  int64_t row_bytes;         /* bytes per row (d * sizeof(dtype)) */
+  int64_t capacity_tokens;   /* per-rank token capacity; <= 0: max(ceil(1.5*sum(l)/P), max l) */
+  int64_t d_model;           /* d of Eq. (1) */
+} luffy_migration_problem;
+
+/* Alg. 1 with Eq. (1) in exact int64 arithmetic (P := 1, R16): f_ij = row_bytes *
+ * (rows_i - rows_at[i][j]); H_i = q ranks of least f (ties -> lower rank); sequences by length desc
+ * (ties -> id asc) go to the capacity-feasible j in H_i of least s_ij = T_att(B_j+1, max(L_j, l_i)) -
+ * T_att(B_j, L_j) (ties -> smaller f, then lower rank), else to any feasible rank by the same key,
+ * else LUFFY_E_CAPACITY.  seq_dest [S] (host) receives the ranks; combine_bytes [P][P] (host, nullable)
+ * the predicted combine traffic from rank r to rank dest. */
+LUFFY_API luffy_status luffy_plan_migration(const luffy_migration_problem* prob, int32_t* seq_dest, int64_t* combine_bytes);
+
+/* Eq. (1): 3*B*L*d^2 + 2*B*L^2*d (P := 1), exact int64. */
+LUFFY_API int64_t luffy_attention_cost(int64_t B, int64_t L, int64_t d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LUFFY_H_ */

@@ -103,6 +103,24 @@ def route(X: np.ndarray, Wg: np.ndarray, k: int, renormalize: bool, tie_tol: flo
     return Routing(logits, probs, idx, w, near_tie)
 
 
+def route_with_idx(X: np.ndarray, Wg: np.ndarray, idx: np.ndarray, renormalize: bool) -> Routing:
+    """The gate of `route` with the expert selection `idx` given (the GPU's choice on near-tie tokens,
+    reading R2): same logits, softmax and weight formulas."""
+    X = np.asarray(X, np.float64)
+    logits = X @ np.asarray(Wg, np.float64).T
+    m = logits.max(axis=1, keepdims=True)
+    ex = np.exp(logits - m)
+    probs = ex / ex.sum(axis=1, keepdims=True)
+    idx = np.asarray(idx, np.int64)
+    sel = np.take_along_axis(logits, idx, axis=1)
+    if renormalize:
+        es = np.exp(sel - sel.max(axis=1, keepdims=True))
+        w = es / es.sum(axis=1, keepdims=True)
+    else:
+        w = np.take_along_axis(probs, idx, axis=1)
+    return Routing(logits, probs, idx, w, np.zeros(X.shape[0], bool))
+
+
 # ----------------------------------------------------------------------------------------------
 # Steps 2-3: groups, normalized cosine similarity, threshold graph (P:224, P:358, P:373, P:378)
 # ----------------------------------------------------------------------------------------------

@@ -1,0 +1,481 @@
+// Token condensation (token_to_token map P:405).
+//
+//  1. group_build: fast-similarity step 1 -- only copies routed to the same expert are compared.
+//     Group e = copies (t, j) with idx[t, j] == e in ascending token order (R6), laid out in a padded
+//     expert-major row space (segments of LUFFY_ROW_ALIGN rows).
+//  2. gather_norm: the group rows (xg) and their fp64 norms.
+//  3. gram: step 3 -- G = Xg Xg^T on upper-triangle tiles; the epilogue applies the threshold
+//     (R4): edge(i, j) iff G_ij >= (2h - 1) |x_i| |x_j|, i != j, both norms > 0 (R7), and packs
+//     the bits of (i, j) and (j, i) so the graph is symmetric by construction.  (bf16: tcgen05 kernel in
+//     gram_tc.cu; fp32: the SIMT tile kernel below, exact fp32 FFMA.)
+//  4. greedy: "keep the token with the highest degree ... condense its neighbouring tokens ... repeat"
+//      with the dynamic residual degree and lowest-index ties (R8), computed EXACTLY by parallel
+//     2-hop rounds: an alive node whose (degree, -index) is the strict maximum of its alive 2-hop ball
+//     is selected together with all its alive neighbours; such winners are >= 3 hops apart, so their
+//     claims are disjoint and commute with the sequential greedy.  One cooperative
+//     kernel, grid-wide barriers between the phases of a round.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace luffy {
+namespace {
+
+// Block-wide exclusive scan of one flag per thread (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ int block_scan_flag(bool flag, int* warp_sums, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned b = __ballot_sync(0xffffffffu, flag);
+  int pre = __popc(b & ((1u << lane) - 1u));
+  if (lane == 0) warp_sums[wid] = __popc(b);
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < nw ? warp_sums[lane] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane < nw) warp_sums[lane] = inc - v;
+    if (lane == 31) warp_sums[32] = inc;
+  }
+  __syncthreads();
+  pre += warp_sums[wid];
+  total = warp_sums[32];
+  __syncthreads();
+  return pre;
+}
+
+__global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                                           int T, int k, int E, int32_t* __restrict__ gcnt,
+                                                           int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
+                                                           float* __restrict__ gw, int32_t* __restrict__ gloc) {
+  __shared__ int cnt[LUFFY_MAX_EXPERTS];
+  __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int warp_sums[33];
+  const int e = blockIdx.x;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * k; i += blockDim.x) atomicAdd(&cnt[idx[i]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    offs[0] = 0;
+    for (int g = 0; g < E; ++g) offs[g + 1] = offs[g] + (cnt[g] + kRowAlign - 1) / kRowAlign * kRowAlign;
+  }
+  __syncthreads();
+  if (e == 0) {
+    for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+      goff[i] = offs[i];
+      if (i < E) gcnt[i] = cnt[i];
+    }
+  }
+  int base = offs[e];
+  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    int jj = -1;
+    if (t < T)
+      for (int j = 0; j < k; ++j)
+        if (idx[(size_t)t * k + j] == e) jj = j;
+    int total;
+    int pre = block_scan_flag(jj >= 0, warp_sums, total);
+    if (jj >= 0) {
+      const int g = base + pre;
+      gtok[g] = t;
+      gw[g] = w[(size_t)t * k + jj];
+      gloc[(size_t)t * k + jj] = g;
+    }
+    base += total;
+  }
+  for (int g = offs[e] + cnt[e] + threadIdx.x; g < offs[e + 1]; g += blockDim.x) {
+    gtok[g] = -1;
+    gw[g] = 0.f;
+  }
+}
+
+// xg[g] = x[gtok[g]] (zero for padding), gnorm[g] = |x| in fp64.  One warp per padded row.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_norm_kernel(const T* __restrict__ x, const int32_t* __restrict__ gtok,
+                                                          const int32_t* __restrict__ goff, int E, int d,
+                                                          T* __restrict__ xg, double* __restrict__ gnorm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = goff[E];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < rows; g += nw) {
+    const int t = gtok[g];
+    T* dst = xg + g * d;
+    double ss = 0.0;
+    if (t < 0) {
+      for (int c = lane * 8; c < d; c += 256) zero8(dst + c);
+    } else {
+      const T* src = x + (size_t)t * d;
+      for (int c = lane * 8; c < d; c += 256) {
+        if constexpr (sizeof(T) == 2) {
+          uint4 u = *reinterpret_cast<const uint4*>(src + c);
+          *reinterpret_cast<uint4*>(dst + c) = u;
+        } else {
+          *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+          *reinterpret_cast<float4*>(dst + c + 4) = *reinterpret_cast<const float4*>(src + c + 4);
+        }
+        float v[8];
+        load8(src + c, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss += (double)v[i] * (double)v[i];
+      }
+    }
+    ss = warp_sum_d(ss);
+    if (lane == 0) gnorm[g] = sqrt(ss);
+  }
+}
+
+// Decode a linear upper-triangle tile id into (group, I, J), J >= I, for tiles of `TS` rows.
+__device__ __forceinline__ bool decode_tri_tile(int64_t id, const int32_t* goff_s, int E, int TS, int& e, int& I, int& J) {
+  for (e = 0; e < E; ++e) {
+    const int nt = (goff_s[e + 1] - goff_s[e]) / TS;
+    const int64_t pairs = (int64_t)nt * (nt + 1) / 2;
+    if (id < pairs) {
+      // row I holds tiles J = I..nt-1; find I
+      int i = 0;
+      int64_t rem = id;
+      while (rem >= nt - i) { rem -= nt - i; ++i; }
+      I = i;
+      J = i + (int)rem;
+      return true;
+    }
+    id -= pairs;
+  }
+  return false;
+}
+
+// SIMT Gram + threshold + bit pack, fp32 FFMA (the fp32 path; also usable for bf16 inputs).
+// 64x64 tiles, 256 threads, 4x4 outputs per thread, K staged through shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg, const double* __restrict__ gnorm,
+                                                        const int32_t* __restrict__ goff, const int32_t* __restrict__ gcnt,
+                                                        const int64_t* __restrict__ adjoff, int E, int d, double c2h,
+                                                        uint32_t* __restrict__ adj) {
+  constexpr int TS = 64, BK = 32;
+  __shared__ float As[BK][TS + 4];
+  __shared__ float Bs[BK][TS + 4];
+  __shared__ unsigned char edge[TS][TS + 4];
+  __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) goff_s[i] = goff[i];
+  __syncthreads();
+  int e, I, J;
+  if (!decode_tri_tile(blockIdx.x, goff_s, E, TS, e, I, J)) return;
+  const int n = gcnt[e];
+  const int npad = goff_s[e + 1] - goff_s[e];
+  const int W = npad / 32;
+  const T* A = xg + (size_t)(goff_s[e] + I * TS) * d;
+  const T* B = xg + (size_t)(goff_s[e] + J * TS) * d;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < d; k0 += BK) {
+    // load 64 rows x 32 k of A and B (transposed into [k][row])
+    for (int i = threadIdx.x; i < TS * BK; i += blockDim.x) {
+      const int r = i / BK, kk = i % BK;
+      As[kk][r] = to_f(A[(size_t)r * d + k0 + kk]);
+      Bs[kk][r] = to_f(B[(size_t)r * d + k0 + kk]);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int li = I * TS + ty * 4 + i;
+    const double ni = gnorm[goff_s[e] + li];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int lj = J * TS + tx * 4 + j;
+      const double nj = gnorm[goff_s[e] + lj];
+      bool on = li < n && lj < n && li != lj && ni > 0.0 && nj > 0.0 && (double)acc[i][j] >= c2h * ni * nj;
+      edge[ty * 4 + i][tx * 4 + j] = on;
+    }
+  }
+  __syncthreads();
+  uint32_t* base = adj + adjoff[e];
+  const int t = threadIdx.x;
+  if (I < J) {
+    if (t < 128) {  // direct words: row I*64 + r, word J*2 + h
+      const int r = t >> 1, h = t & 1;
+      uint32_t word = 0;
+      for (int b = 0; b < 32; ++b) word |= (uint32_t)edge[r][h * 32 + b] << b;
+      base[(size_t)(I * TS + r) * W + J * 2 + h] = word;
+    } else {        // transposed words: row J*64 + c, word I*2 + h
+      const int c = (t - 128) >> 1, h = (t - 128) & 1;
+      uint32_t word = 0;
+      for (int b = 0; b < 32; ++b) word |= (uint32_t)edge[h * 32 + b][c] << b;
+      base[(size_t)(J * TS + c) * W + I * 2 + h] = word;
+    }
+  } else if (t < 128) {  // diagonal tile: bit (r, c) = c > r ? edge[r][c] : c < r ? edge[c][r] : 0
+    const int r = t >> 1, h = t & 1;
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int c = h * 32 + b;
+      const unsigned char v = c > r ? edge[r][c] : (c < r ? edge[c][r] : 0);
+      word |= (uint32_t)v << b;
+    }
+    base[(size_t)(I * TS + r) * W + I * 2 + h] = word;
+  }
+}
+
+// Word offsets of each group's adjacency: sum over groups of npad^2 / 32.
+__global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t o = 0;
+    for (int e = 0; e < E; ++e) {
+      adjoff[e] = o;
+      const int64_t np = goff[e + 1] - goff[e];
+      o += np * np / 32;
+    }
+    adjoff[E] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Greedy representative selection by exact parallel 2-hop rounds (cooperative launch).
+
+__device__ __forceinline__ void grid_barrier(uint32_t* ctrl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* vgen = ctrl + 1;
+    const uint32_t gen = *vgen;
+    __threadfence();
+    const uint32_t arrived = atomicAdd(ctrl, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(ctrl, 0u);
+      __threadfence();
+      atomicAdd(ctrl + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+struct GreedyArgs {
+  int E;
+  const int32_t* goff;
+  const int32_t* gcnt;
+  const int64_t* adjoff;
+  const uint32_t* adj;
+  uint32_t* alive;
+  uint32_t* win;
+  unsigned long long* key;
+  unsigned long long* m1;
+  int32_t* rep_local;
+  uint32_t* ctrl;
+  int max_rounds;
+};
+
+__global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
+  __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int64_t adjoff_s[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
+  const int E = a.E;
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+    goff_s[i] = a.goff[i];
+    adjoff_s[i] = a.adjoff[i];
+    if (i < E) gcnt_s[i] = a.gcnt[i];
+  }
+  __syncthreads();
+  const int rows = goff_s[E];
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int gwarp = (int)(gtid >> 5);
+  const int nwarps = (int)(nthreads >> 5);
+
+  for (int64_t wd = gtid; wd < rows / 32; wd += nthreads) {
+    const int r0 = (int)wd * 32;
+    const int g = find_group(goff_s, E, r0);
+    const int valid = gcnt_s[g] - (r0 - goff_s[g]);
+    a.alive[wd] = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
+    a.win[wd] = 0u;
+  }
+  for (int64_t r = gtid; r < rows; r += nthreads) a.rep_local[r] = -1;
+  grid_barrier(a.ctrl);
+
+  int round = 0;
+  for (;; ++round) {
+    // ---- phase A: residual degree -> priority key (deg, -index)
+    for (int r = gwarp; r < rows; r += nwarps) {
+      const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
+      if (!alive) {
+        if (lane == 0) a.key[r] = 0ull;
+        continue;
+      }
+      const int g = find_group(goff_s, E, r);
+      const int rl = r - goff_s[g];
+      const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
+      const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
+      const uint32_t* al = a.alive + (goff_s[g] >> 5);
+      int deg = 0;
+      for (int wd = lane; wd < W; wd += 32) deg += __popc(row[wd] & __ldcg(al + wd));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+      if (lane == 0) a.key[r] = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)rl);
+    }
+    grid_barrier(a.ctrl);
+    // ---- phase B: m1 = max key over the alive closed neighbourhood;  phase C: m2 from m1
+    for (int ph = 0; ph < 2; ++ph) {
+      const unsigned long long* src = ph == 0 ? a.key : a.m1;
+      for (int r = gwarp; r < rows; r += nwarps) {
+        const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
+        if (!alive) continue;
+        const int g = find_group(goff_s, E, r);
+        const int rl = r - goff_s[g];
+        const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
+        const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
+        const uint32_t* al = a.alive + (goff_s[g] >> 5);
+        unsigned long long m = __ldcg(src + r);
+        for (int wd = lane; wd < W; wd += 32) {
+          uint32_t bits = row[wd] & __ldcg(al + wd);
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const unsigned long long v = __ldcg(src + goff_s[g] + wd * 32 + b);
+            m = v > m ? v : m;
+          }
+        }
+        m = warp_max_u64(m);
+        if (lane == 0) {
+          if (ph == 0) a.m1[r] = m;
+          else if (m == __ldcg(a.key + r)) atomicOr(a.win + (r >> 5), 1u << (r & 31));
+        }
+      }
+      grid_barrier(a.ctrl);
+    }
+    // ---- phase D: winners and their alive neighbours leave; count the survivors
+    for (int r = gwarp; r < rows; r += nwarps) {
+      const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
+      if (!alive) continue;
+      const int g = find_group(goff_s, E, r);
+      const bool winner = (__ldcg(a.win + (r >> 5)) >> (r & 31)) & 1u;
+      int owner = -1;
+      if (winner) {
+        owner = r;
+      } else {
+        const int rl = r - goff_s[g];
+        const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
+        const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
+        const uint32_t* wn = a.win + (goff_s[g] >> 5);
+        int found = 0x7fffffff;
+        for (int wd = lane; wd < W; wd += 32) {
+          const uint32_t bits = row[wd] & __ldcg(wn + wd);
+          if (bits) found = min(found, goff_s[g] + wd * 32 + __ffs(bits) - 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
+        if (found != 0x7fffffff) owner = found;
+      }
+      if (lane == 0) {
+        if (owner >= 0) {
+          a.rep_local[r] = owner;
+          atomicAnd(a.alive + (r >> 5), ~(1u << (r & 31)));
+        } else {
+          atomicAdd(a.ctrl + 64 + round, 1u);
+        }
+      }
+    }
+    grid_barrier(a.ctrl);
+    const uint32_t left = __ldcg(a.ctrl + 64 + round);
+    if (left == 0u || round + 1 >= a.max_rounds) break;
+    for (int64_t wd = gtid; wd < rows / 32; wd += nthreads) a.win[wd] = 0u;
+    // (win words are next written in phase C, two barriers later)
+  }
+  if (gtid == 0) a.ctrl[2] = (uint32_t)(round + 1);
+}
+
+// h > 1: no edges -- every copy represents itself.
+__global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int32_t* __restrict__ gtok, int E,
+                                    int32_t* __restrict__ rep_local, uint32_t* __restrict__ ctrl) {
+  const int rows = goff[E];
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    rep_local[r] = gtok[r] >= 0 ? (int32_t)r : -1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[2] = 0u;
+}
+
+}  // namespace
+
+int launch_group_build(luffy_layer* L, const void* x, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  group_build_kernel<<<L->E, 1024, 0, st>>>(L->idx, L->w, L->T, L->k, L->E, L->gcnt, L->goff, L->gtok,
+                                            L->gw, L->gloc);
+  LUFFY_LAUNCHED();
+  int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);
+  if (L->dtype == LUFFY_BF16)
+    gather_norm_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->gtok, L->goff, L->E, L->d,
+                                                     static_cast<bf16*>(L->xg), L->gnorm);
+  else
+    gather_norm_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->gtok, L->goff, L->E, L->d,
+                                                      static_cast<float*>(L->xg), L->gnorm);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+int launch_identity_rep(luffy_layer* L, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  identity_rep_kernel<<<148, 256, 0, st>>>(L->goff, L->gtok, L->E, L->rep_local, L->ctrl);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+int launch_gram_simt(luffy_layer* L, float h, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  adj_offsets_kernel<<<1, 32, 0, st>>>(L->goff, L->E, L->adjoff);
+  LUFFY_LAUNCHED();
+  const int64_t nt = L->Cpad_max / 64;
+  const int64_t tiles = nt * (nt + 1) / 2;  // upper bound over any split of the rows into groups
+  const double c2h = 2.0 * (double)h - 1.0;
+  if (L->dtype == LUFFY_BF16)
+    gram_simt_kernel<bf16><<<(unsigned)tiles, 256, 0, st>>>(static_cast<const bf16*>(L->xg), L->gnorm, L->goff, L->gcnt,
+                                                            L->adjoff, L->E, L->d, c2h, L->adj);
+  else
+    gram_simt_kernel<float><<<(unsigned)tiles, 256, 0, st>>>(static_cast<const float*>(L->xg), L->gnorm, L->goff, L->gcnt,
+                                                             L->adjoff, L->E, L->d, c2h, L->adj);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+int launch_greedy(luffy_layer* L, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * (64 + kGreedyMaxRounds), st));
+  static int blocks = 0;
+  if (blocks == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    LUFFY_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, greedy_kernel, 256, 0));
+    LUFFY_CUDA_TRY(cudaGetDevice(&dev));
+    LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    blocks = std::max(1, std::min(per_sm, 4)) * sms;
+  }
+  GreedyArgs a;
+  a.E = L->E;
+  a.goff = L->goff;
+  a.gcnt = L->gcnt;
+  a.adjoff = L->adjoff;
+  a.adj = L->adj;
+  a.alive = L->alive;
+  a.win = L->win;
+  a.key = reinterpret_cast<unsigned long long*>(L->key);
+  a.m1 = reinterpret_cast<unsigned long long*>(L->m1);
+  a.rep_local = L->rep_local;
+  a.ctrl = L->ctrl;
+  a.max_rounds = kGreedyMaxRounds;
+  void* args[] = {&a};
+  LUFFY_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)greedy_kernel, dim3(blocks), dim3(256), args, 0, st));
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+}  // namespace luffy

@@ -1,0 +1,94 @@
+// Internal declarations of libluffy (not part of the C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "luffy.h"
+
+namespace luffy {
+
+luffy_status fail(luffy_status st, const std::string& msg);
+void note_launch(int n = 1);
+
+constexpr int kRowAlign = LUFFY_ROW_ALIGN;
+constexpr int kGreedyMaxRounds = 1 << 14;
+constexpr int kWgParts = 16;  // token slices of the deterministic dW_g reduction
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace luffy
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#endif
+
+// Layer state: pointers into the caller's workspace (device) plus host-side bookkeeping.
+struct luffy_layer {
+  struct luffy_ctx* ctx;
+  // ---- config copies
+  int P, rank, E, El, k, d, f, dtype, act, renorm, Tmax;
+  int64_t C_max, Cpad_max, Rpad_max, recv_max, adj_words_max;
+  // ---- routing (saved for backward)
+  float* probs;       // [Tmax, E]
+  int32_t* idx;       // [Tmax, k]
+  float* w;           // [Tmax, k]
+  // ---- groups (one per expert; source rank = this rank)
+  int32_t* gcnt;      // [E] copies per expert
+  int32_t* goff;      // [E+1] padded group-row offsets
+  int32_t* gtok;      // [Cpad_max] token of each group row (-1 = padding)
+  int32_t* gloc;      // [Tmax, k] group row (global, padded space) of copy (t, j)
+  float* gw;          // [Cpad_max] gate weight of each group row (0 for padding)
+  void* xg;           // [Cpad_max, d] gathered group rows (dtype)
+  double* gnorm;      // [Cpad_max] |x| in fp64
+  int64_t* adjoff;    // [E+1] word offsets of each group's bit adjacency
+  uint32_t* adj;      // adjacency bits, group e: rows of W_e = goff-span/32 words
+  int32_t* rep_local; // [Cpad_max] group row of the representative
+  uint64_t* key;      // [Cpad_max] greedy priorities
+  uint64_t* m1;       // [Cpad_max]
+  uint32_t* alive;    // [Cpad_max/32]
+  uint32_t* win;      // [Cpad_max/32]
+  uint32_t* ctrl;     // [64 + kGreedyMaxRounds] grid barrier + per-round counters
+  // ---- pack / layout
+  int32_t* nrep;      // [E] representatives per expert
+  int32_t* soff;      // [E+1] padded send offsets
+  int32_t* lslot;     // [Cpad_max] slot of a group row that is a representative (-1 otherwise)
+  int32_t* perm;      // [Rpad_max] slot -> token (-1 = padding)
+  int32_t* slot_gl;   // [Rpad_max] slot -> group row (-1 = padding)
+  int32_t* pos;       // [Tmax, k] slot of the representative of copy (t, j)
+  int32_t* rep;       // [Tmax, k] representative token of copy (t, j)
+  int32_t* roff;      // [El+1] padded expert-side row offsets (device)
+  int32_t* cnt_all;   // [P, E] all-gathered representative counts (device)
+  void* send;         // [Rpad_max, d] send buffer (world > 1); reused as d_send in backward
+  // ---- backward scratch
+  float* dl;          // [Tmax, E] gate logit gradients
+  float* wg_part;     // [kWgParts, E, d]
+  // ---- host-side state
+  int T;
+  float h;
+  bool has_adj;
+  int stage;          // 0 none, 1 routed, 2 condensed, 3 dispatched, 4 ffn, 5 combined, 6 uncondensed
+  int64_t send_rows_h, recv_rows_h;
+  int32_t* cnt_all_h;  // pinned [P*E]
+  int32_t* roff_h;     // pinned [El+1]
+  int32_t* soff_h;     // pinned [E+1] (world > 1)
+};
+
+// ---- kernel launchers (defined in the .cu files); all enqueue on `s` and return cudaError_t as int
+namespace luffy {
+struct Ctx;
+int launch_route(const luffy_layer* L, const void* x, const float* wg, int32_t* idx_out, float* w_out, void* s);
+int launch_group_build(luffy_layer* L, const void* x, void* s);
+int launch_identity_rep(luffy_layer* L, void* s);
+int launch_gram_simt(luffy_layer* L, float h, void* s);
+int launch_gram_tc(luffy_layer* L, float h, void* s);
+int launch_greedy(luffy_layer* L, void* s);
+int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out, void* s);
+int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void* s);
+int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gathered, void* dg, float* dw, void* s);
+int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s);
+int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s);
+
+// Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).
+enum Epi { EPI_STORE = 0, EPI_GELU = 1, EPI_SWIGLU = 2, EPI_DGELU = 3, EPI_DSWIGLU = 4 };
+}  // namespace luffy

@@ -1,0 +1,104 @@
+"""Token-condensed expert-parallel MoE layer driven through the libluffy C ABI.
+
+This class is plumbing: it allocates device buffers with PyTorch and calls the C-ABI entry points in the
+paper's order: route -> condense -> dispatch -> expert FFN -> combine -> uncondense, and the
+backward in reverse.  Every arithmetic step runs in libluffy's CUDA kernels.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import luffy as L
+
+_TORCH_DT = {L.BF16: torch.bfloat16, L.FP32: torch.float32}
+
+
+class CondensedMoELayer:
+    def __init__(self, num_experts: int, top_k: int, d_model: int, d_ffn: int, max_tokens: int,
+                 dtype: str = "bf16", act: str = "gelu", world: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None, renormalize: int = -1, max_recv_rows: int = 0,
+                 device: torch.device | str = "cuda"):
+        self.device = torch.device(device)
+        self.dt = L.BF16 if dtype == "bf16" else L.FP32
+        self.tdt = _TORCH_DT[self.dt]
+        self.act = L.SWIGLU if act == "swiglu" else L.GELU
+        self.E, self.k, self.d, self.f, self.Tmax = num_experts, top_k, d_model, d_ffn, max_tokens
+        self.world, self.rank = world, rank
+        self.El = num_experts // world
+        self.cfg = L.make_config(world, rank, num_experts, top_k, d_model, d_ffn, self.dt, self.act, renormalize,
+                                 max_tokens, max_recv_rows)
+        self.ctx = L.luffy_create(self.cfg, nccl_id)
+        nbytes = L.luffy_layer_workspace_bytes(self.cfg)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.layer = L.luffy_layer_create(self.ctx, self.ws, nbytes)
+        C = max_tokens * top_k
+        self.send_rows = C + num_experts * L.ROW_ALIGN
+        self.recv_rows = max_recv_rows if max_recv_rows > 0 else world * C + self.El * L.ROW_ALIGN
+        if world == 1:
+            self.recv_rows = max(self.recv_rows, self.send_rows)
+        pre_cols = 2 * d_ffn if self.act == L.SWIGLU else d_ffn
+        dev, tdt = self.device, self.tdt
+        self.idx = torch.empty(max_tokens, top_k, dtype=torch.int32, device=dev)
+        self.w = torch.empty(max_tokens, top_k, dtype=torch.float32, device=dev)
+        self.rep = torch.empty(max_tokens, top_k, dtype=torch.int32, device=dev)
+        self.recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.pre = torch.empty(self.recv_rows, pre_cols, dtype=tdt, device=dev)
+        self.act_buf = torch.empty(self.recv_rows, d_ffn, dtype=tdt, device=dev)
+        self.out = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.gathered = self.out if world == 1 else torch.empty(self.send_rows, d_model, dtype=tdt, device=dev)
+        self.y = torch.empty(max_tokens, d_model, dtype=tdt, device=dev)
+        # backward buffers
+        self.d_gathered = torch.empty(self.send_rows if world > 1 else self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.d_out = self.d_gathered if world == 1 else torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.dpre = torch.empty(self.recv_rows, pre_cols, dtype=tdt, device=dev)
+        self.d_recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.dx = torch.empty(max_tokens, d_model, dtype=tdt, device=dev)
+        self.dw = torch.empty(max_tokens, top_k, dtype=torch.float32, device=dev)
+        self.dw1 = torch.empty(self.El, d_ffn, d_model, dtype=torch.float32, device=dev)
+        self.dw2 = torch.empty(self.El, d_model, d_ffn, dtype=torch.float32, device=dev)
+        self.dw3 = torch.empty(self.El, d_ffn, d_model, dtype=torch.float32, device=dev) if self.act == L.SWIGLU else None
+        self.dwg = torch.empty(num_experts, d_model, dtype=torch.float32, device=dev)
+        self.T = 0
+        self.stats = None
+
+    def close(self):
+        if getattr(self, "layer", None):
+            L.luffy_layer_destroy(self.layer)
+            self.layer = None
+        if getattr(self, "ctx", None):
+            L.luffy_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream().cuda_stream
+
+    def forward(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
+                stats: bool = False, want_rows: bool = False) -> torch.Tensor:
+        T = x.shape[0]
+        s = self._stream()
+        self.T = T
+        L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
+        self.stats = L.luffy_condense(self.layer, x, h, self.rep, s, stats=stats)
+        self.rows = L.luffy_dispatch(self.layer, x, self.recv, s, want_rows=want_rows)
+        L.luffy_expert_ffn(self.layer, self.recv, w1, w2, w3, self.out, self.pre, self.act_buf, s)
+        L.luffy_combine(self.layer, self.out, self.gathered, s)
+        L.luffy_uncondense(self.layer, self.gathered, self.y, s)
+        return self.y[:T]
+
+    def backward(self, dy: torch.Tensor, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None):
+        s = self._stream()
+        L.luffy_uncondense_bwd(self.layer, dy, self.gathered, self.d_gathered, self.dw, s)
+        L.luffy_combine_bwd(self.layer, self.d_gathered, self.d_out, s)
+        L.luffy_expert_ffn_bwd(self.layer, self.d_out, self.recv, w1, w2, w3, self.pre, self.act_buf, self.dpre,
+                               self.d_recv, self.dw1, self.dw2, self.dw3, s)
+        L.luffy_dispatch_bwd(self.layer, self.d_recv, self.dx, s)
+        L.luffy_route_bwd(self.layer, x, w_gate, self.dw, self.dx, self.dwg, s)
+        T = self.T
+        return dict(dx=self.dx[:T], dwg=self.dwg, dw1=self.dw1, dw2=self.dw2, dw3=self.dw3, dw=self.dw[:T])

@@ -204,6 +204,16 @@ typedef enum {
  * *bytes (in: capacity of dst, out: bytes of the item).  [sync] */
 LUFFY_API luffy_status luffy_debug_copy(luffy_layer* layer, int32_t item, void* dst, size_t* bytes, void* stream);
 
+/* Grouped GEMM used by the expert FFN, exposed for unit tests.  kind 0 ("rows"): D[r, :N] over the
+ * row segments off[0..G] (device, multiples of LUFFY_ROW_ALIGN) = A[r, :K] B_g^T with the epilogue `epi`
+ * (0 store, 1 GeLU: aux = pre, 2 SwiGLU, 3 GeLU', 4 SwiGLU'); b_kmajor: B_g is [N, K], else [K, N].
+ * kind 1 ("wgrad"): D_g[M, N] (fp32) = sum over segment rows of A[r, :M]^T B[r, :N]; here K is the leading
+ * dimension of A (lda) and rows m >= Msplit go to D3.  dtype selects tcgen05 (bf16) or SIMT (fp32). */
+LUFFY_API luffy_status luffy_debug_gemm(int32_t kind, int32_t dtype, int32_t epi, const void* A, const void* B,
+                                        const void* B3, void* D, void* aux, float* D3, int32_t Msplit,
+                                        const int32_t* off, int32_t G, int64_t max_rows, int32_t M, int32_t N,
+                                        int32_t K, int32_t b_kmajor, void* stream);
+
 /* ---- sequence migration placement (CPU, host memory, synchronous, reentrant, deterministic) ------ */
 
 typedef struct {

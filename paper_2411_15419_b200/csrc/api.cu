@@ -33,7 +33,7 @@ int gemm_wgrad_simt(int dtype, const void* A, const void* B, float* D, float* D3
 int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
                  int64_t max_rows, int N, int K, int b_kmajor, void* s);
 int gemm_wgrad_tc(const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M, int N,
-                  int lda, int ldb, void* s);
+                  int lda, int ldb, int64_t max_rows, void* s);
 int launch_pack_rows(luffy_layer* L, const void* x, void* dst_rows, void* s);
 
 namespace {
@@ -144,6 +144,8 @@ luffy_status validate(const luffy_config* c) {
   if (c->act != LUFFY_GELU && c->act != LUFFY_SWIGLU) return fail(LUFFY_E_INVALID, "act must be LUFFY_GELU or LUFFY_SWIGLU");
   if (c->renormalize < -1 || c->renormalize > 1) return fail(LUFFY_E_INVALID, "renormalize must be -1, 0 or 1");
   if (c->max_tokens < 1) return fail(LUFFY_E_INVALID, "max_tokens must be >= 1");
+  if (c->dtype == LUFFY_BF16 && (c->d_model % 256 || c->d_ffn % 256))
+    return fail(LUFFY_E_UNSUPPORTED, "bf16 (tcgen05) path needs d_model and d_ffn multiples of 256");
   const Dims m = dims_of(c);
   if (m.Cpad >= (int64_t)1 << 30) return fail(LUFFY_E_INVALID, "max_tokens * top_k too large");
   if (c->world == 1 && c->max_recv_rows > 0 && c->max_recv_rows < m.Rpad)
@@ -151,12 +153,15 @@ luffy_status validate(const luffy_config* c) {
   return LUFFY_OK;
 }
 
+// bf16: tcgen05 tensor cores; fp32: exact SIMT FFMA (tf32 would break the fp32 tolerance).
 int gemm_rows(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off,
               int G, int64_t max_rows, int N, int K, int b_kmajor, void* s) {
+  if (dtype == LUFFY_BF16) return gemm_rows_tc(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, s);
   return gemm_rows_simt(dtype, epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, s);
 }
 int gemm_wgrad(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M,
-               int N, int lda, int ldb, void* s) {
+               int N, int lda, int ldb, int64_t max_rows, void* s) {
+  if (dtype == LUFFY_BF16) return gemm_wgrad_tc(A, B, D, D3, Msplit, off, G, M, N, lda, ldb, max_rows, s);
   return gemm_wgrad_simt(dtype, A, B, D, D3, Msplit, off, G, M, N, lda, ldb, s);
 }
 
@@ -606,15 +611,15 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
                           f, d, 0, stream), "ffn_bwd/dgrad2");
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, nullptr, d_recv, nullptr, off, G, rows, d, f, 0, stream),
                 "ffn_bwd/dgrad1");
-    LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, stream), "ffn_bwd/wgrad2");
-    LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, nullptr, f, off, G, f, d, f, d, stream), "ffn_bwd/wgrad1");
+    LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, rows, stream), "ffn_bwd/wgrad2");
+    LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, nullptr, f, off, G, f, d, f, d, rows, stream), "ffn_bwd/wgrad1");
   } else {
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_DSWIGLU, d_out, w2, nullptr, scratch_dpre, const_cast<void*>(saved_pre), off, G,
                           rows, f, d, 0, stream), "ffn_bwd/dgrad2");
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, w3, d_recv, nullptr, off, G, rows, d, 2 * f, 0, stream),
                 "ffn_bwd/dgrad1");
-    LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, stream), "ffn_bwd/wgrad2");
-    LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, dw3, f, off, G, 2 * f, d, 2 * f, d, stream), "ffn_bwd/wgrad1");
+    LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, rows, stream), "ffn_bwd/wgrad2");
+    LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, dw3, f, off, G, 2 * f, d, 2 * f, d, rows, stream), "ffn_bwd/wgrad1");
   }
   return LUFFY_OK;
 }
@@ -646,6 +651,22 @@ luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate,
   LUFFY_NEED(dw_gate);
   LUFFY_STAGE(L, 6, "luffy_route_bwd");
   LUFFY_CHECK(launch_route_bwd(L, x, w_gate, d_topk_w, dx, dw_gate, stream), "luffy_route_bwd");
+  return LUFFY_OK;
+}
+
+luffy_status luffy_debug_gemm(int32_t kind, int32_t dtype, int32_t epi, const void* A, const void* B, const void* B3,
+                              void* D, void* aux, float* D3, int32_t Msplit, const int32_t* off, int32_t G,
+                              int64_t max_rows, int32_t M, int32_t N, int32_t K, int32_t b_kmajor, void* stream) {
+  LUFFY_NEED(A);
+  LUFFY_NEED(B);
+  LUFFY_NEED(D);
+  LUFFY_NEED(off);
+  if (kind == 0) {
+    LUFFY_CHECK(gemm_rows(dtype, epi, A, B, B3, D, aux, off, G, max_rows, N, K, b_kmajor, stream), "luffy_debug_gemm");
+  } else {
+    LUFFY_CHECK(gemm_wgrad(dtype, A, B, static_cast<float*>(D), D3, Msplit, off, G, M, N, K, N, max_rows, stream),
+                "luffy_debug_gemm");
+  }
   return LUFFY_OK;
 }
 

@@ -10,7 +10,7 @@ namespace luffy {
 
 #define LUFFY_CUDA_TRY(expr)                          \
   do {                                                \
-    cudaError_t _e = (expr);                          \
+    cudaError_t _e = (cudaError_t)(expr);             \
     if (_e != cudaSuccess) return (int)_e;            \
   } while (0)
 

@@ -1,0 +1,421 @@
+// tcgen05 grouped GEMMs for the expert FFN (bf16 in, fp32 accumulation in TMEM), sm_100a.
+//
+// One persistent CTA per SM, warp-specialized:
+//   warp 0      TMA producer: 4-stage ring of (A 128x64, B 256x64) bf16 tiles, SWIZZLE_128B, mbarrier
+//               transaction counts;
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16)
+//               into a double-buffered TMEM accumulator (2 x 256 columns);
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> fused GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the
+//               fp32 weight gradient) stored straight to global memory.
+// Tiles walk expert segments whose row offsets (multiples of 128) live on the device, so no host sync
+// is needed to size the work.  Operands may be K-major or MN-major (the backward reads W1/W2 and the
+// token-major activations transposed through the descriptor's major bit instead of transposing data).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace luffy {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KiB
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+constexpr int THREADS = 192;
+
+struct TcArgs {
+  const int32_t* off;  // [G+1] segment offsets (rows), multiples of 128
+  int G;
+  int N, K, M;         // rows mode: D[rows, N] = A[rows, K] B^T.  wgrad: D[M, N] per group, K = segment rows
+  int nbc;             // n-blocks per m-block
+  int Nb, Kb;          // rows of one group's B in the B tensor map (K-major: Nb; MN-major: Kb)
+  int ksplit;          // MN-major B split along K over (tB, tB3) at Kb
+  void* D;
+  void* aux;
+  float* D3;
+  int Msplit;
+  int f;               // SwiGLU: d_ffn
+};
+
+struct Tile {
+  int g, m0, n0, nkb, krow0;
+};
+
+template <bool WG>
+__device__ __forceinline__ int num_tiles(const TcArgs& a, const int32_t* off_s) {
+  if (WG) return a.G * (a.M / BM) * a.nbc;
+  return (off_s[a.G] / BM) * a.nbc;
+}
+
+template <int EPI, bool WG>
+__device__ __forceinline__ Tile decode(int t, const TcArgs& a, const int32_t* off_s) {
+  Tile x;
+  if (WG) {
+    const int tpg = (a.M / BM) * a.nbc;
+    x.g = t / tpg;
+    const int r = t % tpg;
+    x.m0 = (r / a.nbc) * BM;
+    x.n0 = (r % a.nbc) * BN;
+    x.krow0 = off_s[x.g];
+    x.nkb = (off_s[x.g + 1] - off_s[x.g]) / BK;
+  } else {
+    const int mb = t / a.nbc, nb = t % a.nbc;
+    x.m0 = mb * BM;
+    x.g = find_group(off_s, a.G, x.m0);
+    x.n0 = nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
+    x.nkb = a.K / BK;
+    x.krow0 = 0;
+  }
+  return x;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void store32_bf16(bf16* dst, const float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                         pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    reinterpret_cast<uint4*>(dst)[q] = u;
+  }
+}
+__device__ __forceinline__ void load32_bf16(const bf16* src, float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = reinterpret_cast<const uint4*>(src)[q];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      v[8 * q + 2 * i] = f.x;
+      v[8 * q + 2 * i + 1] = f.y;
+    }
+  }
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool WG>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                   const __grid_constant__ CUtensorMap tB3, const TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int32_t off_s[LUFFY_MAX_EXPERTS + 1];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i <= a.G; i += blockDim.x) off_s[i] = a.off[i];
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 4);
+    }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tA);
+    tc::tma_prefetch(&tB);
+    if (EPI == EPI_SWIGLU || B_MN) tc::tma_prefetch(&tB3);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int ntiles = num_tiles<WG>(a, off_s);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile x = decode<EPI, WG>(t, a, off_s);
+        for (int kb = 0; kb < x.nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dA = sA + stage * A_BYTES;
+          uint8_t* dB = sB + stage * B_BYTES;
+          tc::mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          if (!A_MN) {
+            tc::tma_load_2d(dA, &tA, &full[stage], kb * BK, x.m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tc::tma_load_2d(dA + j * 8192, &tA, &full[stage], x.m0 + 64 * j, x.krow0 + kb * BK);
+          }
+          if (WG) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tc::tma_load_2d(dB + j * 8192, &tB, &full[stage], x.n0 + 64 * j, x.krow0 + kb * BK);
+          } else if (!B_MN) {
+            if (EPI == EPI_SWIGLU) {
+              tc::tma_load_2d(dB, &tB, &full[stage], kb * BK, x.g * a.Nb + x.n0);
+              tc::tma_load_2d(dB + B_BYTES / 2, &tB3, &full[stage], kb * BK, x.g * a.Nb + x.n0);
+            } else {
+              tc::tma_load_2d(dB, &tB, &full[stage], kb * BK, x.g * a.Nb + x.n0);
+            }
+          } else {
+            const int kk = kb * BK;
+            const bool hi = a.ksplit && kk >= a.Kb;
+            const CUtensorMap* mp = hi ? &tB3 : &tB;
+            const int kl = hi ? kk - a.Kb : kk;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tc::tma_load_2d(dB + j * 8192, mp, &full[stage], x.n0 + 64 * j, x.g * a.Kb + kl);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------------ MMA issuer (single thread)
+      constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile x = decode<EPI, WG>(t, a, off_s);
+        tc::mbar_wait(&tempty[acc], aphase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < x.nkb; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t a0 = tc::smem_u32(sA + stage * A_BYTES);
+          const uint32_t b0 = tc::smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? tc::smem_desc(a0 + kk * 2048, 8192, 1024) : tc::smem_desc(a0 + kk * 32, 16, 1024);
+            const uint64_t bd = (B_MN || WG) ? tc::smem_desc(b0 + kk * 2048, 8192, 1024) : tc::smem_desc(b0 + kk * 32, 16, 1024);
+            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    // -------------------------------------------------------------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int rt = 32 * q + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const Tile x = decode<EPI, WG>(t, a, off_s);
+      tc::mbar_wait(&tfull[acc], aphase);
+      tc::tc_fence_after();
+      const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+      if (WG) {
+        const int m = x.m0 + rt;
+        float* dst = m < a.Msplit ? static_cast<float*>(a.D) + ((size_t)x.g * a.Msplit + m) * a.N
+                                  : a.D3 + ((size_t)x.g * (a.M - a.Msplit) + (m - a.Msplit)) * a.N;
+        dst += x.n0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tc::tmem_ld32(tb + c0, r);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 v = x.nkb > 0 ? make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                                               __uint_as_float(r[i + 3]))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(dst + c0 + i) = v;
+          }
+        }
+      } else {
+        const size_t row = (size_t)(x.m0 + rt);
+        bf16* D = static_cast<bf16*>(a.D);
+        bf16* X = static_cast<bf16*>(a.aux);
+        if (EPI == EPI_SWIGLU) {
+          const int f = a.f;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+            uint32_t r1[32], r3[32];
+            tc::tmem_ld32(tb + c0, r1);
+            tc::tmem_ld32(tb + BN / 2 + c0, r3);
+            tc::tmem_ld_wait();
+            float p1[32], p3[32], o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              p1[i] = __uint_as_float(r1[i]);
+              p3[i] = __uint_as_float(r3[i]);
+              o[i] = silu_f(p1[i]) * p3[i];
+            }
+            const int n = x.n0 + c0;
+            store32_bf16(X + row * (2 * f) + n, p1);
+            store32_bf16(X + row * (2 * f) + f + n, p3);
+            store32_bf16(D + row * f + n, o);
+          }
+        } else {
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            uint32_t r[32];
+            tc::tmem_ld32(tb + c0, r);
+            tc::tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            const int n = x.n0 + c0;
+            if (EPI == EPI_STORE) {
+              store32_bf16(D + row * a.N + n, v);
+            } else if (EPI == EPI_GELU) {
+              store32_bf16(X + row * a.N + n, v);
+              float o[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = gelu_f(v[i]);
+              store32_bf16(D + row * a.N + n, o);
+            } else if (EPI == EPI_DGELU) {
+              float p[32];
+              load32_bf16(X + row * a.N + n, p);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(p[i]);
+              store32_bf16(D + row * a.N + n, v);
+            } else {  // EPI_DSWIGLU: v = d_act, aux = pre [rows, 2N]
+              float p1[32], p3[32], g1[32], g3[32];
+              load32_bf16(X + row * (2 * a.N) + n, p1);
+              load32_bf16(X + row * (2 * a.N) + a.N + n, p3);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                g1[i] = v[i] * p3[i] * silu_grad_f(p1[i]);
+                g3[i] = v[i] * silu_f(p1[i]);
+              }
+              store32_bf16(D + row * (2 * a.N) + n, g1);
+              store32_bf16(D + row * (2 * a.N) + a.N + n, g3);
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem_base, 512);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool WG>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
+  auto kern = gemm_tc_kernel<EPI, A_MN, B_MN, WG>;
+  static bool attr = false;
+  if (!attr) {
+    LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr = true;
+  }
+  kern<<<num_sms(), THREADS, SMEM_BYTES, s>>>(ta, tb, tb3, a);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+}  // namespace
+
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                   uint32_t box_outer) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    LUFFY_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return (int)cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+// Rows GEMM: D[r, :] over expert segments; see luffy_internal.h (Epi) for the epilogues.
+int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
+                 int64_t max_rows, int N, int K, int b_kmajor, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  TcArgs a{};
+  a.off = off;
+  a.G = G;
+  a.N = N;
+  a.K = K;
+  a.D = D;
+  a.aux = aux0;
+  a.f = N / 2;
+  CUtensorMap ta, tb, tb3;
+  LUFFY_CUDA_TRY(make_tmap_bf16(&ta, A, K, max_rows, K, BM));
+  if (b_kmajor) {
+    const bool sw = epi == EPI_SWIGLU;
+    a.Nb = sw ? N / 2 : N;
+    a.nbc = sw ? (N / 2) / (BN / 2) : N / BN;
+    LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, K, (uint64_t)G * a.Nb, K, sw ? BN / 2 : BN));
+    if (sw) LUFFY_CUDA_TRY(make_tmap_bf16(&tb3, B3, K, (uint64_t)G * a.Nb, K, BN / 2));
+    else tb3 = tb;
+    switch (epi) {
+      case EPI_STORE: return launch<EPI_STORE, false, false, false>(ta, tb, tb3, a, st);
+      case EPI_GELU: return launch<EPI_GELU, false, false, false>(ta, tb, tb3, a, st);
+      case EPI_SWIGLU: return launch<EPI_SWIGLU, false, false, false>(ta, tb, tb3, a, st);
+      default: return (int)cudaErrorNotSupported;
+    }
+  }
+  a.ksplit = B3 != nullptr && epi == EPI_STORE;
+  a.Kb = a.ksplit ? K / 2 : K;
+  a.nbc = N / BN;
+  LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, N, (uint64_t)G * a.Kb, N, 64));
+  if (a.ksplit) LUFFY_CUDA_TRY(make_tmap_bf16(&tb3, B3, N, (uint64_t)G * a.Kb, N, 64));
+  else tb3 = tb;
+  switch (epi) {
+    case EPI_STORE: return launch<EPI_STORE, false, true, false>(ta, tb, tb3, a, st);
+    case EPI_DGELU: return launch<EPI_DGELU, false, true, false>(ta, tb, tb3, a, st);
+    case EPI_DSWIGLU: return launch<EPI_DSWIGLU, false, true, false>(ta, tb, tb3, a, st);
+    default: return (int)cudaErrorNotSupported;
+  }
+}
+
+// Weight gradient: D_g[m, n] = sum over segment g rows of A[r, m] * B[r, n] (fp32 out, rows m >= Msplit -> D3).
+int gemm_wgrad_tc(const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M, int N,
+                  int lda, int ldb, int64_t max_rows, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  TcArgs a{};
+  a.off = off;
+  a.G = G;
+  a.M = M;
+  a.N = N;
+  a.nbc = N / BN;
+  a.D = D;
+  a.D3 = D3;
+  a.Msplit = Msplit;
+  CUtensorMap ta, tb;
+  LUFFY_CUDA_TRY(make_tmap_bf16(&ta, A, M, max_rows, lda, 64));
+  LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, N, max_rows, ldb, 64));
+  return launch<EPI_STORE, true, true, true>(ta, tb, tb, a, st);
+}
+
+}  // namespace luffy

@@ -26,7 +26,7 @@ EXPORTED = [
     "luffy_layer_rows", "luffy_route", "luffy_condense", "luffy_dispatch", "luffy_expert_ffn",
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
-    "luffy_attention_cost", "luffy_debug_copy",
+    "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm",
 ]
 
 
@@ -85,6 +85,7 @@ def _load():
         "luffy_plan_migration": (I32, [ctypes.POINTER(MigrationProblem), P, P]),
         "luffy_attention_cost": (I64, [I64, I64, I64]),
         "luffy_debug_copy": (I32, [P, I32, P, ctypes.POINTER(SZ), P]),
+        "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -251,3 +252,8 @@ def luffy_debug_copy(layer, item: str, stream) -> np.ndarray:
     if n.value:
         _check(LIB.luffy_debug_copy(layer, code, out.ctypes.data, ctypes.byref(n), stream))
     return out
+
+
+def luffy_debug_gemm(kind, dtype, epi, A, B, B3, D, aux, D3, Msplit, off, G, max_rows, M, N, K, b_kmajor, stream):
+    _check(LIB.luffy_debug_gemm(kind, dtype, epi, _p(A), _p(B), _p(B3), _p(D), _p(aux), _p(D3), Msplit, _p(off), G,
+                                max_rows, M, N, K, b_kmajor, stream))

@@ -129,7 +129,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->cnt_all = cv.take<int32_t>((size_t)m.P * m.E);
   o->send = m.P > 1 ? cv.take<char>(m.Rpad * m.d * es) : nullptr;
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
-  o->wg_part = cv.take<float>((size_t)kWgParts * m.E * m.d);
+  o->wg_part = cv.take<float>((size_t)wg_parts(m.E, m.d) * m.E * m.d);
 }
 
 luffy_status validate(const luffy_config* c) {
@@ -421,7 +421,9 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
     LUFFY_CHECK(launch_identity_rep(L, stream), "luffy_condense/identity");
   } else {
     L->has_adj = true;
-    LUFFY_CHECK(launch_gram_simt(L, h, stream), "luffy_condense/gram");
+    // bf16: tcgen05 Gram; fp32: exact SIMT FFMA Gram
+    if (L->dtype == LUFFY_BF16) LUFFY_CHECK(launch_gram_tc(L, h, stream), "luffy_condense/gram");
+    else LUFFY_CHECK(launch_gram_simt(L, h, stream), "luffy_condense/gram");
     LUFFY_CHECK(launch_greedy(L, stream), "luffy_condense/greedy");
   }
   LUFFY_CHECK(launch_pack(L, x, nullptr, rep, stream), "luffy_condense/layout");

@@ -13,7 +13,11 @@ void note_launch(int n = 1);
 
 constexpr int kRowAlign = LUFFY_ROW_ALIGN;
 constexpr int kGreedyMaxRounds = 1 << 14;
-constexpr int kWgParts = 16;  // token slices of the deterministic dW_g reduction
+// token slices of the deterministic dW_g reduction: enough CTAs to stream X once, bounded scratch
+inline int wg_parts(int E, int d) {
+  int p = (1 << 22) / (E * d);
+  return p < 16 ? 16 : (p > 128 ? 128 : p);
+}
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 

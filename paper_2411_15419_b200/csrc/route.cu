@@ -228,16 +228,17 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
     route_bwd_kernel<float><<<blocks, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, L->renorm,
                                                     L->dl, static_cast<float*>(dx));
   LUFFY_LAUNCHED();
-  const int chunk = (L->T + kWgParts - 1) / kWgParts;
+  const int parts = wg_parts(L->E, L->d);
+  const int chunk = (L->T + parts - 1) / parts;
   constexpr int EB = 16;
-  dim3 grid((L->d + 255) / 256, kWgParts, (L->E + EB - 1) / EB);
+  dim3 grid((L->d + 255) / 256, parts, (L->E + EB - 1) / EB);
   if (L->dtype == LUFFY_BF16)
     wg_partial_kernel<bf16, EB><<<grid, 256, 0, st>>>(L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d, chunk, L->wg_part);
   else
     wg_partial_kernel<float, EB><<<grid, 256, 0, st>>>(L->dl, static_cast<const float*>(x), L->T, L->E, L->d, chunk, L->wg_part);
   LUFFY_LAUNCHED();
   const int n = L->E * L->d;
-  wg_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(L->wg_part, kWgParts, n, dwg);
+  wg_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(L->wg_part, parts, n, dwg);
   LUFFY_LAUNCHED();
   return 0;
 }

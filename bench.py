@@ -48,27 +48,31 @@ class ClockSampler:
     def __init__(self, dev: int):
         self.dev = dev
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = (0.0, float("inf"))
 
-    def __enter__(self):
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.dev)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 20:   # wait for the first sample
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -79,7 +83,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = self.window
+        for ts, ln in self.lines:
+            if ts < lo or ts > hi:
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -150,7 +157,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--h", type=float, default=None)
@@ -231,6 +238,7 @@ def main():
     reps_e = np.array(st.reps_per_expert[:E], np.int64)
     R = int(st.reps)
     rounds = int(st.rounds)
+    clk = ClockSampler(local).start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -240,17 +248,20 @@ def main():
     evs = [[ev() for _ in range(n_ev)] for _ in range(args.steps)]
     start, stop = ev(), ev()
     launches0 = L.luffy_launch_count()
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start.record(stream)
-        for i in range(args.steps):
-            step(evs[i])
-        stop.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_host0 = time.time()
+    start.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    stop.record(stream)
+    torch.cuda.synchronize()
+    clk.window = (t_host0, time.time())
+    time.sleep(0.06)
+    clk.stop()
+    if world > 1:
+        dist.barrier()
     launches = (L.luffy_launch_count() - launches0) // args.steps
     ms = start.elapsed_time(stop)
     if world > 1:

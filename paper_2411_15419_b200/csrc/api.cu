@@ -125,11 +125,17 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->slot_gl = cv.take<int32_t>(m.Rpad);
   o->pos = cv.take<int32_t>(m.C);
   o->rep = cv.take<int32_t>(m.C);
+  o->mstart = cv.take<int32_t>(m.Rpad);
+  o->mcnt = cv.take<int32_t>(m.Rpad);
+  o->mcur = cv.take<int32_t>(m.Rpad);
+  o->members = cv.take<int32_t>(m.Cpad);
+  o->mslot = cv.take<int32_t>(m.Cpad);
+  o->mpart = cv.take<float>((size_t)(m.Cpad / 16) * 2 * m.d);
   o->roff = cv.take<int32_t>(m.El + 1);
   o->cnt_all = cv.take<int32_t>((size_t)m.P * m.E);
   o->send = m.P > 1 ? cv.take<char>(m.Rpad * m.d * es) : nullptr;
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
-  o->wg_part = cv.take<float>((size_t)wg_parts(m.E, m.d) * m.E * m.d);
+  o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 63) / 64) * m.E * m.d);
 }
 
 luffy_status validate(const luffy_config* c) {

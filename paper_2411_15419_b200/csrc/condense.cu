@@ -340,12 +340,17 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
         const uint32_t* al = a.alive + (goff_s[g] >> 5);
         unsigned long long m = __ldcg(src + r);
         for (int wd = lane; wd < W; wd += 32) {
-          uint32_t bits = row[wd] & __ldcg(al + wd);
-          while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const unsigned long long v = __ldcg(src + goff_s[g] + wd * 32 + b);
-            m = v > m ? v : m;
+          const uint32_t bits = row[wd] & __ldcg(al + wd);
+          if (bits) {
+            // independent predicated loads (not a dependent bit walk) so they are all in flight at once
+            const unsigned long long* p = src + goff_s[g] + wd * 32;
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+              if ((bits >> b) & 1u) {
+                const unsigned long long v = __ldcg(p + b);
+                m = v > m ? v : m;
+              }
+            }
           }
         }
         m = warp_max_u64(m);

@@ -5,7 +5,7 @@
 //               transaction counts;
 //   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16)
 //               into a double-buffered TMEM accumulator (2 x 256 columns);
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> fused GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the
+//   warps 2-9   epilogue (two per TMEM lane quarter, one column half each): tcgen05.ld 32x32b.x32 -> fused GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the
 //               fp32 weight gradient) stored straight to global memory.
 // Tiles walk expert segments whose row offsets (multiples of 128) live on the device, so no host sync
 // is needed to size the work.  Operands may be K-major or MN-major (the backward reads W1/W2 and the
@@ -22,7 +22,7 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KiB
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quarter)
 
 struct TcArgs {
   const int32_t* off;  // [G+1] segment offsets (rows), multiples of 128
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 4);
+      tc::mbar_init(&tempty[s], 8);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tA);
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // -------------------------------------------------------------------- epilogue warps 2..5
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int hc = (warp - 2) >> 2;  // column half handled by this warp
     const int rt = 32 * q + lane;
     int acc = 0;
     uint32_t aphase = 0;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                   : a.D3 + ((size_t)x.g * (a.M - a.Msplit) + (m - a.Msplit)) * a.N;
         dst += x.n0;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = hc * (BN / 2); c0 < (hc + 1) * (BN / 2); c0 += 32) {
           uint32_t r[32];
           tc::tmem_ld32(tb + c0, r);
           tc::tmem_ld_wait();
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (EPI == EPI_SWIGLU) {
           const int f = a.f;
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+          for (int c0 = hc * (BN / 4); c0 < (hc + 1) * (BN / 4); c0 += 32) {
             uint32_t r1[32], r3[32];
             tc::tmem_ld32(tb + c0, r1);
             tc::tmem_ld32(tb + BN / 2 + c0, r3);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         } else {
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
+          for (int c0 = hc * (BN / 2); c0 < (hc + 1) * (BN / 2); c0 += 32) {
             uint32_t r[32];
             tc::tmem_ld32(tb + c0, r);
             tc::tmem_ld_wait();

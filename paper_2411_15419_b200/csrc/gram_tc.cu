@@ -19,7 +19,7 @@ namespace {
 constexpr int TS = 128, BK = 64, STAGES = 6;
 constexpr int T_BYTES = TS * BK * 2;  // 16 KiB per operand tile
 constexpr int SMEM_BYTES = STAGES * 2 * T_BYTES + 1024 + 256;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
 struct GramArgs {
   const int32_t* goff;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 4);
+      tc::mbar_init(&tempty[s], 8);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tX);
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     }
   } else {
     const int q = warp & 3;
+    const int hc = (warp - 2) >> 2;  // column half of the tile handled by this warp
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
       tc::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * TS;
 #pragma unroll 1
-      for (int c = 0; c < TS / 32; ++c) {
+      for (int c = 2 * hc; c < 2 * hc + 2; ++c) {
         uint32_t r[32];
         tc::tmem_ld32(tb + 32 * c, r);
         tc::tmem_ld_wait();

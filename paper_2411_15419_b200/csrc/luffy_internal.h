@@ -61,6 +61,12 @@ struct luffy_layer {
   int32_t* slot_gl;   // [Rpad_max] slot -> group row (-1 = padding)
   int32_t* pos;       // [Tmax, k] slot of the representative of copy (t, j)
   int32_t* rep;       // [Tmax, k] representative token of copy (t, j)
+  int32_t* mstart;    // [Rpad_max] first member (group-row space) of each slot's member list
+  int32_t* mcnt;      // [Rpad_max] members per slot
+  int32_t* mcur;      // [Rpad_max] placement cursor
+  int32_t* members;   // [Cpad_max] member group rows, slot-major, token order within a slot
+  int32_t* mslot;     // [Cpad_max] slot of each member entry (-1 = padding)
+  float* mpart;       // [Cpad_max / 16 * 2, d] fp32 partial sums of slots crossing member windows
   int32_t* roff;      // [El+1] padded expert-side row offsets (device)
   int32_t* cnt_all;   // [P, E] all-gathered representative counts (device)
   void* send;         // [Rpad_max, d] send buffer (world > 1); reused as d_send in backward

@@ -39,6 +39,35 @@ __device__ __forceinline__ int block_scan_flag2(bool flag, int* warp_sums, int& 
   return pre;
 }
 
+// Block-wide exclusive scan of one int per thread.
+__device__ __forceinline__ int block_scan_value(int v, int* warp_sums, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) warp_sums[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const int w = lane < nw ? warp_sums[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += u;
+    }
+    if (lane < nw) warp_sums[lane] = wi - w;
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  const int pre = inc - v + warp_sums[wid];
+  total = warp_sums[32];
+  __syncthreads();
+  return pre;
+}
+
 // One CTA per expert.  Every CTA recounts the representatives of all experts (cheap) so that the
 // padded send offsets need no second launch.
 __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict__ goff, const int32_t* __restrict__ gcnt,
@@ -47,7 +76,11 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ nrep, int32_t* __restrict__ soff,
                                                       int32_t* __restrict__ lslot, int32_t* __restrict__ perm,
                                                       int32_t* __restrict__ slot_gl, int32_t* __restrict__ pos,
-                                                      int32_t* __restrict__ rep) {
+                                                      int32_t* __restrict__ rep, int32_t* __restrict__ mstart,
+                                                      int32_t* __restrict__ mcnt, int32_t* __restrict__ mcur,
+                                                      int32_t* __restrict__ members, int32_t* __restrict__ mslot,
+                                                      int cur_cap) {
+  extern __shared__ int cur_smem[];
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
@@ -104,6 +137,55 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
       if (idx[(size_t)t * k + j] == e) jj = j;
     pos[(size_t)t * k + jj] = lslot[r];
     rep[(size_t)t * k + jj] = gtok[r];
+  }
+  // ---- member CSR of every slot of this expert, members in token (= group row) order, stored in the
+  // group-row space [g0, g0 + n) (padding rows of the space hold -1): mstart[slot], mcnt[slot],
+  // members[], mslot[] (the slot of each member).  Deterministic: integer-atomic counts, then a stable
+  // block-wide placement (in-warp ranks by __match_any_sync, cross-warp order by warp index).
+  const int s0 = offs[e], ns = cnt[e];
+  for (int s = s0 + threadIdx.x; s < offs[e + 1]; s += blockDim.x) mcnt[s] = 0;
+  for (int g = g0 + n + threadIdx.x; g < goff_s[e + 1]; g += blockDim.x) {
+    members[g] = -1;
+    mslot[g] = -1;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x) atomicAdd(&mcnt[lslot[rep_local[g0 + c]]], 1);
+  __syncthreads();
+  int* cur = ns <= cur_cap ? cur_smem : mcur + s0;  // placement cursors (shared memory when they fit)
+  int run = g0;
+  for (int c0 = 0; c0 < ns; c0 += blockDim.x) {
+    const int s = s0 + c0 + threadIdx.x;
+    const int v = c0 + threadIdx.x < ns ? mcnt[s] : 0;
+    int total;
+    const int pre = block_scan_value(v, warp_sums, total);
+    if (c0 + threadIdx.x < ns) {
+      mstart[s] = run + pre;
+      cur[c0 + threadIdx.x] = run + pre;
+    }
+    run += total;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+    const bool valid = c0 + threadIdx.x < n;
+    const int g = g0 + c0 + threadIdx.x;
+    const int key = valid ? lslot[rep_local[g]] - s0 : -1 - lane;  // invalid lanes never group
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    int b = 0;
+    for (int w = 0; w < nwb; ++w) {  // warps claim their runs in order: stable across the block
+      if (wid == w && valid && lane == leader) {
+        b = cur[key];
+        cur[key] = b + __popc(peers);
+      }
+      __syncthreads();
+    }
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (valid) {
+      const int p = b + __popc(peers & ((1u << lane) - 1u));
+      members[p] = g;
+      mslot[p] = key + s0;
+    }
   }
 }
 
@@ -179,69 +261,137 @@ __global__ void __launch_bounds__(256) dw_kernel(const T* __restrict__ dy, const
 }
 
 // d_gathered[slot] = sum_{members m of the slot, token order} gw[m] * dy[gtok[m]]; padding -> 0.
-// One warp per slot; columns in passes of 256 * CH elements (CH 16-byte chunks per lane).
-template <typename T, int CH>
-__global__ void __launch_bounds__(256) uncondense_bwd_kernel(const T* __restrict__ dy, const int32_t* __restrict__ slot_gl,
-                                                             const int32_t* __restrict__ soff, const int32_t* __restrict__ goff,
-                                                             const int32_t* __restrict__ gtok, const float* __restrict__ gw,
-                                                             const int32_t* __restrict__ rep_local,
-                                                             const int64_t* __restrict__ adjoff, const uint32_t* __restrict__ adj,
-                                                             int has_adj, int E, int d, T* __restrict__ dg) {
-  __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
-  for (int i = threadIdx.x; i <= E; i += blockDim.x) goff_s[i] = goff[i];
-  __syncthreads();
+//
+// Load-balanced and deterministic: the slot-sorted member array (group-row space) is cut into fixed
+// windows of WIN members; one warp per window walks its members in order, accumulating the current
+// slot in fp32.  A slot that lies inside one window is written directly; a slot crossing window
+// boundaries leaves fp32 partials (the head run of a window at part[w][0], the tail run at part[w][1])
+// that uncondense_bwd_finalize sums in window order.
+constexpr int WIN = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
+    const T* __restrict__ dy, const int32_t* __restrict__ goff, int E, const int32_t* __restrict__ members,
+    const int32_t* __restrict__ mslot, const int32_t* __restrict__ mstart, const int32_t* __restrict__ mcnt,
+    const int32_t* __restrict__ gtok, const float* __restrict__ gw, int d, T* __restrict__ dg, float* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwin = goff[E] / WIN;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwin; wi += nw) {
+    const int m0 = (int)(wi * WIN);
+    int my_slot = -1, my_tok = 0;
+    float my_w = 0.f;
+    if (lane < WIN) {
+      const int g = members[m0 + lane];
+      if (g >= 0) {
+        my_slot = mslot[m0 + lane];
+        my_tok = gtok[g];
+        my_w = gw[g];
+      }
+    }
+    const unsigned live = __ballot_sync(0xffffffffu, my_slot >= 0);
+    if (!live) continue;
+    for (int c0 = 0; c0 < d; c0 += 512) {
+      float acc[2][8];
+      int cur = -1;
+      auto flush = [&](int slot) {
+        const int ms = mstart[slot], me = ms + mcnt[slot];
+        const int c = c0 + lane * 8;
+        if (ms >= m0 && me <= m0 + WIN) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (c + q * 256 < d) store8(dg + (size_t)slot * d + c + q * 256, acc[q]);
+        } else {
+          float* dst = part + ((size_t)wi * 2 + (ms < m0 ? 0 : 1)) * d;
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (c + q * 256 < d) store8(dst + c + q * 256, acc[q]);
+        }
+      };
+      // issue all row loads of the window first (at most WIN rows of 2 x 16 bytes per lane)
+      uint4 raw[WIN][2];
+#pragma unroll
+      for (int u = 0; u < WIN; ++u) {
+        const int tok = __shfl_sync(0xffffffffu, my_tok, u);
+        const bool ok = (live >> u) & 1u;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = c0 + q * 256 + lane * 8;
+          if (sizeof(T) == 2 && ok && c < d)
+            raw[u][q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(dy) + (size_t)tok * d + c);
+          else
+            raw[u][q] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < WIN; ++u) {
+        const int slot = __shfl_sync(0xffffffffu, my_slot, u);
+        const float wm = __shfl_sync(0xffffffffu, my_w, u);
+        const int tok = __shfl_sync(0xffffffffu, my_tok, u);
+        if (slot < 0) continue;  // padding rows (warp-uniform)
+        if (slot != cur) {
+          if (cur >= 0) flush(cur);
+          cur = slot;
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = c0 + q * 256 + lane * 8;
+          float v[8];
+          if constexpr (sizeof(T) == 2) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u][q]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(h[i]);
+              v[2 * i] = f.x;
+              v[2 * i + 1] = f.y;
+            }
+          } else {
+            if (c < d) load8(reinterpret_cast<const float*>(dy) + (size_t)tok * d + c, v);
+            else
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[q][i] = fmaf(wm, v[i], acc[q][i]);
+        }
+      }
+      if (cur >= 0) flush(cur);
+    }
+  }
+}
+
+// Slots crossing window boundaries: sum the partials in window order.  Padding slots are zeroed.
+template <typename T>
+__global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int32_t* __restrict__ perm,
+                                                                      const int32_t* __restrict__ soff, int E,
+                                                                      const int32_t* __restrict__ mstart,
+                                                                      const int32_t* __restrict__ mcnt, int d,
+                                                                      const float* __restrict__ part, T* __restrict__ dg) {
   const int lane = threadIdx.x & 31;
   const int64_t rows = soff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < rows; s += nw) {
-    const int u = slot_gl[s];
     T* out = dg + s * d;
-    if (u < 0) {
+    if (perm[s] < 0) {
       for (int c = lane * 8; c < d; c += 256) zero8(out + c);
       continue;
     }
-    const int g = find_group(goff_s, E, u);
-    const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
-    const uint32_t* row = has_adj ? adj + adjoff[g] + (int64_t)(u - goff_s[g]) * W : nullptr;
-    for (int c0 = 0; c0 < d; c0 += 256 * CH) {
-      float acc[CH][8];
+    const int ms = mstart[s], me = ms + mcnt[s];
+    const int ws = ms / WIN, we = (me - 1) / WIN;
+    if (ws == we) continue;  // written by the window kernel
+    for (int c = lane * 8; c < d; c += 256) {
+      float acc[8], v[8];
+      load8(part + ((size_t)ws * 2 + 1) * d + c, acc);
+      for (int w = ws + 1; w <= we; ++w) {
+        load8(part + ((size_t)w * 2) * d + c, v);
 #pragma unroll
-      for (int q = 0; q < CH; ++q)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
-      auto add_member = [&](int m) {
-        const float wm = gw[m];
-        const T* src = dy + (size_t)gtok[m] * d;
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int c = c0 + q * 256 + lane * 8;
-          if (c < d) {
-            float v[8];
-            load8(src + c, v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[q][i] = fmaf(wm, v[i], acc[q][i]);
-          }
-        }
-      };
-      bool self_done = false;
-      if (has_adj) {
-        for (int wd = 0; wd < W; ++wd) {
-          uint32_t bits = row[wd];  // warp-uniform broadcast load
-          while (bits) {
-            const int b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int m = goff_s[g] + wd * 32 + b;
-            if (!self_done && m > u) { add_member(u); self_done = true; }
-            if (rep_local[m] == u) add_member(m);
-          }
-        }
+        for (int i = 0; i < 8; ++i) acc[i] += v[i];
       }
-      if (!self_done) add_member(u);
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int c = c0 + q * 256 + lane * 8;
-        if (c < d) store8(out + c, acc[q]);
-      }
+      store8(out + c, acc);
     }
   }
 }
@@ -277,8 +427,15 @@ inline int grid_for_warps(int64_t warps) {
 
 int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  layout_kernel<<<L->E, 1024, 0, st>>>(L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep, L->soff,
-                                       L->lslot, L->perm, L->slot_gl, L->pos, L->rep);
+  const int cur_cap = (int)std::min<int64_t>(L->Rpad_max, 40000);
+  static bool attr = false;
+  if (!attr) {
+    LUFFY_CUDA_TRY(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000 * 4));
+    attr = true;
+  }
+  layout_kernel<<<L->E, 1024, cur_cap * 4, st>>>(L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
+                                                 L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
+                                                 L->mcnt, L->mcur, L->members, L->mslot, cur_cap);
   LUFFY_LAUNCHED();
   if (rep_out) {
     LUFFY_CUDA_TRY(cudaMemcpyAsync(rep_out, L->rep, sizeof(int32_t) * L->T * L->k, cudaMemcpyDeviceToDevice, st));
@@ -325,21 +482,28 @@ int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void*
 int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gathered, void* dg, float* dw, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int bt = grid_for_warps(L->T);
+  const int bw = grid_for_warps(L->Cpad_max / WIN);
   const int bs = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16) {
     dw_kernel<bf16><<<bt, 256, 0, st>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
                                         L->k, L->d, dw);
     LUFFY_LAUNCHED();
-    uncondense_bwd_kernel<bf16, 4><<<bs, 256, 0, st>>>(static_cast<const bf16*>(dy), L->slot_gl, L->soff, L->goff, L->gtok,
-                                                       L->gw, L->rep_local, L->adjoff, L->adj, L->has_adj ? 1 : 0, L->E,
-                                                       L->d, static_cast<bf16*>(dg));
+    uncondense_bwd_window_kernel<bf16><<<bw, 256, 0, st>>>(static_cast<const bf16*>(dy), L->goff, L->E, L->members,
+                                                           L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
+                                                           static_cast<bf16*>(dg), L->mpart);
+    LUFFY_LAUNCHED();
+    uncondense_bwd_finalize_kernel<bf16><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
+                                                             static_cast<bf16*>(dg));
   } else {
     dw_kernel<float><<<bt, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos, L->T,
                                          L->k, L->d, dw);
     LUFFY_LAUNCHED();
-    uncondense_bwd_kernel<float, 4><<<bs, 256, 0, st>>>(static_cast<const float*>(dy), L->slot_gl, L->soff, L->goff,
-                                                        L->gtok, L->gw, L->rep_local, L->adjoff, L->adj,
-                                                        L->has_adj ? 1 : 0, L->E, L->d, static_cast<float*>(dg));
+    uncondense_bwd_window_kernel<float><<<bw, 256, 0, st>>>(static_cast<const float*>(dy), L->goff, L->E, L->members,
+                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
+                                                            static_cast<float*>(dg), L->mpart);
+    LUFFY_LAUNCHED();
+    uncondense_bwd_finalize_kernel<float><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,
+                                                              L->mpart, static_cast<float*>(dg));
   }
   LUFFY_LAUNCHED();
   return 0;

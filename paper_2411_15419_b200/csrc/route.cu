@@ -114,6 +114,130 @@ __global__ void __launch_bounds__(256) route_kernel(const T* __restrict__ x, con
   }
 }
 
+// Fast gate for E <= 32: a CTA of 8 warps owns 32 tokens (4 per warp); W_g is staged through shared
+// memory in chunks of RC columns and every weight read from shared memory feeds 4 tokens.  Lane l owns
+// columns {4l..4l+3} and {128+4l..128+4l+3} of each 256-wide sub-chunk (conflict-free float4 reads).
+// Summation order is fixed (chunk, lane partial, butterfly), so the logits are reproducible.
+template <typename T, int EB>
+__global__ void __launch_bounds__(256) route_fast_kernel(const T* __restrict__ x, const float* __restrict__ wg, int T_,
+                                                         int E, int d, int k, int renorm, float* __restrict__ probs,
+                                                         int32_t* __restrict__ idx, float* __restrict__ w,
+                                                         int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
+  constexpr int TB = 4, RC = 8192 / EB;  // 32 KiB of staged weights per chunk
+  __shared__ __align__(16) float ws[EB][RC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t0 = blockIdx.x * 32 + wid * TB;
+  float acc[TB][EB];
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int e = 0; e < EB; ++e) acc[i][e] = 0.f;
+  for (int c0 = 0; c0 < d; c0 += RC) {
+    const int rc = min(RC, d - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < E * (rc / 4); i += blockDim.x) {
+      const int e = i / (rc / 4), c = (i % (rc / 4)) * 4;
+      *reinterpret_cast<float4*>(&ws[e][c]) = *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c);
+    }
+    __syncthreads();
+    for (int s0 = 0; s0 < rc; s0 += 256) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int cl = s0 + half * 128 + lane * 4;
+        float xv[TB][4];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int t = t0 + i;
+          if (t < T_) {
+            const T* p = x + (size_t)t * d + c0 + cl;
+            if constexpr (sizeof(T) == 2) {
+              const uint2 u = *reinterpret_cast<const uint2*>(p);
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+              xv[i][0] = a.x; xv[i][1] = a.y; xv[i][2] = b.x; xv[i][3] = b.y;
+            } else {
+              const float4 u = *reinterpret_cast<const float4*>(p);
+              xv[i][0] = u.x; xv[i][1] = u.y; xv[i][2] = u.z; xv[i][3] = u.w;
+            }
+          } else {
+            xv[i][0] = xv[i][1] = xv[i][2] = xv[i][3] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EB; ++e) {
+          if (e < E) {
+            const float4 wv = *reinterpret_cast<const float4*>(&ws[e][cl]);
+#pragma unroll
+            for (int i = 0; i < TB; ++i) {
+              float s = acc[i][e];
+              s = fmaf(xv[i][0], wv.x, s);
+              s = fmaf(xv[i][1], wv.y, s);
+              s = fmaf(xv[i][2], wv.z, s);
+              s = fmaf(xv[i][3], wv.w, s);
+              acc[i][e] = s;
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int e = 0; e < EB; ++e) acc[i][e] = warp_sum(acc[i][e]);
+  // lane i < TB finishes token t0 + i: softmax over E, top-k by (logit desc, id asc), gate weights
+#pragma unroll
+  for (int i = 0; i < TB; ++i) {
+    const int t = t0 + i;
+    if (lane != i || t >= T_) continue;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E) mx = fmaxf(mx, acc[i][e]);
+    float se = 0.f;
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E) se += expf(acc[i][e] - mx);
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E) probs[(size_t)t * E + e] = expf(acc[i][e] - mx) / se;
+    unsigned taken = 0;
+    float selv[8];
+    int seli[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= k) break;
+      float bv = -INFINITY;
+      int bi = -1;
+#pragma unroll
+      for (int e = 0; e < EB; ++e)  // ascending ids, strict '>' keeps the lowest id among equal logits
+        if (e < E && !((taken >> e) & 1u) && (bi < 0 || acc[i][e] > bv)) {
+          bv = acc[i][e];
+          bi = e;
+        }
+      taken |= 1u << bi;
+      selv[j] = bv;
+      seli[j] = bi;
+    }
+    float ev[8], sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k) {
+        ev[j] = renorm ? expf(selv[j] - selv[0]) : expf(selv[j] - mx) / se;
+        sum += ev[j];
+      }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k) {
+        const float wv = renorm ? ev[j] / sum : ev[j];
+        w[(size_t)t * k + j] = wv;
+        w_out[(size_t)t * k + j] = wv;
+        idx[(size_t)t * k + j] = seli[j];
+        idx_out[(size_t)t * k + j] = seli[j];
+      }
+  }
+}
+
 // Gate backward, per token: dl from dw (renormalized or raw softmax), then dx[t] += dl W_g.
 template <typename T>
 __global__ void __launch_bounds__(256) route_bwd_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
@@ -159,6 +283,134 @@ __global__ void __launch_bounds__(256) route_bwd_kernel(const float* __restrict_
   }
 }
 
+// Fast gate backward for E <= 32, d % 256 == 0: CTA = 32 tokens (4 per warp).  dl (renormalized:
+// w_j (dw_j - sum_i w_i dw_i); raw softmax: p (g - <p, g>)) is formed per token in shared memory, then
+// dx[t] += dl[t] W_g with W_g chunks staged in shared memory (each float4 read feeds 4 tokens).
+template <typename T, int EB>
+__global__ void __launch_bounds__(256) route_bwd_fast_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
+                                                             const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                                             const float* __restrict__ dw, int T_, int E, int d, int k,
+                                                             int renorm, float* __restrict__ dl, T* __restrict__ dx) {
+  constexpr int TB = 4, RC = 8192 / EB;
+  __shared__ __align__(16) float ws[EB][RC];
+  __shared__ float dls[32][EB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tb0 = blockIdx.x * 32;
+  // dl for the CTA's 32 tokens: thread (token lt, expert e)
+  for (int i = threadIdx.x; i < 32 * EB; i += blockDim.x) {
+    const int lt = i / EB, e = i % EB;
+    const int t = tb0 + lt;
+    float v = 0.f;
+    if (t < T_ && e < E) {
+      float s = 0.f, g = 0.f, wsel = 0.f;
+      bool sel = false;
+      for (int j = 0; j < k; ++j) {
+        const int ej = idx[(size_t)t * k + j];
+        const float dwj = dw[(size_t)t * k + j];
+        s += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
+        if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
+      }
+      v = renorm ? (sel ? wsel * (g - s) : 0.f) : probs[(size_t)t * E + e] * (g - s);
+      dl[(size_t)t * E + e] = v;
+    }
+    dls[lt][e] = v;
+  }
+  const int t0 = tb0 + wid * TB;
+  for (int c0 = 0; c0 < d; c0 += RC) {
+    const int rc = min(RC, d - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < E * (rc / 4); i += blockDim.x) {
+      const int e = i / (rc / 4), c = (i % (rc / 4)) * 4;
+      *reinterpret_cast<float4*>(&ws[e][c]) = *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c);
+    }
+    __syncthreads();
+    for (int s0 = 0; s0 < rc; s0 += 256) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int cl = s0 + half * 128 + lane * 4;
+        float acc[TB][4];
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int t = t0 + i;
+          if (t < T_) {
+            T* p = dx + (size_t)t * d + c0 + cl;
+            if constexpr (sizeof(T) == 2) {
+              const uint2 u = *reinterpret_cast<const uint2*>(p);
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+              acc[i][0] = a.x; acc[i][1] = a.y; acc[i][2] = b.x; acc[i][3] = b.y;
+            } else {
+              const float4 u = *reinterpret_cast<const float4*>(p);
+              acc[i][0] = u.x; acc[i][1] = u.y; acc[i][2] = u.z; acc[i][3] = u.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < EB; ++e) {
+          if (e < E) {
+            const float4 wv = *reinterpret_cast<const float4*>(&ws[e][cl]);
+#pragma unroll
+            for (int i = 0; i < TB; ++i) {
+              const float de = dls[wid * TB + i][e];
+              acc[i][0] = fmaf(de, wv.x, acc[i][0]);
+              acc[i][1] = fmaf(de, wv.y, acc[i][1]);
+              acc[i][2] = fmaf(de, wv.z, acc[i][2]);
+              acc[i][3] = fmaf(de, wv.w, acc[i][3]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < TB; ++i) {
+          const int t = t0 + i;
+          if (t < T_) {
+            T* p = dx + (size_t)t * d + c0 + cl;
+            if constexpr (sizeof(T) == 2) {
+              const __nv_bfloat162 a = __floats2bfloat162_rn(acc[i][0], acc[i][1]);
+              const __nv_bfloat162 b = __floats2bfloat162_rn(acc[i][2], acc[i][3]);
+              uint2 u;
+              u.x = *reinterpret_cast<const uint32_t*>(&a);
+              u.y = *reinterpret_cast<const uint32_t*>(&b);
+              *reinterpret_cast<uint2*>(p) = u;
+            } else {
+              *reinterpret_cast<float4*>(p) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// dW_g partials, fast path: CTA = (64 tokens, 256 columns); dl of the tile staged in shared memory,
+// x streamed with unrolled loads; part[p][e][col] for token tile p.
+template <typename T, int EB>
+__global__ void __launch_bounds__(256) wg_partial_fast_kernel(const float* __restrict__ dl, const T* __restrict__ x,
+                                                              int T_, int E, int d, float* __restrict__ part) {
+  constexpr int TT = 64;
+  __shared__ float dls[TT][EB];
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  const int p = blockIdx.y;
+  const int t0 = p * TT;
+  for (int i = threadIdx.x; i < TT * EB; i += 256) {
+    const int lt = i / EB, e = i % EB;
+    dls[lt][e] = (t0 + lt < T_ && e < E) ? dl[(size_t)(t0 + lt) * E + e] : 0.f;
+  }
+  __syncthreads();
+  float acc[EB];
+#pragma unroll
+  for (int e = 0; e < EB; ++e) acc[e] = 0.f;
+  const int nt = min(TT, T_ - t0);
+#pragma unroll 8
+  for (int lt = 0; lt < nt; ++lt) {
+    const float xv = to_f(x[(size_t)(t0 + lt) * d + col]);
+#pragma unroll
+    for (int e = 0; e < EB; ++e) acc[e] = fmaf(dls[lt][e], xv, acc[e]);
+  }
+#pragma unroll
+  for (int e = 0; e < EB; ++e)
+    if (e < E) part[((size_t)p * E + e) * d + col] = acc[e];
+}
+
 // dW_g partials: part p covers tokens [p*chunk, (p+1)*chunk); one thread per column, E accumulators.
 template <typename T, int EB>
 __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict__ dl, const T* __restrict__ x,
@@ -197,7 +449,21 @@ int route_dispatch(const luffy_layer* L, const void* x, const float* wg, int32_t
   int blocks = (L->T + warps_per_block - 1) / warps_per_block;
   blocks = blocks > 148 * 16 ? 148 * 16 : blocks;
   const T* xp = static_cast<const T*>(x);
-#define LUFFY_ROUTE(EBV)                                                                                   \
+  if (L->E <= 32 && L->d % 256 == 0) {
+    const int fb = (L->T + 31) / 32;
+    if (L->E <= 8)
+      route_fast_kernel<T, 8><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+                                                  idx_out, w_out);
+    else if (L->E <= 16)
+      route_fast_kernel<T, 16><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+                                                   idx_out, w_out);
+    else
+      route_fast_kernel<T, 32><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+                                                   idx_out, w_out);
+    LUFFY_LAUNCHED();
+    return 0;
+  }
+#define LUFFY_ROUTE(EBV)                                                                                 \
   route_kernel<T, EBV><<<blocks, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, \
                                               L->w, idx_out, w_out)
   if (L->E <= 32) LUFFY_ROUTE(32);
@@ -219,6 +485,37 @@ int launch_route(const luffy_layer* L, const void* x, const float* wg, int32_t* 
 
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
+  const bool fast = L->E <= 32 && L->d % 256 == 0;
+  if (fast) {
+    const int fb = (L->T + 31) / 32;
+    const int parts = (L->T + 63) / 64;
+    dim3 pg(L->d / 256, parts);
+#define LUFFY_RB(EBV)                                                                                               \
+  do {                                                                                                              \
+    if (L->dtype == LUFFY_BF16) {                                                                                   \
+      route_bwd_fast_kernel<bf16, EBV><<<fb, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k,  \
+                                                          L->renorm, L->dl, static_cast<bf16*>(dx));                \
+      LUFFY_LAUNCHED();                                                                                             \
+      wg_partial_fast_kernel<bf16, EBV><<<pg, 256, 0, st>>>(L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d,    \
+                                                           L->wg_part);                                             \
+    } else {                                                                                                        \
+      route_bwd_fast_kernel<float, EBV><<<fb, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, \
+                                                           L->renorm, L->dl, static_cast<float*>(dx));              \
+      LUFFY_LAUNCHED();                                                                                             \
+      wg_partial_fast_kernel<float, EBV><<<pg, 256, 0, st>>>(L->dl, static_cast<const float*>(x), L->T, L->E, L->d,  \
+                                                            L->wg_part);                                            \
+    }                                                                                                               \
+    LUFFY_LAUNCHED();                                                                                               \
+  } while (0)
+    if (L->E <= 8) LUFFY_RB(8);
+    else if (L->E <= 16) LUFFY_RB(16);
+    else LUFFY_RB(32);
+#undef LUFFY_RB
+    const int n = L->E * L->d;
+    wg_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(L->wg_part, parts, n, dwg);
+    LUFFY_LAUNCHED();
+    return 0;
+  }
   int blocks = (L->T + 7) / 8;
   blocks = blocks > 148 * 16 ? 148 * 16 : blocks;
   if (L->dtype == LUFFY_BF16)

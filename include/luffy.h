@@ -184,6 +184,15 @@ LUFFY_API luffy_status luffy_dispatch_bwd(luffy_layer* layer, const void* d_recv
 LUFFY_API luffy_status luffy_route_bwd(luffy_layer* layer, const void* x, const float* w_gate, const float* d_topk_w,
                              void* dx, float* dw_gate, void* stream);
 
+/* Host-side exchange plan of the dispatch/combine (used inside luffy_dispatch; exported for tests).
+ * counts_all [P][E] (host): representatives each source rank sends to each expert.  Outputs (host):
+ * send_off [E+1]  padded send layout of `rank` (expert asc, each segment rounded up to LUFFY_ROW_ALIGN);
+ * recv_off [E_l+1] padded expert layout of `rank` (local expert asc; within a segment source rank asc);
+ * send_rows_to [P] / recv_rows_from [P] (nullable): rows exchanged with each peer (self included). */
+LUFFY_API luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts_all,
+                                           int32_t* send_off, int32_t* recv_off, int64_t* send_rows_to,
+                                           int64_t* recv_rows_from);
+
 /* ---- debug export (tests) ----------------------------------------------------------------------- */
 
 typedef enum {
@@ -197,7 +206,8 @@ typedef enum {
   LUFFY_DBG_PERM = 7,      /* int32 [soff[E]] slot -> token (-1 padding) */
   LUFFY_DBG_POS = 8,       /* int32 [T, k]  slot of the representative of copy (t, j) */
   LUFFY_DBG_NREP = 9,      /* int32 [E]     representatives per expert */
-  LUFFY_DBG_ROUNDS = 10    /* uint32 [1]    greedy rounds of the last condense */
+  LUFFY_DBG_ROUNDS = 10,   /* uint32 [1]    greedy rounds of the last condense */
+  LUFFY_DBG_GREEDY_TIMES = 11 /* uint32 [64] greedy control block: [3] = #stamps, [8+2i..9+2i] = %globaltimer ns at barrier i */
 } luffy_debug_item;
 
 /* Synchronously copies an internal array of the layer's current forward to host memory `dst` (host).

@@ -271,6 +271,39 @@ using namespace luffy;
 extern "C" {
 
 const char* luffy_last_error(void) { return g_err.c_str(); }
+
+luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts_all,
+                                 int32_t* send_off, int32_t* recv_off, int64_t* send_rows_to, int64_t* recv_rows_from) {
+  if (world < 1 || rank < 0 || rank >= world || num_experts < 1 || num_experts % world)
+    return fail(LUFFY_E_INVALID, "exchange_plan: bad world/rank/num_experts");
+  LUFFY_NEED(counts_all);
+  LUFFY_NEED(send_off);
+  LUFFY_NEED(recv_off);
+  const int P = world, E = num_experts, El = E / world;
+  send_off[0] = 0;
+  for (int e = 0; e < E; ++e) {
+    const int32_t c = counts_all[(size_t)rank * E + e];
+    if (c < 0) return fail(LUFFY_E_INVALID, "exchange_plan: negative count");
+    send_off[e + 1] = send_off[e] + (int32_t)round_up(c, kRowAlign);
+  }
+  recv_off[0] = 0;
+  for (int el = 0; el < El; ++el) {
+    const int e = rank * El + el;
+    int64_t rows = 0;
+    for (int q = 0; q < P; ++q) rows += counts_all[(size_t)q * E + e];
+    recv_off[el + 1] = recv_off[el] + (int32_t)round_up(rows, kRowAlign);
+  }
+  for (int p = 0; p < P; ++p) {
+    int64_t so = 0, ri = 0;
+    for (int el = 0; el < El; ++el) {
+      so += counts_all[(size_t)rank * E + p * El + el];
+      ri += counts_all[(size_t)p * E + rank * El + el];
+    }
+    if (send_rows_to) send_rows_to[p] = so;
+    if (recv_rows_from) recv_rows_from[p] = ri;
+  }
+  return LUFFY_OK;
+}
 int64_t luffy_launch_count(void) { return g_launches.load(); }
 
 luffy_status luffy_get_unique_id(uint8_t id[128]) {
@@ -483,16 +516,8 @@ luffy_status luffy_dispatch(luffy_layer* L, const void* x, void* recv, int64_t* 
   LUFFY_NCCL(a->AllGather(L->nrep, L->cnt_all, L->E, nccl::kInt32, L->ctx->comm, st), "ncclAllGather(counts)");
   LUFFY_CHECK(cudaMemcpyAsync(L->cnt_all_h, L->cnt_all, sizeof(int32_t) * L->P * L->E, cudaMemcpyDeviceToHost, st), "counts D2H");
   LUFFY_CHECK(cudaStreamSynchronize(st), "counts sync");
-  const int32_t* cnt = L->cnt_all_h;
-  L->soff_h[0] = 0;
-  for (int e = 0; e < L->E; ++e) L->soff_h[e + 1] = L->soff_h[e] + (int32_t)round_up(cnt[(size_t)L->rank * L->E + e], kRowAlign);
-  L->roff_h[0] = 0;
-  for (int el = 0; el < L->El; ++el) {
-    const int e = L->rank * L->El + el;
-    int64_t rows = 0;
-    for (int q = 0; q < L->P; ++q) rows += cnt[(size_t)q * L->E + e];
-    L->roff_h[el + 1] = L->roff_h[el] + (int32_t)round_up(rows, kRowAlign);
-  }
+  luffy_status sp = luffy_exchange_plan(L->P, L->rank, L->E, L->cnt_all_h, L->soff_h, L->roff_h, nullptr, nullptr);
+  if (sp != LUFFY_OK) return sp;
   if (L->roff_h[L->El] > L->recv_max)
     return fail(LUFFY_E_CAPACITY, "dispatch: " + std::to_string(L->roff_h[L->El]) + " expert rows exceed max_recv_rows " +
                                       std::to_string(L->recv_max));
@@ -704,6 +729,7 @@ luffy_status luffy_debug_copy(luffy_layer* L, int32_t item, void* dst, size_t* b
     case LUFFY_DBG_POS: src = L->pos; n = sizeof(int32_t) * L->T * L->k; break;
     case LUFFY_DBG_NREP: src = L->nrep; n = sizeof(int32_t) * L->E; break;
     case LUFFY_DBG_ROUNDS: src = L->ctrl + 2; n = sizeof(uint32_t); break;
+    case LUFFY_DBG_GREEDY_TIMES: src = L->ctrl; n = sizeof(uint32_t) * 64; break;
     default: return fail(LUFFY_E_INVALID, "luffy_debug_copy: unknown item");
   }
   if (dst == nullptr || *bytes < n) {

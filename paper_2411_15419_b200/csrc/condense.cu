@@ -244,7 +244,22 @@ __global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int6
 // ---------------------------------------------------------------------------------------------------
 // Greedy representative selection by exact parallel 2-hop rounds (cooperative launch).
 
+__device__ __forceinline__ void stamp(uint32_t* ctrl) {
+  // phase timeline for the debug export: block 0 records %globaltimer (ns) at every barrier
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t i = ctrl[3];
+    if (i < 28) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ctrl[8 + 2 * i] = (uint32_t)t;
+      ctrl[9 + 2 * i] = (uint32_t)(t >> 32);
+      ctrl[3] = i + 1;
+    }
+  }
+}
+
 __device__ __forceinline__ void grid_barrier(uint32_t* ctrl) {
+  stamp(ctrl);
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile uint32_t* vgen = ctrl + 1;
@@ -306,55 +321,73 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
   for (int64_t r = gtid; r < rows; r += nthreads) a.rep_local[r] = -1;
   grid_barrier(a.ctrl);
 
+  // Two rows per warp (16 lanes per row); the row's alive bit, adjacency words and the alive words of
+  // its group are loaded together, so each phase costs ~2 dependent L2 round trips per row pair.
+  const int hl = lane & 15;
+  const int half = lane >> 4;
+  const int pairs = rows >> 1;
   int round = 0;
   for (;; ++round) {
     // ---- phase A: residual degree -> priority key (deg, -index)
-    for (int r = gwarp; r < rows; r += nwarps) {
-      const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
-      if (!alive) {
-        if (lane == 0) a.key[r] = 0ull;
+    for (int p = gwarp; p < pairs; p += nwarps) {
+      const int r = 2 * p + half;
+      const uint32_t aw = __ldcg(a.alive + (r >> 5));
+      const uint32_t pair_bits = (aw >> ((2 * p) & 31)) & 3u;
+      if (!pair_bits) {
+        if (hl == 0) a.key[r] = 0ull;
         continue;
       }
+      const bool me = (aw >> (r & 31)) & 1u;
       const int g = find_group(goff_s, E, r);
       const int rl = r - goff_s[g];
       const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
       const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
       const uint32_t* al = a.alive + (goff_s[g] >> 5);
       int deg = 0;
-      for (int wd = lane; wd < W; wd += 32) deg += __popc(row[wd] & __ldcg(al + wd));
+      if (me)
+        for (int wd = hl; wd < W; wd += 16) deg += __popc(row[wd] & __ldcg(al + wd));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
-      if (lane == 0) a.key[r] = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)rl);
+      for (int o = 8; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+      if (hl == 0)
+        a.key[r] = me ? ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)rl) : 0ull;
     }
     grid_barrier(a.ctrl);
-    // ---- phase B: m1 = max key over the alive closed neighbourhood;  phase C: m2 from m1
+    // ---- phase B: m1 = max key over the alive closed neighbourhood;  phase C: m2 from m1 -> winners
     for (int ph = 0; ph < 2; ++ph) {
       const unsigned long long* src = ph == 0 ? a.key : a.m1;
-      for (int r = gwarp; r < rows; r += nwarps) {
-        const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
-        if (!alive) continue;
+      for (int p = gwarp; p < pairs; p += nwarps) {
+        const int r = 2 * p + half;
+        const uint32_t aw = __ldcg(a.alive + (r >> 5));
+        if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
+        const bool me = (aw >> (r & 31)) & 1u;
         const int g = find_group(goff_s, E, r);
         const int rl = r - goff_s[g];
         const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
         const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
         const uint32_t* al = a.alive + (goff_s[g] >> 5);
-        unsigned long long m = __ldcg(src + r);
-        for (int wd = lane; wd < W; wd += 32) {
-          const uint32_t bits = row[wd] & __ldcg(al + wd);
-          if (bits) {
-            // independent predicated loads (not a dependent bit walk) so they are all in flight at once
-            const unsigned long long* p = src + goff_s[g] + wd * 32;
+        unsigned long long m = me ? __ldcg(src + r) : 0ull;
+        if (me) {
+          for (int wd = hl; wd < W; wd += 16) {
+            const uint32_t bits = row[wd] & __ldcg(al + wd);
+            if (bits) {
+              // independent predicated loads (not a dependent bit walk) so they are all in flight at once
+              const unsigned long long* q = src + goff_s[g] + wd * 32;
 #pragma unroll
-            for (int b = 0; b < 32; ++b) {
-              if ((bits >> b) & 1u) {
-                const unsigned long long v = __ldcg(p + b);
-                m = v > m ? v : m;
+              for (int b = 0; b < 32; ++b) {
+                if ((bits >> b) & 1u) {
+                  const unsigned long long v = __ldcg(q + b);
+                  m = v > m ? v : m;
+                }
               }
             }
           }
         }
-        m = warp_max_u64(m);
-        if (lane == 0) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+          m = u > m ? u : m;
+        }
+        if (hl == 0 && me) {
           if (ph == 0) a.m1[r] = m;
           else if (m == __ldcg(a.key + r)) atomicOr(a.win + (r >> 5), 1u << (r & 31));
         }
@@ -362,29 +395,28 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
       grid_barrier(a.ctrl);
     }
     // ---- phase D: winners and their alive neighbours leave; count the survivors
-    for (int r = gwarp; r < rows; r += nwarps) {
-      const bool alive = (__ldcg(a.alive + (r >> 5)) >> (r & 31)) & 1u;
-      if (!alive) continue;
+    for (int p = gwarp; p < pairs; p += nwarps) {
+      const int r = 2 * p + half;
+      const uint32_t aw = __ldcg(a.alive + (r >> 5));
+      if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
+      const bool me = (aw >> (r & 31)) & 1u;
       const int g = find_group(goff_s, E, r);
-      const bool winner = (__ldcg(a.win + (r >> 5)) >> (r & 31)) & 1u;
-      int owner = -1;
-      if (winner) {
-        owner = r;
-      } else {
+      const bool winner = me && ((__ldcg(a.win + (r >> 5)) >> (r & 31)) & 1u);
+      int found = 0x7fffffff;
+      if (me && !winner) {
         const int rl = r - goff_s[g];
         const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
         const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
         const uint32_t* wn = a.win + (goff_s[g] >> 5);
-        int found = 0x7fffffff;
-        for (int wd = lane; wd < W; wd += 32) {
+        for (int wd = hl; wd < W; wd += 16) {
           const uint32_t bits = row[wd] & __ldcg(wn + wd);
           if (bits) found = min(found, goff_s[g] + wd * 32 + __ffs(bits) - 1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
-        if (found != 0x7fffffff) owner = found;
       }
-      if (lane == 0) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
+      if (hl == 0 && me) {
+        const int owner = winner ? r : (found != 0x7fffffff ? found : -1);
         if (owner >= 0) {
           a.rep_local[r] = owner;
           atomicAnd(a.alive + (r >> 5), ~(1u << (r & 31)));
@@ -462,7 +494,7 @@ int launch_greedy(luffy_layer* L, void* s) {
     LUFFY_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, greedy_kernel, 256, 0));
     LUFFY_CUDA_TRY(cudaGetDevice(&dev));
     LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    blocks = std::max(1, std::min(per_sm, 4)) * sms;
+    blocks = std::max(1, std::min(per_sm, 8)) * sms;
   }
   GreedyArgs a;
   a.E = L->E;

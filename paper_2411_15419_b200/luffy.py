@@ -26,7 +26,7 @@ EXPORTED = [
     "luffy_layer_rows", "luffy_route", "luffy_condense", "luffy_dispatch", "luffy_expert_ffn",
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
-    "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm",
+    "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
 ]
 
 
@@ -85,6 +85,7 @@ def _load():
         "luffy_plan_migration": (I32, [ctypes.POINTER(MigrationProblem), P, P]),
         "luffy_attention_cost": (I64, [I64, I64, I64]),
         "luffy_debug_copy": (I32, [P, I32, P, ctypes.POINTER(SZ), P]),
+        "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -241,7 +242,7 @@ def luffy_attention_cost(B, L, d) -> int:
 
 DBG = dict(gcnt=(0, np.int32), goff=(1, np.int32), gtok=(2, np.int32), adjoff=(3, np.int64), adj=(4, np.uint32),
            rep_local=(5, np.int32), soff=(6, np.int32), perm=(7, np.int32), pos=(8, np.int32), nrep=(9, np.int32),
-           rounds=(10, np.uint32))
+           rounds=(10, np.uint32), greedy_times=(11, np.uint32))
 
 
 def luffy_debug_copy(layer, item: str, stream) -> np.ndarray:
@@ -257,3 +258,16 @@ def luffy_debug_copy(layer, item: str, stream) -> np.ndarray:
 def luffy_debug_gemm(kind, dtype, epi, A, B, B3, D, aux, D3, Msplit, off, G, max_rows, M, N, K, b_kmajor, stream):
     _check(LIB.luffy_debug_gemm(kind, dtype, epi, _p(A), _p(B), _p(B3), _p(D), _p(aux), _p(D3), Msplit, _p(off), G,
                                 max_rows, M, N, K, b_kmajor, stream))
+
+
+def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
+    """Host-side dispatch/combine plan: (send_off [E+1], recv_off [E_l+1], send_rows_to [P], recv_rows_from [P])."""
+    counts_all = np.ascontiguousarray(counts_all, dtype=np.int32)
+    El = num_experts // world
+    so = np.empty(num_experts + 1, np.int32)
+    ro = np.empty(El + 1, np.int32)
+    st = np.empty(world, np.int64)
+    rf = np.empty(world, np.int64)
+    _check(LIB.luffy_exchange_plan(world, rank, num_experts, counts_all.ctypes.data, so.ctypes.data, ro.ctypes.data,
+                                   st.ctypes.data, rf.ctypes.data))
+    return so, ro, st, rf

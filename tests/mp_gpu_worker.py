@@ -1,0 +1,110 @@
+"""torchrun worker for the multi-GPU parity test (one process per GPU, NCCL over NVLink).
+
+Every rank runs the condensed MoE layer fwd+bwd through the C ABI with world = N (expert parallel:
+E/N experts per rank, dispatch/combine via NCCL) on its own seeded tokens, then checks against the fp64
+oracle with the GPU's routing and representative maps frozen: its outputs Y, dX, dW_g and the gradients
+of its local experts (summed over the representatives of ALL ranks, gathered with all_gather_object).
+Exit code 0 = pass; one JSON line per rank."""
+import argparse
+import dataclasses
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import workload  # noqa: E402
+from oracle import luffy_oracle as O  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.abs(b).max()
+    return float(np.abs(a - b).max() / (den if den > 0 else 1.0))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2S")
+    ap.add_argument("--h", type=float, default=0.9)
+    args = ap.parse_args()
+    from paper_2411_15419_b200 import layer as LY
+    from paper_2411_15419_b200 import luffy as L
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    obj = [L.luffy_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    if args.config == "C2S":
+        cfg = dataclasses.replace(workload.CONFIGS["C2"], seqs_per_rank=2)
+    elif args.config == "C1":
+        cfg = workload.CONFIGS["C1"]          # fp32 (SIMT path) through NCCL
+    else:
+        cfg = dataclasses.replace(workload.CONFIGS[args.config], seqs_per_rank=1, seq_len=512)
+    E, El = cfg.num_experts, cfg.num_experts // world
+    inp = workload.make_layer_inputs(cfg, rank=rank)
+    T = inp["X"].shape[0]
+    tdt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    dt = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev, tdt)
+    loc = slice(rank * El, (rank + 1) * El)
+    x, dy = dt(inp["X"]), dt(inp["dY"])
+    wg = torch.from_numpy(inp["Wg"]).to(dev)
+    w1, w2 = dt(inp["W1"][loc]), dt(inp["W2"][loc])
+    w3 = dt(inp["W3"][loc]) if inp["W3"] is not None else None
+    lay = LY.CondensedMoELayer(E, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T, dtype=cfg.dtype, act=cfg.act,
+                               world=world, rank=rank, nccl_id=obj[0], device=dev)
+    y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True)
+    g = lay.backward(dy, x, wg, w1, w2, w3)
+    torch.cuda.synchronize()
+    idx = lay.idx[:T].cpu().numpy().astype(np.int64)
+    rep = lay.rep[:T].cpu().numpy().astype(np.int64)
+    # every rank's discrete decisions, to rebuild the expert-side sums
+    allmaps = [None] * world
+    dist.all_gather_object(allmaps, (idx, rep))
+    tol = 2e-2 if cfg.dtype == "bf16" else 1e-4
+    errs = {}
+    dW1 = np.zeros((El,) + inp["W1"].shape[1:])
+    dW2 = np.zeros((El,) + inp["W2"].shape[1:])
+    for q in range(world):
+        iq = workload.make_layer_inputs(cfg, rank=q)
+        r = O.route_with_idx(iq["X"], iq["Wg"], allmaps[q][0], cfg.renormalize)
+        st = O.layer_forward(iq["X"], iq["Wg"], iq["W1"], iq["W2"], iq["W3"], cfg.top_k, args.h, act=cfg.act,
+                             renormalize=cfg.renormalize, routing=r, rep=allmaps[q][1])
+        gr = O.layer_backward(st, iq["X"], iq["Wg"], iq["W1"], iq["W2"], iq["W3"], iq["dY"], act=cfg.act,
+                              renormalize=cfg.renormalize)
+        dW1 += gr.dW1[loc]
+        dW2 += gr.dW2[loc]
+        if q == rank:
+            errs["Y"] = rel(y.float().cpu().numpy(), st.Y)
+            errs["dx"] = rel(g["dx"].float().cpu().numpy(), gr.dX)
+            errs["dwg"] = rel(g["dwg"].cpu().numpy(), gr.dWg)
+            errs["dw"] = rel(g["dw"].cpu().numpy(), gr.dw)
+    errs["dw1"] = rel(g["dw1"].cpu().numpy(), dW1)
+    errs["dw2"] = rel(g["dw2"].cpu().numpy(), dW2)
+    # routing exact outside near-ties
+    rr = O.route(inp["X"], inp["Wg"], cfg.top_k, cfg.renormalize)
+    route_ok = bool(np.array_equal(idx[~rr.near_tie], rr.idx[~rr.near_tie]))
+    send_rows, recv_rows = L.luffy_layer_rows(lay.layer)
+    ok = route_ok and all(v <= tol for v in errs.values())
+    print(json.dumps({"rank": rank, "world": world, "ok": ok, "route_ok": route_ok, "errs": errs,
+                      "reps": int(lay.stats.reps), "copies": int(lay.stats.copies), "send_rows": send_rows,
+                      "recv_rows": recv_rows}), flush=True)
+    lay.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

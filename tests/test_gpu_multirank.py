@@ -1,0 +1,38 @@
+"""Multi-GPU parity (NCCL dispatch/combine over NVLink): torchrun with 2 (and 4 when available) ranks,
+each checked against the fp64 oracle by tests/mp_gpu_worker.py."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(n, config, h=0.9):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_gpu_worker.py"),
+           "--config", config, "--h", str(h)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    return r
+
+
+@pytest.mark.parametrize("n,config,h", [(2, "C2S", 0.9), (2, "C2S", 1.01), (2, "C1", 0.9), (4, "C2S", 0.9)])
+def test_expert_parallel_parity(n, config, h):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = _run(n, config, h)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"ok": true') == n

@@ -186,12 +186,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        obj = [L.luffy_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
     E, El = cfg.num_experts, cfg.num_experts // world
     inp = workload.make_layer_inputs(cfg, rank=rank)
     T = inp["X"].shape[0]
@@ -206,7 +202,7 @@ def main():
     w1, w2 = dev_t(W1), dev_t(W2)
     w3 = dev_t(W3) if W3 is not None else None
     lay = LY.CondensedMoELayer(E, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T, dtype=cfg.dtype, act=cfg.act,
-                               world=world, rank=rank, nccl_id=nccl_id, device=dev)
+                               world=world, rank=rank, device=dev)
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
     ev = lambda: torch.cuda.Event(enable_timing=True)

@@ -22,9 +22,19 @@
  *    layout (expert asc, then token asc, R15).  On the expert side (recv / expert_out) the segment of
  *    local expert e holds source rank 0's rows, then rank 1's, ... then zero padding.  With world == 1
  *    the two layouts coincide: recv == send, expert_out == gathered.
+ *  - world > 1 (expert parallel, one process per GPU): the exchange is device-initiated over NVLink.
+ *    luffy_layer_create allocates the layer's peer-visible exchange region (recv x2, gathered, d_expert,
+ *    d_send, counts, flags); the caller all-gathers the ranks' luffy_layer_ipc_handle blobs (e.g. with
+ *    torch.distributed) and passes them to luffy_layer_ipc_open.  The pack kernel, the GEMM2 / dgrad1
+ *    epilogues and the uncondense backward then store rows straight into the destination rank's buffer
+ *    and publish per-step sequence flags (system-scope release); consumers wait on the device (acquire),
+ *    so no host synchronisation is needed.  With world > 1 the expert-side and gathered buffer
+ *    arguments are NULL (the layer's exchange buffers are used; luffy_layer_exchange_buffers returns them).
+ *    All ranks must issue the same sequence of calls.
  *  - Errors: arguments are validated on the host before anything is enqueued; on failure a status is
- *    returned, nothing is launched and luffy_last_error() describes the problem.  CUDA / NCCL failures
- *    map to LUFFY_E_CUDA / LUFFY_E_NCCL.  Calling out of order returns LUFFY_E_STATE.
+ *    returned, nothing is launched and luffy_last_error() describes the problem.  CUDA failures map to
+ *    LUFFY_E_CUDA.  Calling out of order returns LUFFY_E_STATE.  A rank that stops participating makes the
+ *    others trap after a bounded wait (~20 s) instead of hanging.
  *  - Determinism: identical inputs give bitwise-identical outputs (no floating-point atomics).
  *  - Thread-compatibility: one thread at a time per luffy_ctx.
  * ------------------------------------------------------------------------------------------------- */
@@ -51,7 +61,7 @@ typedef enum {
   LUFFY_OK = 0,
   LUFFY_E_INVALID = 1,      /* bad argument (shape, alignment, null pointer, range) */
   LUFFY_E_CUDA = 2,         /* a CUDA runtime call failed */
-  LUFFY_E_NCCL = 3,         /* an NCCL call failed or NCCL could not be loaded */
+  LUFFY_E_NCCL = 3,         /* reserved (the exchange does not use NCCL) */
   LUFFY_E_CAPACITY = 4,     /* a receive / migration capacity would be exceeded (checked before any transfer) */
   LUFFY_E_UNSUPPORTED = 5,  /* configuration not supported by this build (e.g. no sm_100a device) */
   LUFFY_E_STATE = 6         /* call order violated (e.g. combine before dispatch) */
@@ -88,20 +98,29 @@ typedef struct {
 
 /* ---- lifetime ---------------------------------------------------------------------------------- */
 
-/* NCCL unique id for world > 1, produced on rank 0 and broadcast by the caller.  [sync] */
-LUFFY_API luffy_status luffy_get_unique_id(uint8_t id[128]);
-
-/* Validates cfg, selects the current CUDA device, and (world > 1) creates the NCCL communicator with
- * ncclCommInitRank(world, id, rank).  `nccl_id` (host, 128 bytes) may be NULL when world == 1.  [sync] */
-LUFFY_API luffy_status luffy_create(const luffy_config* cfg, const uint8_t* nccl_id, luffy_ctx** out);
+/* Validates cfg and binds the context to the current CUDA device (must be sm_100).  [sync] */
+LUFFY_API luffy_status luffy_create(const luffy_config* cfg, luffy_ctx** out);
 LUFFY_API void luffy_destroy(luffy_ctx* ctx);
 
 /* Bytes of device workspace one layer needs (saved state + scratch), a function of cfg only. */
 LUFFY_API size_t luffy_layer_workspace_bytes(const luffy_config* cfg);
 
-/* Binds a layer to `dev_workspace` (device, >= luffy_layer_workspace_bytes, 256-byte aligned). */
+/* Binds a layer to `dev_workspace` (device, >= luffy_layer_workspace_bytes, 256-byte aligned).  With
+ * world > 1 it also allocates the layer's exchange region (cudaMalloc; freed by luffy_layer_destroy).
+ * [sync] */
 LUFFY_API luffy_status luffy_layer_create(luffy_ctx* ctx, void* dev_workspace, size_t bytes, luffy_layer** out);
 LUFFY_API void luffy_layer_destroy(luffy_layer* layer);
+
+/* world > 1: size of one IPC handle blob; this rank's blob (host out[luffy_ipc_handle_bytes()]); and the
+ * mapping of every rank's region from the all-gathered blobs (host [world][bytes], rank order).  [sync] */
+LUFFY_API size_t luffy_ipc_handle_bytes(void);
+LUFFY_API luffy_status luffy_layer_ipc_handle(const luffy_layer* layer, uint8_t* out);
+LUFFY_API luffy_status luffy_layer_ipc_open(luffy_layer* layer, const uint8_t* all_handles);
+
+/* world > 1: the layer's exchange buffers for the current step (any pointer argument may be NULL):
+ * recv / d_expert_out [max_recv_rows, d] expert layout, gathered / d_send [send rows, d] send layout. */
+LUFFY_API luffy_status luffy_layer_exchange_buffers(const luffy_layer* layer, void** recv, void** gathered,
+                                                    void** d_expert_out, void** d_send);
 
 /* Thread-local description of the last failure. */
 LUFFY_API const char* luffy_last_error(void);
@@ -133,12 +152,12 @@ LUFFY_API luffy_status luffy_route(luffy_layer* layer, const void* x, const floa
 LUFFY_API luffy_status luffy_condense(luffy_layer* layer, const void* x, float h, int32_t* rep,
                             luffy_condense_stats* stats, void* stream);
 
-/* Dispatch phase: packs only the representatives into the send layout and, for
- * world > 1, exchanges counts (ncclAllGather) and rows (grouped ncclSend/ncclRecv) so that `recv`
- * [max_recv_rows, d] holds this rank's local-expert rows in the expert layout.  world == 1: `recv`
- * receives the packed rows directly (no communication).  *recv_rows (host) = padded rows written.
- * [sync] for world > 1 (the all-gathered counts are copied to the host to post the receives).
- * LUFFY_E_CAPACITY if the padded rows exceed max_recv_rows (checked before any transfer). */
+/* Dispatch phase: packs only the representatives.  world == 1: into `recv` (the send
+ * layout is the expert layout).  world > 1 (recv = NULL): the representative counts are pushed to every
+ * rank, every rank derives all layouts on the device, and one fused kernel copies each representative
+ * row from x straight into its expert's rank's receive buffer over NVLink; the call then waits (on the
+ * device) for every rank's rows.  recv_rows (host, nullable): padded expert-layout rows ([sync]).
+ * Capacity: max_recv_rows defaults to the worst case (every copy of every rank to this rank). */
 LUFFY_API luffy_status luffy_dispatch(luffy_layer* layer, const void* x, void* recv, int64_t* recv_rows, void* stream);
 
 /* Expert FFN ("expert networks that are essentially FFNs"; R12):
@@ -149,8 +168,10 @@ LUFFY_API luffy_status luffy_dispatch(luffy_layer* layer, const void* x, void* r
 LUFFY_API luffy_status luffy_expert_ffn(luffy_layer* layer, const void* recv, const void* w1, const void* w2,
                               const void* w3, void* out, void* saved_pre, void* saved_act, void* stream);
 
-/* Combine phase: returns expert outputs to the source ranks so that `gathered` [send rows, d]
- * is in this rank's send layout.  world == 1: gathered may alias expert_out (no-op) or is a copy. */
+/* Combine phase: expert outputs in this rank's send layout (`gathered`).  world == 1: gathered
+ * may alias expert_out (no-op) or is a copy.  world > 1: luffy_expert_ffn's GEMM2 epilogue already
+ * stored every row into its source rank's gathered buffer over NVLink (fused combine); this call waits
+ * for every rank's rows (expert_out and gathered may be NULL). */
 LUFFY_API luffy_status luffy_combine(luffy_layer* layer, const void* expert_out, void* gathered, void* stream);
 
 /* Output reuse, "use the expert output of token j to replace it" (R10):

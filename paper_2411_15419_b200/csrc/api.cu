@@ -1,5 +1,5 @@
 // C ABI of libluffy (include/luffy.h): context, workspace layout, argument validation, call order and
-// the expert-parallel exchange (NCCL over NVLink) between the kernels.
+// the device-initiated expert-parallel exchange over NVLink (CUDA IPC) between the kernels.
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -7,12 +7,11 @@
 #include <vector>
 
 #include "common.cuh"
-#include "nccl_shim.h"
+#include "exchange.cuh"
 
 struct luffy_ctx {
   luffy_config cfg;
   int device;
-  luffy::nccl::CommPtr comm;
 };
 
 namespace luffy {
@@ -27,11 +26,12 @@ luffy_status fail(luffy_status st, const std::string& msg) {
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int gemm_rows_simt(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0,
-                   const int32_t* off, int G, int64_t max_rows, int N, int K, int b_kmajor, void* s);
+                   const int32_t* off, int G, int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd,
+                   const XSignal* sig, void* s);
 int gemm_wgrad_simt(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G,
                     int M, int N, int lda, int ldb, void* s);
 int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
-                 int64_t max_rows, int N, int K, int b_kmajor, void* s);
+                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s);
 int gemm_wgrad_tc(const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M, int N,
                   int lda, int ldb, int64_t max_rows, void* s);
 int launch_pack_rows(luffy_layer* L, const void* x, void* dst_rows, void* s);
@@ -46,16 +46,6 @@ luffy_status cuda_fail(int err, const char* where) {
   do {                                                     \
     int _r = (expr);                                       \
     if (_r != 0) return cuda_fail(_r, where);              \
-  } while (0)
-
-luffy_status nccl_fail(nccl::Result r, const char* where) {
-  const nccl::Api* a = nccl::api();
-  return fail(LUFFY_E_NCCL, std::string(where) + ": " + (a ? a->GetErrorString(r) : "NCCL unavailable"));
-}
-#define LUFFY_NCCL(expr, where)                            \
-  do {                                                     \
-    nccl::Result _r = (expr);                              \
-    if (_r != 0) return nccl_fail(_r, where);              \
   } while (0)
 
 size_t elem_size(int dtype) { return dtype == LUFFY_BF16 ? 2 : 4; }
@@ -134,6 +124,18 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->roff = cv.take<int32_t>(m.El + 1);
   o->cnt_all = cv.take<int32_t>((size_t)m.P * m.E);
   o->send = m.P > 1 ? cv.take<char>(m.Rpad * m.d * es) : nullptr;
+  if (m.P > 1) {
+    o->x_peer_recv = cv.take<void*>(2 * m.P);
+    o->x_peer_gathered = cv.take<void*>(m.P);
+    o->x_peer_dexp = cv.take<void*>(m.P);
+    o->x_peer_dsend = cv.take<void*>(m.P);
+    o->x_peer_cnt = cv.take<int32_t*>(m.P);
+    o->x_flagptr = cv.take<uint32_t*>((size_t)XP_NUM * m.P);
+    o->x_dst_base = cv.take<int32_t>(m.E);
+    o->x_src_soff = cv.take<int32_t>((size_t)m.P * (m.E + 1));
+    o->x_rank_of = cv.take<int32_t>(m.recv);
+    o->x_slot_of = cv.take<int32_t>(m.recv);
+  }
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
   o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 63) / 64) * m.E * m.d);
 }
@@ -154,6 +156,7 @@ luffy_status validate(const luffy_config* c) {
     return fail(LUFFY_E_UNSUPPORTED, "bf16 (tcgen05) path needs d_model and d_ffn multiples of 256");
   const Dims m = dims_of(c);
   if (m.Cpad >= (int64_t)1 << 30) return fail(LUFFY_E_INVALID, "max_tokens * top_k too large");
+  if (c->world > kMaxWorld) return fail(LUFFY_E_INVALID, "world > 64 is not supported");
   if (c->world == 1 && c->max_recv_rows > 0 && c->max_recv_rows < m.Rpad)
     return fail(LUFFY_E_INVALID, "world == 1 needs max_recv_rows >= max_tokens*top_k + E*LUFFY_ROW_ALIGN (or 0)");
   return LUFFY_OK;
@@ -161,9 +164,10 @@ luffy_status validate(const luffy_config* c) {
 
 // bf16: tcgen05 tensor cores; fp32: exact SIMT FFMA (tf32 would break the fp32 tolerance).
 int gemm_rows(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off,
-              int G, int64_t max_rows, int N, int K, int b_kmajor, void* s) {
-  if (dtype == LUFFY_BF16) return gemm_rows_tc(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, s);
-  return gemm_rows_simt(dtype, epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, s);
+              int G, int64_t max_rows, int N, int K, int b_kmajor, void* s, const XRedirect* rd = nullptr,
+              const XSignal* sig = nullptr) {
+  if (dtype == LUFFY_BF16) return gemm_rows_tc(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, s);
+  return gemm_rows_simt(dtype, epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, s);
 }
 int gemm_wgrad(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M,
                int N, int lda, int ldb, int64_t max_rows, void* s) {
@@ -192,76 +196,39 @@ luffy_status need(const void* p, const char* name) {
 
 // Expert-side row offsets for the GEMMs: with one rank the send layout is the expert layout.
 const int32_t* expert_off(const luffy_layer* L) { return L->P == 1 ? L->soff : L->roff; }
-int64_t expert_rows_bound(const luffy_layer* L) { return L->P == 1 ? L->Rpad_max : L->recv_rows_h; }
+int64_t expert_rows_bound(const luffy_layer* L) { return L->P == 1 ? L->Rpad_max : L->recv_max; }
 
-// One grouped exchange.  dir 0: source->expert (dispatch / combine_bwd): src rows at send offsets
-// `soff_h` (this rank's counts), dst rows in the expert layout.  dir 1: the reverse.
-luffy_status exchange(luffy_layer* L, int dir, const void* src, void* dst, cudaStream_t st) {
-  const nccl::Api* a = nccl::api();
-  if (!a) return fail(LUFFY_E_NCCL, "NCCL could not be loaded (libnccl.so.2)");
+// Exchange region layout (identical offsets on every rank).
+struct XLayout {
+  size_t recv[2], gathered, dexp, dsend, cnt, flags, counters, total;
+};
+XLayout xlayout(const luffy_layer* L) {
   const size_t rb = (size_t)L->d * elem_size(L->dtype);
-  const int P = L->P, E = L->E, El = L->El, me = L->rank;
-  const int32_t* cnt = L->cnt_all_h;
-  auto expert_row = [&](int e, int srcrank) {  // row of (srcrank's block of expert e) at its owner
-    const int el = e % El;
-    int64_t r = L->roff_h[el];
-    for (int q = 0; q < srcrank; ++q) r += cnt[(size_t)q * E + e];
-    return r;
-  };
-  const char* s = static_cast<const char*>(src);
-  char* d = static_cast<char*>(dst);
-  LUFFY_NCCL(a->GroupStart(), "ncclGroupStart");
-  for (int p = 0; p < P; ++p) {
-    for (int el = 0; el < El; ++el) {
-      if (dir == 0) {
-        // I send my rows for expert e = p*El + el to p; I receive p's rows for my expert me*El + el.
-        const int e_out = p * El + el, e_in = me * El + el;
-        const size_t n_out = cnt[(size_t)me * E + e_out], n_in = cnt[(size_t)p * E + e_in];
-        const char* sp = s + (size_t)L->soff_h[e_out] * rb;
-        char* dp = d + (size_t)expert_row(e_in, p) * rb;
-        if (p == me) {
-          if (n_out) {
-            cudaError_t ce = cudaMemcpyAsync(d + (size_t)expert_row(e_out, me) * rb, sp, n_out * rb, cudaMemcpyDeviceToDevice, st);
-            if (ce != cudaSuccess) { a->GroupEnd(); return cuda_fail(ce, "exchange self copy"); }
-          }
-          continue;
-        }
-        if (n_out) LUFFY_NCCL(a->Send(sp, n_out * rb, nccl::kUint8, p, L->ctx->comm, st), "ncclSend");
-        if (n_in) LUFFY_NCCL(a->Recv(dp, n_in * rb, nccl::kUint8, p, L->ctx->comm, st), "ncclRecv");
-      } else {
-        // I send p's rows of my expert me*El + el back to p; I receive my rows of expert p*El + el.
-        const int e_out = me * El + el, e_in = p * El + el;
-        const size_t n_out = cnt[(size_t)p * E + e_out], n_in = cnt[(size_t)me * E + e_in];
-        const char* sp = s + (size_t)expert_row(e_out, p) * rb;
-        char* dp = d + (size_t)L->soff_h[e_in] * rb;
-        if (p == me) {
-          if (n_in) {
-            cudaError_t ce = cudaMemcpyAsync(dp, s + (size_t)expert_row(e_in, me) * rb, n_in * rb, cudaMemcpyDeviceToDevice, st);
-            if (ce != cudaSuccess) { a->GroupEnd(); return cuda_fail(ce, "exchange self copy"); }
-          }
-          continue;
-        }
-        if (n_out) LUFFY_NCCL(a->Send(sp, n_out * rb, nccl::kUint8, p, L->ctx->comm, st), "ncclSend");
-        if (n_in) LUFFY_NCCL(a->Recv(dp, n_in * rb, nccl::kUint8, p, L->ctx->comm, st), "ncclRecv");
-      }
-    }
-  }
-  LUFFY_NCCL(a->GroupEnd(), "ncclGroupEnd");
-  return LUFFY_OK;
+  XLayout x;
+  size_t o = 0;
+  auto take = [&](size_t n) { o = (o + 255) / 256 * 256; size_t r = o; o += n; return r; };
+  x.recv[0] = take((size_t)L->recv_max * rb);
+  x.recv[1] = take((size_t)L->recv_max * rb);
+  x.gathered = take((size_t)L->Rpad_max * rb);
+  x.dexp = take((size_t)L->recv_max * rb);
+  x.dsend = take((size_t)L->Rpad_max * rb);
+  x.cnt = take(sizeof(int32_t) * L->P * L->E);
+  x.flags = take(sizeof(uint32_t) * XP_NUM * L->P);
+  x.counters = take(sizeof(uint32_t) * XP_NUM);
+  x.total = (o + 4095) / 4096 * 4096;
+  return x;
 }
 
-// Zero the padding rows of an expert-layout buffer (host-known layout, world > 1).
-luffy_status zero_expert_padding(luffy_layer* L, void* buf, cudaStream_t st) {
-  const size_t rb = (size_t)L->d * elem_size(L->dtype);
-  for (int el = 0; el < L->El; ++el) {
-    const int e = L->rank * L->El + el;
-    int64_t used = 0;
-    for (int q = 0; q < L->P; ++q) used += L->cnt_all_h[(size_t)q * L->E + e];
-    const int64_t r0 = L->roff_h[el] + used, r1 = L->roff_h[el + 1];
-    if (r1 > r0) LUFFY_CHECK(cudaMemsetAsync(static_cast<char*>(buf) + r0 * rb, 0, (r1 - r0) * rb, st), "memset padding");
-  }
+luffy_status need_open(const luffy_layer* L, const char* where) {
+  if (L->P > 1 && !L->x_open)
+    return fail(LUFFY_E_STATE, std::string(where) + ": world > 1 needs luffy_layer_ipc_open first");
   return LUFFY_OK;
 }
+#define LUFFY_OPEN(L, where)                             \
+  do {                                                   \
+    luffy_status _s = need_open((L), (where));           \
+    if (_s != LUFFY_OK) return _s;                       \
+  } while (0)
 
 }  // namespace
 }  // namespace luffy
@@ -306,17 +273,7 @@ luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_expert
 }
 int64_t luffy_launch_count(void) { return g_launches.load(); }
 
-luffy_status luffy_get_unique_id(uint8_t id[128]) {
-  if (!id) return fail(LUFFY_E_INVALID, "id is NULL");
-  const nccl::Api* a = nccl::api();
-  if (!a) return fail(LUFFY_E_NCCL, "NCCL could not be loaded (libnccl.so.2)");
-  nccl::UniqueId u;
-  LUFFY_NCCL(a->GetUniqueId(&u), "ncclGetUniqueId");
-  std::memcpy(id, u.internal, 128);
-  return LUFFY_OK;
-}
-
-luffy_status luffy_create(const luffy_config* cfg, const uint8_t* nccl_id, luffy_ctx** out) {
+luffy_status luffy_create(const luffy_config* cfg, luffy_ctx** out) {
   luffy_status st = validate(cfg);
   if (st != LUFFY_OK) return st;
   LUFFY_NEED(out);
@@ -331,37 +288,11 @@ luffy_status luffy_create(const luffy_config* cfg, const uint8_t* nccl_id, luffy
   c->cfg = *cfg;
   if (c->cfg.renormalize < 0) c->cfg.renormalize = cfg->top_k > 1 ? 1 : 0;
   c->device = dev;
-  c->comm = nullptr;
-  if (cfg->world > 1) {
-    if (!nccl_id) {
-      delete c;
-      return fail(LUFFY_E_INVALID, "world > 1 needs an NCCL unique id");
-    }
-    const nccl::Api* a = nccl::api();
-    if (!a) {
-      delete c;
-      return fail(LUFFY_E_NCCL, "NCCL could not be loaded (libnccl.so.2)");
-    }
-    nccl::UniqueId u;
-    std::memcpy(u.internal, nccl_id, 128);
-    nccl::Result r = a->CommInitRank(&c->comm, cfg->world, u, cfg->rank);
-    if (r != 0) {
-      delete c;
-      return nccl_fail(r, "ncclCommInitRank");
-    }
-  }
   *out = c;
   return LUFFY_OK;
 }
 
-void luffy_destroy(luffy_ctx* ctx) {
-  if (!ctx) return;
-  if (ctx->comm) {
-    const nccl::Api* a = nccl::api();
-    if (a) a->CommDestroy(ctx->comm);
-  }
-  delete ctx;
-}
+void luffy_destroy(luffy_ctx* ctx) { delete ctx; }
 
 size_t luffy_layer_workspace_bytes(const luffy_config* cfg) {
   if (validate(cfg) != LUFFY_OK) return 0;
@@ -399,12 +330,27 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   L->Rpad_max = m.Rpad;
   L->recv_max = m.recv;
   L->adj_words_max = m.adjw;
-  cudaError_t e1 = cudaMallocHost(&L->cnt_all_h, sizeof(int32_t) * m.P * m.E);
-  cudaError_t e2 = cudaMallocHost(&L->roff_h, sizeof(int32_t) * (m.El + 1));
-  cudaError_t e3 = cudaMallocHost(&L->soff_h, sizeof(int32_t) * (m.E + 1));
-  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
-    luffy_layer_destroy(L);
-    return fail(LUFFY_E_CUDA, "cudaMallocHost failed");
+  if (L->P > 1) {
+    // the peer-visible exchange region: allocated once here, mapped by the peers via CUDA IPC
+    const XLayout xl = xlayout(L);
+    L->x_region_bytes = xl.total;
+    cudaError_t e = cudaMalloc(&L->x_region, xl.total);
+    if (e == cudaSuccess) e = cudaMemset(L->x_region, 0, xl.total);
+    cudaIpcMemHandle_t h;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, L->x_region);
+    if (e != cudaSuccess) {
+      luffy_layer_destroy(L);
+      return cuda_fail(e, "exchange region (cudaMalloc / cudaIpcGetMemHandle)");
+    }
+    std::memcpy(L->x_handle, &h, sizeof(h));
+    L->x_recv[0] = L->x_region + xl.recv[0];
+    L->x_recv[1] = L->x_region + xl.recv[1];
+    L->x_gathered = L->x_region + xl.gathered;
+    L->x_dexp = L->x_region + xl.dexp;
+    L->x_dsend = L->x_region + xl.dsend;
+    L->x_cnt_inbox = reinterpret_cast<int32_t*>(L->x_region + xl.cnt);
+    L->x_flags = reinterpret_cast<uint32_t*>(L->x_region + xl.flags);
+    L->x_counters = reinterpret_cast<uint32_t*>(L->x_region + xl.counters);
   }
   *out = L;
   return LUFFY_OK;
@@ -412,17 +358,79 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
 
 void luffy_layer_destroy(luffy_layer* L) {
   if (!L) return;
-  if (L->cnt_all_h) cudaFreeHost(L->cnt_all_h);
-  if (L->roff_h) cudaFreeHost(L->roff_h);
-  if (L->soff_h) cudaFreeHost(L->soff_h);
+  if (L->x_open)
+    for (int p = 0; p < L->P; ++p)
+      if (p != L->rank && L->x_peer_base_h[p]) cudaIpcCloseMemHandle(L->x_peer_base_h[p]);
+  if (L->x_region) cudaFree(L->x_region);
   delete L;
+}
+
+size_t luffy_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+luffy_status luffy_layer_ipc_handle(const luffy_layer* L, uint8_t* out) {
+  LUFFY_NEED(L);
+  LUFFY_NEED(out);
+  if (L->P == 1) return fail(LUFFY_E_STATE, "luffy_layer_ipc_handle: world == 1 has no exchange region");
+  std::memcpy(out, L->x_handle, sizeof(cudaIpcMemHandle_t));
+  return LUFFY_OK;
+}
+
+luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
+  LUFFY_NEED(L);
+  LUFFY_NEED(all_handles);
+  if (L->P == 1) return LUFFY_OK;
+  if (L->x_open) return fail(LUFFY_E_STATE, "luffy_layer_ipc_open: already open");
+  const XLayout xl = xlayout(L);
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  for (int p = 0; p < L->P; ++p) {
+    if (p == L->rank) {
+      if (std::memcmp(all_handles + p * hb, L->x_handle, hb) != 0)
+        return fail(LUFFY_E_INVALID, "luffy_layer_ipc_open: entry of this rank is not its own handle");
+      L->x_peer_base_h[p] = L->x_region;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, all_handles + p * hb, hb);
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    L->x_peer_base_h[p] = base;
+  }
+  // device tables of peer addresses
+  const int P = L->P;
+  std::vector<void*> recv(2 * P), gath(P), dexp(P), dsend(P);
+  std::vector<int32_t*> cnt(P);
+  std::vector<uint32_t*> flag((size_t)XP_NUM * P);
+  for (int p = 0; p < P; ++p) {
+    char* b = static_cast<char*>(L->x_peer_base_h[p]);
+    recv[p] = b + xl.recv[0];
+    recv[P + p] = b + xl.recv[1];
+    gath[p] = b + xl.gathered;
+    dexp[p] = b + xl.dexp;
+    dsend[p] = b + xl.dsend;
+    cnt[p] = reinterpret_cast<int32_t*>(b + xl.cnt);
+    for (int ph = 0; ph < XP_NUM; ++ph)
+      flag[(size_t)ph * P + p] = reinterpret_cast<uint32_t*>(b + xl.flags) + ph * P + L->rank;
+  }
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_recv, recv.data(), sizeof(void*) * 2 * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_gathered, gath.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_dexp, dexp.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_dsend, dsend.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_cnt, cnt.data(), sizeof(int32_t*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_flagptr, flag.data(), sizeof(uint32_t*) * XP_NUM * P, cudaMemcpyHostToDevice), "ipc tables");
+  L->x_open = true;
+  return LUFFY_OK;
 }
 
 luffy_status luffy_layer_rows(const luffy_layer* L, int64_t* send_rows, int64_t* recv_rows) {
   LUFFY_NEED(L);
   LUFFY_STAGE(L, 3, "luffy_layer_rows");
-  if (send_rows) *send_rows = L->send_rows_h;
-  if (recv_rows) *recv_rows = L->recv_rows_h;
+  int32_t so = 0, ro = 0;
+  LUFFY_CHECK(cudaMemcpy(&so, L->soff + L->E, sizeof(int32_t), cudaMemcpyDeviceToHost), "rows");
+  LUFFY_CHECK(cudaMemcpy(&ro, (L->P == 1 ? L->soff + L->E : L->roff + L->El), sizeof(int32_t), cudaMemcpyDeviceToHost),
+              "rows");
+  if (send_rows) *send_rows = so;
+  if (recv_rows) *recv_rows = ro;
   return LUFFY_OK;
 }
 
@@ -440,6 +448,7 @@ luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int
   if (T < 1 || T > L->Tmax) return fail(LUFFY_E_INVALID, "need 0 < T <= max_tokens");
   L->T = T;
   L->stage = 0;
+  L->seq += 1;  // a new forward step (every rank calls in lockstep)
   LUFFY_CHECK(launch_route(L, x, w_gate, topk_idx, topk_w, stream), "luffy_route");
   L->stage = 1;
   return LUFFY_OK;
@@ -487,65 +496,80 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
   return LUFFY_OK;
 }
 
+// world > 1: the layer's own exchange buffers are the only valid expert-side / gathered buffers; the
+// caller passes NULL (or the same pointer, from luffy_layer_exchange_buffers).
+static luffy_status own_or_null(const void* given, const void* own, const char* name) {
+  if (given != nullptr && given != own)
+    return fail(LUFFY_E_INVALID, std::string(name) + ": with world > 1 pass NULL (the layer's exchange buffer is used)");
+  return LUFFY_OK;
+}
+#define LUFFY_OWN(given, own, name)                               \
+  do {                                                            \
+    luffy_status _s = own_or_null((given), (own), (name));        \
+    if (_s != LUFFY_OK) return _s;                                \
+  } while (0)
+
+luffy_status luffy_layer_exchange_buffers(const luffy_layer* L, void** recv, void** gathered, void** d_expert_out,
+                                          void** d_send) {
+  LUFFY_NEED(L);
+  if (L->P == 1) return fail(LUFFY_E_STATE, "luffy_layer_exchange_buffers: world == 1 uses caller buffers");
+  if (recv) *recv = L->x_recv[L->seq & 1];
+  if (gathered) *gathered = L->x_gathered;
+  if (d_expert_out) *d_expert_out = L->x_dexp;
+  if (d_send) *d_send = L->x_dsend;
+  return LUFFY_OK;
+}
+
 luffy_status luffy_dispatch(luffy_layer* L, const void* x, void* recv, int64_t* recv_rows, void* stream) {
   LUFFY_NEED(L);
   LUFFY_NEED(x);
-  LUFFY_NEED(recv);
   LUFFY_ALIGNED(x);
-  LUFFY_ALIGNED(recv);
   LUFFY_STAGE(L, 2, "luffy_dispatch");
+  LUFFY_OPEN(L, "luffy_dispatch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (L->P == 1) {
+    LUFFY_NEED(recv);
+    LUFFY_ALIGNED(recv);
     LUFFY_CHECK(launch_pack_rows(L, x, recv, stream), "luffy_dispatch/pack");
-    if (recv_rows) {
-      int32_t r = 0;
-      LUFFY_CHECK(cudaMemcpyAsync(&r, L->soff + L->E, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "rows");
-      LUFFY_CHECK(cudaStreamSynchronize(st), "rows sync");
-      L->send_rows_h = L->recv_rows_h = r;
-      *recv_rows = r;
-    } else {
-      L->send_rows_h = L->recv_rows_h = L->Rpad_max;  // upper bound (no host sync at world == 1)
-    }
-    L->stage = 3;
-    return LUFFY_OK;
+  } else {
+    LUFFY_OWN(recv, L->x_recv[L->seq & 1], "luffy_dispatch recv");
+    LUFFY_CHECK(launch_xdispatch(L, x, stream), "luffy_dispatch/exchange");
   }
-  const nccl::Api* a = nccl::api();
-  if (!a) return fail(LUFFY_E_NCCL, "NCCL could not be loaded (libnccl.so.2)");
-  LUFFY_CHECK(launch_pack_rows(L, x, L->send, stream), "luffy_dispatch/pack");
-  // counts of representatives per expert from every rank (1 KiB), then the host posts the receives
-  LUFFY_NCCL(a->AllGather(L->nrep, L->cnt_all, L->E, nccl::kInt32, L->ctx->comm, st), "ncclAllGather(counts)");
-  LUFFY_CHECK(cudaMemcpyAsync(L->cnt_all_h, L->cnt_all, sizeof(int32_t) * L->P * L->E, cudaMemcpyDeviceToHost, st), "counts D2H");
-  LUFFY_CHECK(cudaStreamSynchronize(st), "counts sync");
-  luffy_status sp = luffy_exchange_plan(L->P, L->rank, L->E, L->cnt_all_h, L->soff_h, L->roff_h, nullptr, nullptr);
-  if (sp != LUFFY_OK) return sp;
-  if (L->roff_h[L->El] > L->recv_max)
-    return fail(LUFFY_E_CAPACITY, "dispatch: " + std::to_string(L->roff_h[L->El]) + " expert rows exceed max_recv_rows " +
-                                      std::to_string(L->recv_max));
-  L->send_rows_h = L->soff_h[L->E];
-  L->recv_rows_h = L->roff_h[L->El];
-  LUFFY_CHECK(cudaMemcpyAsync(L->roff, L->roff_h, sizeof(int32_t) * (L->El + 1), cudaMemcpyHostToDevice, st), "roff H2D");
-  luffy_status s2 = zero_expert_padding(L, recv, st);
-  if (s2 != LUFFY_OK) return s2;
-  s2 = exchange(L, 0, L->send, recv, st);
-  if (s2 != LUFFY_OK) return s2;
-  if (recv_rows) *recv_rows = L->recv_rows_h;
   L->stage = 3;
+  if (recv_rows) {
+    int32_t r = 0;
+    LUFFY_CHECK(cudaMemcpyAsync(&r, L->P == 1 ? L->soff + L->E : L->roff + L->El, sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st), "rows");
+    LUFFY_CHECK(cudaStreamSynchronize(st), "rows sync");
+    *recv_rows = r;
+  }
   return LUFFY_OK;
 }
 
 luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, const void* w2, const void* w3, void* out,
                               void* saved_pre, void* saved_act, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(recv);
   LUFFY_NEED(w1);
   LUFFY_NEED(w2);
-  LUFFY_NEED(out);
   LUFFY_NEED(saved_pre);
   LUFFY_NEED(saved_act);
   LUFFY_STAGE(L, 3, "luffy_expert_ffn");
   if (L->act == LUFFY_SWIGLU && !w3) return fail(LUFFY_E_INVALID, "SWIGLU needs w3");
   const int32_t* off = expert_off(L);
   const int64_t rows = expert_rows_bound(L);
+  XRedirect rd{};
+  XSignal sig{};
+  if (L->P == 1) {
+    LUFFY_NEED(recv);
+    LUFFY_NEED(out);
+  } else {
+    LUFFY_OWN(recv, L->x_recv[L->seq & 1], "luffy_expert_ffn recv");
+    recv = L->x_recv[L->seq & 1];
+    rd.rank_of = L->x_rank_of;  // fused combine: GEMM2 rows go to their source rank's gathered buffer
+    rd.slot_of = L->x_slot_of;
+    rd.peer_base = L->x_peer_gathered;
+    sig = make_signal(L, XP_COMB);
+  }
   if (L->act == LUFFY_GELU) {
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_GELU, recv, w1, nullptr, saved_act, saved_pre, off, L->El, rows, L->f, L->d, 1, stream),
                 "expert_ffn/gemm1");
@@ -553,7 +577,8 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_SWIGLU, recv, w1, w3, saved_act, saved_pre, off, L->El, rows, 2 * L->f, L->d, 1, stream),
                 "expert_ffn/gemm1");
   }
-  LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, saved_act, w2, nullptr, out, nullptr, off, L->El, rows, L->d, L->f, 1, stream),
+  LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, saved_act, w2, nullptr, out, nullptr, off, L->El, rows, L->d, L->f, 1, stream,
+                        L->P > 1 ? &rd : nullptr, L->P > 1 ? &sig : nullptr),
               "expert_ffn/gemm2");
   if (L->stage < 4) L->stage = 4;
   return LUFFY_OK;
@@ -561,17 +586,18 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
 
 luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathered, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(expert_out);
-  LUFFY_NEED(gathered);
   LUFFY_STAGE(L, 4, "luffy_combine");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (L->P == 1) {
+    LUFFY_NEED(expert_out);
+    LUFFY_NEED(gathered);
     if (gathered != expert_out)
-      LUFFY_CHECK(cudaMemcpyAsync(gathered, expert_out, (size_t)L->send_rows_h * L->d * elem_size(L->dtype),
+      LUFFY_CHECK(cudaMemcpyAsync(gathered, expert_out, (size_t)L->Rpad_max * L->d * elem_size(L->dtype),
                                   cudaMemcpyDeviceToDevice, st), "combine copy");
   } else {
-    luffy_status s2 = exchange(L, 1, expert_out, gathered, st);
-    if (s2 != LUFFY_OK) return s2;
+    // the rows were pushed by the experts' GEMM2 epilogues; wait until every rank has published them
+    LUFFY_OWN(gathered, L->x_gathered, "luffy_combine gathered");
+    LUFFY_CHECK(launch_xwait(L, XP_COMB, stream), "luffy_combine/wait");
   }
   L->stage = 5;
   return LUFFY_OK;
@@ -579,10 +605,15 @@ luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathere
 
 luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(gathered);
   LUFFY_NEED(y);
   LUFFY_ALIGNED(y);
   LUFFY_STAGE(L, 5, "luffy_uncondense");
+  if (L->P == 1) {
+    LUFFY_NEED(gathered);
+  } else {
+    LUFFY_OWN(gathered, L->x_gathered, "luffy_uncondense gathered");
+    gathered = L->x_gathered;
+  }
   LUFFY_CHECK(launch_uncondense(L, gathered, y, stream), "luffy_uncondense");
   L->stage = 6;
   return LUFFY_OK;
@@ -594,44 +625,46 @@ luffy_status luffy_uncondense_bwd(luffy_layer* L, const void* dy, const void* ga
                                   void* stream) {
   LUFFY_NEED(L);
   LUFFY_NEED(dy);
-  LUFFY_NEED(gathered);
-  LUFFY_NEED(d_gathered);
   LUFFY_NEED(d_topk_w);
   LUFFY_ALIGNED(dy);
   LUFFY_STAGE(L, 6, "luffy_uncondense_bwd");
+  if (L->P == 1) {
+    LUFFY_NEED(gathered);
+    LUFFY_NEED(d_gathered);
+  } else {
+    LUFFY_OWN(gathered, L->x_gathered, "luffy_uncondense_bwd gathered");
+    if (d_gathered) return fail(LUFFY_E_INVALID, "luffy_uncondense_bwd: with world > 1 pass d_gathered = NULL");
+    gathered = L->x_gathered;  // (the rows go straight to the experts' ranks: fused combine backward)
+  }
   LUFFY_CHECK(launch_uncondense_bwd(L, dy, gathered, d_gathered, d_topk_w, stream), "luffy_uncondense_bwd");
   return LUFFY_OK;
 }
 
 luffy_status luffy_combine_bwd(luffy_layer* L, const void* d_gathered, void* d_expert_out, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(d_gathered);
-  LUFFY_NEED(d_expert_out);
   LUFFY_STAGE(L, 6, "luffy_combine_bwd");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (L->P == 1) {
+    LUFFY_NEED(d_gathered);
+    LUFFY_NEED(d_expert_out);
     if (d_gathered != d_expert_out)
-      LUFFY_CHECK(cudaMemcpyAsync(d_expert_out, d_gathered, (size_t)L->send_rows_h * L->d * elem_size(L->dtype),
+      LUFFY_CHECK(cudaMemcpyAsync(d_expert_out, d_gathered, (size_t)L->Rpad_max * L->d * elem_size(L->dtype),
                                   cudaMemcpyDeviceToDevice, st), "combine_bwd copy");
     return LUFFY_OK;
   }
-  luffy_status s2 = zero_expert_padding(L, d_expert_out, st);
-  if (s2 != LUFFY_OK) return s2;
-  return exchange(L, 0, d_gathered, d_expert_out, st);
+  LUFFY_OWN(d_expert_out, L->x_dexp, "luffy_combine_bwd d_expert_out");
+  return launch_xwait(L, XP_CBWD, stream) ? fail(LUFFY_E_CUDA, "luffy_combine_bwd/wait") : LUFFY_OK;
 }
 
 luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void* recv, const void* w1, const void* w2,
                                   const void* w3, const void* saved_pre, const void* saved_act, void* scratch_dpre,
                                   void* d_recv, float* dw1, float* dw2, float* dw3, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(d_out);
-  LUFFY_NEED(recv);
   LUFFY_NEED(w1);
   LUFFY_NEED(w2);
   LUFFY_NEED(saved_pre);
   LUFFY_NEED(saved_act);
   LUFFY_NEED(scratch_dpre);
-  LUFFY_NEED(d_recv);
   LUFFY_NEED(dw1);
   LUFFY_NEED(dw2);
   LUFFY_STAGE(L, 6, "luffy_expert_ffn_bwd");
@@ -639,18 +672,37 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
   const int32_t* off = expert_off(L);
   const int64_t rows = expert_rows_bound(L);
   const int d = L->d, f = L->f, G = L->El;
+  XRedirect rd{};
+  XSignal sig{};
+  if (L->P == 1) {
+    LUFFY_NEED(d_out);
+    LUFFY_NEED(recv);
+    LUFFY_NEED(d_recv);
+  } else {
+    LUFFY_OWN(d_out, L->x_dexp, "luffy_expert_ffn_bwd d_out");
+    LUFFY_OWN(recv, L->x_recv[L->seq & 1], "luffy_expert_ffn_bwd recv");
+    if (d_recv) return fail(LUFFY_E_INVALID, "luffy_expert_ffn_bwd: with world > 1 pass d_recv = NULL");
+    d_out = L->x_dexp;
+    recv = L->x_recv[L->seq & 1];
+    rd.rank_of = L->x_rank_of;  // fused dispatch backward: dX rows go to their source rank's d_send
+    rd.slot_of = L->x_slot_of;
+    rd.peer_base = L->x_peer_dsend;
+    sig = make_signal(L, XP_DBWD);
+  }
+  const XRedirect* rdp = L->P > 1 ? &rd : nullptr;
+  const XSignal* sgp = L->P > 1 ? &sig : nullptr;
   if (L->act == LUFFY_GELU) {
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_DGELU, d_out, w2, nullptr, scratch_dpre, const_cast<void*>(saved_pre), off, G, rows,
                           f, d, 0, stream), "ffn_bwd/dgrad2");
-    LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, nullptr, d_recv, nullptr, off, G, rows, d, f, 0, stream),
-                "ffn_bwd/dgrad1");
+    LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, nullptr, d_recv, nullptr, off, G, rows, d, f, 0, stream,
+                          rdp, sgp), "ffn_bwd/dgrad1");
     LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, rows, stream), "ffn_bwd/wgrad2");
     LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, nullptr, f, off, G, f, d, f, d, rows, stream), "ffn_bwd/wgrad1");
   } else {
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_DSWIGLU, d_out, w2, nullptr, scratch_dpre, const_cast<void*>(saved_pre), off, G,
                           rows, f, d, 0, stream), "ffn_bwd/dgrad2");
-    LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, w3, d_recv, nullptr, off, G, rows, d, 2 * f, 0, stream),
-                "ffn_bwd/dgrad1");
+    LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, scratch_dpre, w1, w3, d_recv, nullptr, off, G, rows, d, 2 * f, 0, stream,
+                          rdp, sgp), "ffn_bwd/dgrad1");
     LUFFY_CHECK(gemm_wgrad(L->dtype, d_out, saved_act, dw2, nullptr, d, off, G, d, f, d, f, rows, stream), "ffn_bwd/wgrad2");
     LUFFY_CHECK(gemm_wgrad(L->dtype, scratch_dpre, recv, dw1, dw3, f, off, G, 2 * f, d, 2 * f, d, rows, stream), "ffn_bwd/wgrad1");
   }
@@ -659,16 +711,16 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
 
 luffy_status luffy_dispatch_bwd(luffy_layer* L, const void* d_recv, void* dx, void* stream) {
   LUFFY_NEED(L);
-  LUFFY_NEED(d_recv);
   LUFFY_NEED(dx);
   LUFFY_ALIGNED(dx);
   LUFFY_STAGE(L, 6, "luffy_dispatch_bwd");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const void* dsend = d_recv;
-  if (L->P > 1) {
-    luffy_status s2 = exchange(L, 1, d_recv, L->send, st);
-    if (s2 != LUFFY_OK) return s2;
-    dsend = L->send;
+  if (L->P == 1) {
+    LUFFY_NEED(d_recv);
+  } else {
+    if (d_recv) return fail(LUFFY_E_INVALID, "luffy_dispatch_bwd: with world > 1 pass d_recv = NULL");
+    LUFFY_CHECK(launch_xwait(L, XP_DBWD, stream), "luffy_dispatch_bwd/wait");
+    dsend = L->x_dsend;
   }
   LUFFY_CHECK(launch_unpack_bwd(L, dsend, dx, stream), "luffy_dispatch_bwd");
   return LUFFY_OK;

@@ -1,0 +1,200 @@
+// Device-initiated dispatch over NVLink (world > 1): count exchange, layout plan and the fused
+// pack-and-push of representative rows into the owning ranks' receive buffers (P:143 dispatch phase,
+// only representatives).  No host synchronisation: every rank derives every layout from
+// the all-to-all counts on the device.  See exchange.cuh for the buffers and the signalling protocol.
+#include "common.cuh"
+#include "exchange.cuh"
+
+namespace luffy {
+namespace {
+
+// Push my representative counts into every rank's inbox row `me`, then publish XP_CNT.
+__global__ void xcnt_push_kernel(const int32_t* __restrict__ nrep, int E, int me, int32_t* const* peer_cnt, int P,
+                                 XSignal sig) {
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
+    const int p = i / E, e = i % E;
+    peer_cnt[p][(size_t)me * E + e] = nrep[e];
+  }
+  xsignal_done(sig);
+}
+
+// Wait until every rank published `seq` for this phase (bounded: traps after ~20 s instead of hanging).
+__global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq) {
+  const int p = threadIdx.x;
+  if (p < P) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(flags + p) < seq) {
+      __nanosleep(128);
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+}
+
+// Layout plan from the all-to-all counts (one CTA): local copy of the counts, my expert layout (roff),
+// and for each expert e the destination row base of my rows in the owner's layout (dst_base[e]).
+__global__ void xplan_small_kernel(const int32_t* __restrict__ inbox, int P, int E, int me, int32_t* __restrict__ cnt_all,
+                                   int32_t* __restrict__ roff, int32_t* __restrict__ dst_base,
+                                   int32_t* __restrict__ src_soff) {
+  const int32_t* c = inbox;  // [P][E], complete (XP_CNT waited)
+  const int El = E / P;
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) cnt_all[i] = c[i];
+  // src_soff[q][e]: padded send offsets of rank q (expert segments rounded up to kRowAlign)
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    int o = 0;
+    for (int e = 0; e < E; ++e) {
+      src_soff[q * (E + 1) + e] = o;
+      o += (c[q * E + e] + kRowAlign - 1) / kRowAlign * kRowAlign;
+    }
+    src_soff[q * (E + 1) + E] = o;
+  }
+  if (threadIdx.x == 0) {
+    // my expert layout
+    int o = 0;
+    for (int el = 0; el < El; ++el) {
+      roff[el] = o;
+      int rows = 0;
+      for (int q = 0; q < P; ++q) rows += c[q * E + me * El + el];
+      o += (rows + kRowAlign - 1) / kRowAlign * kRowAlign;
+    }
+    roff[El] = o;
+  }
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    // owner p = e / El lays out expert e after all experts el' < e % El of p, each padded
+    const int p = e / El, el = e % El;
+    int base = 0;
+    for (int j = 0; j < el; ++j) {
+      int rows = 0;
+      for (int q = 0; q < P; ++q) rows += c[q * E + p * El + j];
+      base += (rows + kRowAlign - 1) / kRowAlign * kRowAlign;
+    }
+    for (int q = 0; q < me; ++q) base += c[q * E + e];
+    dst_base[e] = base;
+  }
+}
+
+// Per expert-layout row: the source rank and its send slot (for the combine and dispatch-backward
+// epilogues); padding rows -> -1 and zeroed in the receive buffer and in dexp.
+__global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restrict__ cnt_all, const int32_t* __restrict__ roff,
+                                                         const int32_t* __restrict__ src_soff, int P, int E, int me,
+                                                         int d, int64_t max_rows, int32_t* __restrict__ rank_of,
+                                                         int32_t* __restrict__ slot_of, bf16* __restrict__ recv,
+                                                         bf16* __restrict__ dexp, int elem_bytes) {
+  const int El = E / P;
+  const int64_t rows = roff[El];
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += nthreads) {
+    int el = 0;
+    while (el + 1 <= El && roff[el + 1] <= r) ++el;
+    const int e = me * El + el;
+    int64_t i = r - roff[el];
+    int q = 0;
+    while (q < P && i >= cnt_all[q * E + e]) {
+      i -= cnt_all[q * E + e];
+      ++q;
+    }
+    if (q < P) {
+      rank_of[r] = q;
+      slot_of[r] = src_soff[q * (E + 1) + e] + (int32_t)i;
+    } else {
+      rank_of[r] = -1;
+      slot_of[r] = -1;
+      // padding row: zero it in the receive buffer and in the backward buffer
+      const size_t rb = (size_t)d * elem_bytes;
+      uint4* a = reinterpret_cast<uint4*>(reinterpret_cast<char*>(recv) + r * rb);
+      uint4* b = reinterpret_cast<uint4*>(reinterpret_cast<char*>(dexp) + r * rb);
+      for (size_t j = 0; j < rb / 16; ++j) {
+        a[j] = make_uint4(0, 0, 0, 0);
+        b[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+
+// Fused pack + dispatch: every representative row is copied from x straight into the owner's
+// receive buffer (16-byte vector stores over NVLink), then XP_DISP is published.
+template <typename T>
+__global__ void __launch_bounds__(256) xpack_push_kernel(const T* __restrict__ x, const int32_t* __restrict__ perm,
+                                                         const int32_t* __restrict__ soff, const int32_t* __restrict__ dst_base,
+                                                         int E, int El, int d, void* const* peer_recv, XSignal sig) {
+  __shared__ int32_t soff_s[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+    soff_s[i] = soff[i];
+    if (i < E) base_s[i] = dst_base[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t rows = soff_s[E];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < rows; s += nw) {
+    const int t = perm[s];
+    if (t < 0) continue;
+    const int e = find_group(soff_s, E, s);
+    const int p = e / El;
+    T* dst = static_cast<T*>(peer_recv[p]) + ((int64_t)base_s[e] + (s - soff_s[e])) * d;
+    const T* src = x + (size_t)t * d;
+    for (int c = lane * 8; c < d; c += 256) {
+      if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(src + c);
+      } else {
+        *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+        *reinterpret_cast<float4*>(dst + c + 4) = *reinterpret_cast<const float4*>(src + c + 4);
+      }
+    }
+  }
+  xsignal_done(sig);
+}
+
+inline int grid_warps(int64_t warps) {
+  int64_t b = (warps + 7) / 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8));
+}
+
+}  // namespace
+
+int launch_xwait(const luffy_layer* L, int phase, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  xwait_kernel<<<1, 64, 0, st>>>(L->x_flags + phase * L->P, L->P, L->seq);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+XSignal make_signal(const luffy_layer* L, int phase) {
+  XSignal sg;
+  sg.counter = L->x_counters + phase;
+  sg.flag = L->x_flagptr + phase * L->P;
+  sg.P = L->P;
+  sg.seq = L->seq;
+  return sg;
+}
+
+// Dispatch at world > 1: counts -> plan -> fused pack/push -> wait for every rank's rows.
+int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  const int par = L->seq & 1;
+  xcnt_push_kernel<<<1, 256, 0, st>>>(L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT));
+  LUFFY_LAUNCHED();
+  LUFFY_CUDA_TRY(launch_xwait(L, XP_CNT, s));
+  xplan_small_kernel<<<1, 256, 0, st>>>(L->x_cnt_inbox, L->P, L->E, L->rank, L->cnt_all, L->roff, L->x_dst_base,
+                                        L->x_src_soff);
+  LUFFY_LAUNCHED();
+  xplan_rows_kernel<<<148, 256, 0, st>>>(L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
+                                         L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),
+                                         static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4);
+  LUFFY_LAUNCHED();
+  const int blocks = grid_warps(L->Rpad_max);
+  if (L->dtype == LUFFY_BF16)
+    xpack_push_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->perm, L->soff, L->x_dst_base, L->E,
+                                                    L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP));
+  else
+    xpack_push_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->perm, L->soff, L->x_dst_base, L->E,
+                                                     L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP));
+  LUFFY_LAUNCHED();
+  return launch_xwait(L, XP_DISP, s);
+}
+
+}  // namespace luffy

@@ -1,0 +1,65 @@
+// Device-initiated expert-parallel exchange over NVLink (world > 1).
+//
+// Every layer owns one peer-visible exchange region (cudaMalloc + CUDA IPC, mapped by every rank):
+//   recv[2]    expert layout, double-buffered by step parity  <- peers' pack kernels (dispatch)
+//   gathered   send layout                                     <- peers' GEMM2 epilogues (combine)
+//   dexp       expert layout                                   <- peers' uncondense-backward (combine bwd)
+//   dsend      send layout                                     <- peers' dgrad1 epilogues (dispatch bwd)
+//   cnt_inbox  [P][E] representative counts                    <- peers (count exchange)
+//   flags      [phase][P] step sequence numbers               <- peers (release stores)
+// Producers store rows straight into the destination rank's buffer; the last CTA of a producing kernel
+// publishes `seq` to every peer's flag with a system-scope release; consumers wait with acquire loads.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "luffy_internal.h"
+
+namespace luffy {
+
+enum XPhase { XP_CNT = 0, XP_DISP = 1, XP_COMB = 2, XP_CBWD = 3, XP_DBWD = 4, XP_NUM = 5 };
+constexpr int kMaxWorld = 64;
+
+// Completion signal of one producing kernel.
+struct XSignal {
+  uint32_t* counter;        // local CTA-completion counter (reset by the last CTA)
+  uint32_t* const* flag;    // [P] address of (phase, my rank) in each peer's flag array
+  int P;
+  uint32_t seq;
+};
+
+// Row redirect for an epilogue: expert-layout row r goes to rank rank_of[r], row slot_of[r] of that
+// rank's buffer peer_base[rank] (row size row_bytes); rank_of[r] < 0 = padding (not sent).
+struct XRedirect {
+  const int32_t* rank_of;
+  const int32_t* slot_of;
+  void* const* peer_base;
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Call by every thread of every CTA at the end of a producing kernel.
+__device__ __forceinline__ void xsignal_done(const XSignal& s) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t total = gridDim.x * gridDim.y * gridDim.z;
+    const uint32_t prev = atomicAdd(s.counter, 1u);
+    if (prev == total - 1) {
+      *s.counter = 0u;
+      __threadfence_system();
+      for (int p = 0; p < s.P; ++p) st_release_sys(s.flag[p], s.seq);
+    }
+  }
+}
+
+XSignal make_signal(const luffy_layer* L, int phase);
+
+}  // namespace luffy

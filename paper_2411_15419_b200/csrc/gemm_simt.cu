@@ -2,6 +2,7 @@
 // (fp32 configs must not use tf32 tensor cores: the 1e-4 bound) and the reference
 // shape of the tcgen05 kernels in gemm_tc.cu (same layouts, same fused epilogues).
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace luffy {
 namespace {
@@ -18,12 +19,16 @@ __device__ __forceinline__ int tcol(int tx, int j) { return (j < 2 ? 2 * tx + j 
 template <typename T, int EPI>
 __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A, const T* __restrict__ B,
                                                         const T* __restrict__ B3, T* __restrict__ D, T* __restrict__ aux0,
-                                                        const int32_t* __restrict__ off, int G, int N, int K, int bkm) {
+                                                        const int32_t* __restrict__ off, int G, int N, int K, int bkm,
+                                                        XRedirect rd, int has_rd, XSignal sig, int has_sig) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int64_t row0 = (int64_t)blockIdx.y * BM;
   const int32_t rows = off[G];
-  if (row0 >= rows) return;
+  if (row0 >= rows) {
+    if (has_sig) xsignal_done(sig);
+    return;
+  }
   const int g = find_group(off, G, row0);
   // Column mapping.  SWIGLU: f = N / 2 logical columns, tile covers f-cols [n0, n0+32) of W1 and W3.
   const int f = N / 2;
@@ -95,7 +100,12 @@ __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A,
         const int n = n0 + tcol(tx, j);
         const float v = acc[i][j];
         if (EPI == EPI_STORE) {
-          store1(D + r * N + n, v);
+          if (has_rd) {
+            const int rk = rd.rank_of[r];
+            if (rk >= 0) store1(static_cast<T*>(rd.peer_base[rk]) + (size_t)rd.slot_of[r] * N + n, v);
+          } else {
+            store1(D + r * N + n, v);
+          }
         } else if (EPI == EPI_GELU) {
           store1(aux0 + r * N + n, v);
           store1(D + r * N + n, gelu_f(v));
@@ -109,6 +119,7 @@ __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A,
       }
     }
   }
+  if (has_sig) xsignal_done(sig);
 }
 
 // D_g[m, n] = sum_{r in segment g} A[r, m] * B[r, n], fp32 output; rows m >= Msplit go to D3.
@@ -155,7 +166,12 @@ __global__ void __launch_bounds__(256) gemm_wgrad_kernel(const T* __restrict__ A
 
 template <typename T>
 int gemm_rows_t(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
-                int64_t max_rows, int N, int K, int bkm, cudaStream_t s) {
+                int64_t max_rows, int N, int K, int bkm, const XRedirect* rdp, const XSignal* sgp, cudaStream_t s) {
+  XRedirect rd{};
+  XSignal sg{};
+  const int has_rd = rdp != nullptr, has_sig = sgp != nullptr;
+  if (rdp) rd = *rdp;
+  if (sgp) sg = *sgp;
   dim3 grid(epi == EPI_SWIGLU ? (N / 2) / 32 : N / BN, (unsigned)((max_rows + BM - 1) / BM));
   const T* a = static_cast<const T*>(A);
   const T* b = static_cast<const T*>(B);
@@ -163,11 +179,11 @@ int gemm_rows_t(int epi, const void* A, const void* B, const void* B3, void* D, 
   T* d = static_cast<T*>(D);
   T* x = static_cast<T*>(aux0);
   switch (epi) {
-    case EPI_STORE: gemm_rows_kernel<T, EPI_STORE><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm); break;
-    case EPI_GELU: gemm_rows_kernel<T, EPI_GELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm); break;
-    case EPI_SWIGLU: gemm_rows_kernel<T, EPI_SWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm); break;
-    case EPI_DGELU: gemm_rows_kernel<T, EPI_DGELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm); break;
-    default: gemm_rows_kernel<T, EPI_DSWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm); break;
+    case EPI_STORE: gemm_rows_kernel<T, EPI_STORE><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_GELU: gemm_rows_kernel<T, EPI_GELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_SWIGLU: gemm_rows_kernel<T, EPI_SWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_DGELU: gemm_rows_kernel<T, EPI_DGELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    default: gemm_rows_kernel<T, EPI_DSWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
   }
   LUFFY_LAUNCHED();
   return 0;
@@ -176,10 +192,11 @@ int gemm_rows_t(int epi, const void* A, const void* B, const void* B3, void* D, 
 }  // namespace
 
 int gemm_rows_simt(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0,
-                   const int32_t* off, int G, int64_t max_rows, int N, int K, int b_kmajor, void* s) {
+                   const int32_t* off, int G, int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd,
+                   const XSignal* sig, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  return dtype == LUFFY_BF16 ? gemm_rows_t<bf16>(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, st)
-                             : gemm_rows_t<float>(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, st);
+  return dtype == LUFFY_BF16 ? gemm_rows_t<bf16>(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, st)
+                             : gemm_rows_t<float>(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, st);
 }
 
 int gemm_wgrad_simt(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G,

@@ -13,6 +13,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "exchange.cuh"
 #include "tc_common.cuh"
 
 namespace luffy {
@@ -36,6 +37,10 @@ struct TcArgs {
   float* D3;
   int Msplit;
   int f;               // SwiGLU: d_ffn
+  int has_rd;          // EPI_STORE rows: rows go to peer buffers (fused combine / dispatch-backward)
+  XRedirect rd;
+  int has_sig;         // publish completion to the peers when the kernel ends
+  XSignal sig;
 };
 
 struct Tile {
@@ -271,7 +276,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
             const int n = x.n0 + c0;
             if (EPI == EPI_STORE) {
-              store32_bf16(D + row * a.N + n, v);
+              if (a.has_rd) {  // fused exchange: the row goes straight to its rank's buffer over NVLink
+                const int rk = a.rd.rank_of[row];
+                if (rk >= 0)
+                  store32_bf16(static_cast<bf16*>(a.rd.peer_base[rk]) + (size_t)a.rd.slot_of[row] * a.N + n, v);
+              } else {
+                store32_bf16(D + row * a.N + n, v);
+              }
             } else if (EPI == EPI_GELU) {
               store32_bf16(X + row * a.N + n, v);
               float o[32];
@@ -308,6 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem_base, 512);
+  if (a.has_sig) xsignal_done(a.sig);
 }
 
 int num_sms() {
@@ -360,9 +372,17 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
 
 // Rows GEMM: D[r, :] over expert segments; see luffy_internal.h (Epi) for the epilogues.
 int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
-                 int64_t max_rows, int N, int K, int b_kmajor, void* s) {
+                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   TcArgs a{};
+  if (rd) {
+    a.has_rd = 1;
+    a.rd = *rd;
+  }
+  if (sig) {
+    a.has_sig = 1;
+    a.sig = *sig;
+  }
   a.off = off;
   a.G = G;
   a.N = N;

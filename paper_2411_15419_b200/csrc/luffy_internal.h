@@ -79,9 +79,31 @@ struct luffy_layer {
   bool has_adj;
   int stage;          // 0 none, 1 routed, 2 condensed, 3 dispatched, 4 ffn, 5 combined, 6 uncondensed
   int64_t send_rows_h, recv_rows_h;
-  int32_t* cnt_all_h;  // pinned [P*E]
-  int32_t* roff_h;     // pinned [El+1]
-  int32_t* soff_h;     // pinned [E+1] (world > 1)
+  // ---- device-initiated exchange (world > 1), see exchange.cuh
+  uint32_t seq;        // step sequence number (incremented by luffy_route)
+  char* x_region;      // own peer-visible region (cudaMalloc, CUDA IPC)
+  size_t x_region_bytes;
+  uint8_t x_handle[64];
+  void* x_peer_base_h[64];  // host: mapped base of every rank's region (own at [rank])
+  bool x_open;
+  void* x_recv[2];     // own buffers inside the region
+  void* x_gathered;
+  void* x_dexp;
+  void* x_dsend;
+  int32_t* x_cnt_inbox;  // [P][E]
+  uint32_t* x_flags;     // [XP_NUM][P]
+  uint32_t* x_counters;  // [XP_NUM]
+  // device tables (workspace)
+  void** x_peer_recv;      // [2][P]
+  void** x_peer_gathered;  // [P]
+  void** x_peer_dexp;      // [P]
+  void** x_peer_dsend;     // [P]
+  int32_t** x_peer_cnt;    // [P]
+  uint32_t** x_flagptr;    // [XP_NUM][P] -> (phase, my rank) slot in each rank's flags
+  int32_t* x_dst_base;     // [E] destination row base of my rows of expert e in its owner's layout
+  int32_t* x_src_soff;     // [P][E+1] padded send offsets of every rank
+  int32_t* x_rank_of;      // [recv_max] source rank of each expert-layout row (-1 padding)
+  int32_t* x_slot_of;      // [recv_max] its slot in the source's send layout
 };
 
 // ---- kernel launchers (defined in the .cu files); all enqueue on `s` and return cudaError_t as int
@@ -98,6 +120,8 @@ int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void*
 int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gathered, void* dg, float* dw, void* s);
 int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s);
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s);
+int launch_xdispatch(luffy_layer* L, const void* x, void* s);
+int launch_xwait(const luffy_layer* L, int phase, void* s);
 
 // Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).
 enum Epi { EPI_STORE = 0, EPI_GELU = 1, EPI_SWIGLU = 2, EPI_DGELU = 3, EPI_DSWIGLU = 4 };

@@ -11,6 +11,7 @@
 //               members are read from the slot's adjacency row (they are exactly its neighbours whose
 //               rep is the slot, plus itself), so no atomics and a fixed summation order.
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace luffy {
 namespace {
@@ -269,11 +270,31 @@ __global__ void __launch_bounds__(256) dw_kernel(const T* __restrict__ dy, const
 // that uncondense_bwd_finalize sums in window order.
 constexpr int WIN = 16;
 
+// Destination of the backward rows of send slots: local d_gathered, or (fused combine-backward) the
+// owning rank's dexp buffer at row dst_base[e] + (slot - soff[e]).
+struct XDest {
+  int remote;
+  const int32_t* soff;
+  const int32_t* dst_base;
+  void* const* peer;
+  int E, El;
+  template <typename T>
+  __device__ __forceinline__ T* row(int slot, int d) const {
+    int lo = 0, hi = E;  // expert of the slot: soff[lo] <= slot < soff[lo+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (soff[mid] <= slot) lo = mid; else hi = mid;
+    }
+    return static_cast<T*>(peer[lo / El]) + ((int64_t)dst_base[lo] + (slot - soff[lo])) * d;
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
     const T* __restrict__ dy, const int32_t* __restrict__ goff, int E, const int32_t* __restrict__ members,
     const int32_t* __restrict__ mslot, const int32_t* __restrict__ mstart, const int32_t* __restrict__ mcnt,
-    const int32_t* __restrict__ gtok, const float* __restrict__ gw, int d, T* __restrict__ dg, float* __restrict__ part) {
+    const int32_t* __restrict__ gtok, const float* __restrict__ gw, int d, T* __restrict__ dg, float* __restrict__ part,
+    XDest xd) {
   const int lane = threadIdx.x & 31;
   const int64_t nwin = goff[E] / WIN;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -298,9 +319,10 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
         const int ms = mstart[slot], me = ms + mcnt[slot];
         const int c = c0 + lane * 8;
         if (ms >= m0 && me <= m0 + WIN) {
+          T* out = xd.remote ? xd.row<T>(slot, d) : dg + (size_t)slot * d;
 #pragma unroll
           for (int q = 0; q < 2; ++q)
-            if (c + q * 256 < d) store8(dg + (size_t)slot * d + c + q * 256, acc[q]);
+            if (c + q * 256 < d) store8(out + c + q * 256, acc[q]);
         } else {
           float* dst = part + ((size_t)wi * 2 + (ms < m0 ? 0 : 1)) * d;
 #pragma unroll
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
       if (cur >= 0) flush(cur);
     }
   }
+  if (xd.remote) __threadfence_system();
 }
 
 // Slots crossing window boundaries: sum the partials in window order.  Padding slots are zeroed.
@@ -370,16 +393,18 @@ __global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int3
                                                                       const int32_t* __restrict__ soff, int E,
                                                                       const int32_t* __restrict__ mstart,
                                                                       const int32_t* __restrict__ mcnt, int d,
-                                                                      const float* __restrict__ part, T* __restrict__ dg) {
+                                                                      const float* __restrict__ part, T* __restrict__ dg,
+                                                                      XDest xd, XSignal sig) {
   const int lane = threadIdx.x & 31;
   const int64_t rows = soff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < rows; s += nw) {
-    T* out = dg + s * d;
     if (perm[s] < 0) {
-      for (int c = lane * 8; c < d; c += 256) zero8(out + c);
+      if (!xd.remote)  // (remote: the expert rank zeroes its own padding rows)
+        for (int c = lane * 8; c < d; c += 256) zero8(dg + s * d + c);
       continue;
     }
+    T* out = xd.remote ? xd.row<T>((int)s, d) : dg + s * d;
     const int ms = mstart[s], me = ms + mcnt[s];
     const int ws = ms / WIN, we = (me - 1) / WIN;
     if (ws == we) continue;  // written by the window kernel
@@ -394,6 +419,7 @@ __global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int3
       store8(out + c, acc);
     }
   }
+  if (xd.remote) xsignal_done(sig);
 }
 
 // dx[t] = sum_{j : rep(t, j) == t} d_send[pos_tj]   (condensed copies get no expert-path gradient, R11)
@@ -481,6 +507,17 @@ int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void*
 
 int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gathered, void* dg, float* dw, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
+  XDest xd{};
+  XSignal sig{};
+  if (L->P > 1) {
+    xd.remote = 1;
+    xd.soff = L->soff;
+    xd.dst_base = L->x_dst_base;
+    xd.peer = L->x_peer_dexp;
+    xd.E = L->E;
+    xd.El = L->El;
+    sig = make_signal(L, XP_CBWD);
+  }
   const int bt = grid_for_warps(L->T);
   const int bw = grid_for_warps(L->Cpad_max / WIN);
   const int bs = grid_for_warps(L->Rpad_max);
@@ -490,20 +527,20 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
     LUFFY_LAUNCHED();
     uncondense_bwd_window_kernel<bf16><<<bw, 256, 0, st>>>(static_cast<const bf16*>(dy), L->goff, L->E, L->members,
                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
-                                                           static_cast<bf16*>(dg), L->mpart);
+                                                           static_cast<bf16*>(dg), L->mpart, xd);
     LUFFY_LAUNCHED();
     uncondense_bwd_finalize_kernel<bf16><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
-                                                             static_cast<bf16*>(dg));
+                                                             static_cast<bf16*>(dg), xd, sig);
   } else {
     dw_kernel<float><<<bt, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos, L->T,
                                          L->k, L->d, dw);
     LUFFY_LAUNCHED();
     uncondense_bwd_window_kernel<float><<<bw, 256, 0, st>>>(static_cast<const float*>(dy), L->goff, L->E, L->members,
                                                             L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
-                                                            static_cast<float*>(dg), L->mpart);
+                                                            static_cast<float*>(dg), L->mpart, xd);
     LUFFY_LAUNCHED();
     uncondense_bwd_finalize_kernel<float><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,
-                                                              L->mpart, static_cast<float*>(dg));
+                                                              L->mpart, static_cast<float*>(dg), xd, sig);
   }
   LUFFY_LAUNCHED();
   return 0;

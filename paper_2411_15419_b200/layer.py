@@ -16,8 +16,8 @@ _TORCH_DT = {L.BF16: torch.bfloat16, L.FP32: torch.float32}
 class CondensedMoELayer:
     def __init__(self, num_experts: int, top_k: int, d_model: int, d_ffn: int, max_tokens: int,
                  dtype: str = "bf16", act: str = "gelu", world: int = 1, rank: int = 0,
-                 nccl_id: bytes | None = None, renormalize: int = -1, max_recv_rows: int = 0,
-                 device: torch.device | str = "cuda"):
+                 renormalize: int = -1, max_recv_rows: int = 0, device: torch.device | str = "cuda",
+                 group=None):
         self.device = torch.device(device)
         self.dt = L.BF16 if dtype == "bf16" else L.FP32
         self.tdt = _TORCH_DT[self.dt]
@@ -27,10 +27,18 @@ class CondensedMoELayer:
         self.El = num_experts // world
         self.cfg = L.make_config(world, rank, num_experts, top_k, d_model, d_ffn, self.dt, self.act, renormalize,
                                  max_tokens, max_recv_rows)
-        self.ctx = L.luffy_create(self.cfg, nccl_id)
+        self.ctx = L.luffy_create(self.cfg)
         nbytes = L.luffy_layer_workspace_bytes(self.cfg)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.layer = L.luffy_layer_create(self.ctx, self.ws, nbytes)
+        if world > 1:
+            # map every rank's exchange region (CUDA IPC over NVLink); torch.distributed only carries
+            # the handle blobs (plumbing)
+            import torch.distributed as dist
+            mine = L.luffy_layer_ipc_handle(self.layer)
+            handles = [None] * world
+            dist.all_gather_object(handles, mine, group=group)
+            L.luffy_layer_ipc_open(self.layer, handles)
         C = max_tokens * top_k
         self.send_rows = C + num_experts * L.ROW_ALIGN
         self.recv_rows = max_recv_rows if max_recv_rows > 0 else world * C + self.El * L.ROW_ALIGN
@@ -41,17 +49,18 @@ class CondensedMoELayer:
         self.idx = torch.empty(max_tokens, top_k, dtype=torch.int32, device=dev)
         self.w = torch.empty(max_tokens, top_k, dtype=torch.float32, device=dev)
         self.rep = torch.empty(max_tokens, top_k, dtype=torch.int32, device=dev)
-        self.recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        one = world == 1  # world > 1: recv / gathered / d_expert_out / d_send live in the layer's exchange region
+        self.recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev) if one else None
         self.pre = torch.empty(self.recv_rows, pre_cols, dtype=tdt, device=dev)
         self.act_buf = torch.empty(self.recv_rows, d_ffn, dtype=tdt, device=dev)
-        self.out = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
-        self.gathered = self.out if world == 1 else torch.empty(self.send_rows, d_model, dtype=tdt, device=dev)
+        self.out = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev) if one else None
+        self.gathered = self.out
         self.y = torch.empty(max_tokens, d_model, dtype=tdt, device=dev)
         # backward buffers
-        self.d_gathered = torch.empty(self.send_rows if world > 1 else self.recv_rows, d_model, dtype=tdt, device=dev)
-        self.d_out = self.d_gathered if world == 1 else torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.d_gathered = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev) if one else None
+        self.d_out = self.d_gathered
         self.dpre = torch.empty(self.recv_rows, pre_cols, dtype=tdt, device=dev)
-        self.d_recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev)
+        self.d_recv = torch.empty(self.recv_rows, d_model, dtype=tdt, device=dev) if one else None
         self.dx = torch.empty(max_tokens, d_model, dtype=tdt, device=dev)
         self.dw = torch.empty(max_tokens, top_k, dtype=torch.float32, device=dev)
         self.dw1 = torch.empty(self.El, d_ffn, d_model, dtype=torch.float32, device=dev)

@@ -21,12 +21,13 @@ ROW_ALIGN = 128
 MAX_EXPERTS = 256
 
 EXPORTED = [
-    "luffy_get_unique_id", "luffy_create", "luffy_destroy", "luffy_layer_workspace_bytes",
+    "luffy_create", "luffy_destroy", "luffy_layer_workspace_bytes",
     "luffy_layer_create", "luffy_layer_destroy", "luffy_last_error", "luffy_launch_count",
     "luffy_layer_rows", "luffy_route", "luffy_condense", "luffy_dispatch", "luffy_expert_ffn",
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
+    "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
 ]
 
 
@@ -62,8 +63,12 @@ def _load():
     lib = ctypes.CDLL(_LIB_PATH, mode=ctypes.RTLD_GLOBAL)
     P, I32, I64, F32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
     sig = {
-        "luffy_get_unique_id": (I32, [P]),
-        "luffy_create": (I32, [ctypes.POINTER(Config), P, ctypes.POINTER(P)]),
+        "luffy_create": (I32, [ctypes.POINTER(Config), ctypes.POINTER(P)]),
+        "luffy_ipc_handle_bytes": (SZ, []),
+        "luffy_layer_ipc_handle": (I32, [P, P]),
+        "luffy_layer_ipc_open": (I32, [P, P]),
+        "luffy_layer_exchange_buffers": (I32, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                                ctypes.POINTER(P)]),
         "luffy_destroy": (None, [P]),
         "luffy_layer_workspace_bytes": (SZ, [ctypes.POINTER(Config)]),
         "luffy_layer_create": (I32, [P, P, SZ, ctypes.POINTER(P)]),
@@ -120,20 +125,32 @@ def make_config(world=1, rank=0, num_experts=8, top_k=2, d_model=1024, d_ffn=409
                   max_recv_rows)
 
 
-def luffy_get_unique_id() -> bytes:
-    buf = (ctypes.c_uint8 * 128)()
-    _check(LIB.luffy_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+def luffy_create(cfg: Config) -> int:
+    out = ctypes.c_void_p()
+    _check(LIB.luffy_create(ctypes.byref(cfg), ctypes.byref(out)))
+    return out.value
+
+
+def luffy_ipc_handle_bytes() -> int:
+    return LIB.luffy_ipc_handle_bytes()
+
+
+def luffy_layer_ipc_handle(layer: int) -> bytes:
+    buf = (ctypes.c_uint8 * luffy_ipc_handle_bytes())()
+    _check(LIB.luffy_layer_ipc_handle(layer, ctypes.cast(buf, ctypes.c_void_p)))
     return bytes(buf)
 
 
-def luffy_create(cfg: Config, nccl_id: bytes | None = None) -> int:
-    out = ctypes.c_void_p()
-    idp = None
-    if nccl_id is not None:
-        ida = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
-        idp = ctypes.cast(ida, ctypes.c_void_p)
-    _check(LIB.luffy_create(ctypes.byref(cfg), idp, ctypes.byref(out)))
-    return out.value
+def luffy_layer_ipc_open(layer: int, all_handles: list):
+    blob = b"".join(all_handles)
+    arr = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+    _check(LIB.luffy_layer_ipc_open(layer, ctypes.cast(arr, ctypes.c_void_p)))
+
+
+def luffy_layer_exchange_buffers(layer: int):
+    ptrs = [ctypes.c_void_p() for _ in range(4)]
+    _check(LIB.luffy_layer_exchange_buffers(layer, *[ctypes.byref(p) for p in ptrs]))
+    return tuple(p.value for p in ptrs)
 
 
 def luffy_destroy(ctx: int):

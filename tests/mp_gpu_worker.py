@@ -44,8 +44,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    obj = [L.luffy_get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
     if args.config == "C2S":
         cfg = dataclasses.replace(workload.CONFIGS["C2"], seqs_per_rank=2)
     elif args.config == "C1":
@@ -63,7 +61,7 @@ def main():
     w1, w2 = dt(inp["W1"][loc]), dt(inp["W2"][loc])
     w3 = dt(inp["W3"][loc]) if inp["W3"] is not None else None
     lay = LY.CondensedMoELayer(E, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T, dtype=cfg.dtype, act=cfg.act,
-                               world=world, rank=rank, nccl_id=obj[0], device=dev)
+                               world=world, rank=rank, device=dev)
     y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True)
     g = lay.backward(dy, x, wg, w1, w2, w3)
     torch.cuda.synchronize()

@@ -83,9 +83,10 @@ typedef struct {
                              probability; -1: default (top_k > 1), R1 */
   int32_t max_tokens;     /* T capacity per rank */
   int32_t max_recv_rows;  /* expert-side row capacity incl. padding; 0: world*max_tokens*top_k + E_l*LUFFY_ROW_ALIGN */
+  int32_t max_seqs;       /* sequences per rank for sequence migration (world > 1); 0: 256 */
 } luffy_config;
 
-typedef struct luffy_ctx luffy_ctx;     /* per rank: config, NCCL communicator, pinned host buffers */
+typedef struct luffy_ctx luffy_ctx;     /* per rank: config and device */
 typedef struct luffy_layer luffy_layer; /* per MoE layer call chain: saved routing/condensation/layout */
 
 typedef struct {
@@ -244,6 +245,28 @@ LUFFY_API luffy_status luffy_debug_gemm(int32_t kind, int32_t dtype, int32_t epi
                                         const void* B3, void* D, void* aux, float* D3, int32_t Msplit,
                                         const int32_t* off, int32_t G, int64_t max_rows, int32_t M, int32_t N,
                                         int32_t K, int32_t b_kmajor, void* stream);
+
+/* ---- sequence migration in the layer (world > 1), P:264-299 -------------------------------------- */
+
+/* K9: after luffy_condense and before luffy_dispatch.  seq_len (host, [num_seqs], sums to T) splits this
+ * rank's tokens into sequences; returns rows_at_all (host, [world * num_seqs][world], every rank's
+ * sequences in rank order): the number of DISTINCT representative rows each sequence uses on each rank
+ * (reading R16; Alg. 1 line 1 input).  Every rank gets the same table (device exchange).  [sync] */
+LUFFY_API luffy_status luffy_sequence_rows(luffy_layer* layer, const int32_t* seq_len, int32_t num_seqs,
+                                           int64_t* rows_at_all, void* stream);
+
+/* Registers the placement of this step (e.g. from luffy_plan_migration, run identically on every rank):
+ * seq_len_all / seq_dest (host, [world * num_seqs]).  The combine then delivers each expert-output row to
+ * every rank hosting a sequence that uses it (GEMM2 epilogue over NVLink); luffy_uncondense writes the
+ * tokens this rank hosts (*out_rows of them, host) in (home rank, sequence, token) order -- see
+ * luffy_migration_out_tokens; luffy_uncondense_bwd takes dY in that order and returns dY / d(gate weight)
+ * to the home ranks.  Before luffy_dispatch.  [sync] */
+LUFFY_API luffy_status luffy_set_migration(luffy_layer* layer, const int32_t* seq_len_all, const int32_t* seq_dest,
+                                           int64_t* out_rows, void* stream);
+
+/* (home rank, home token index) of each output row of this rank (host [out_rows]; either may be NULL).
+ * After luffy_combine; synchronize the stream first.  [sync] */
+LUFFY_API luffy_status luffy_migration_out_tokens(const luffy_layer* layer, int32_t* home_rank, int32_t* home_token);
 
 /* ---- sequence migration placement (CPU, host memory, synchronous, reentrant, deterministic) ------ */
 

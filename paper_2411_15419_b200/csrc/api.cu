@@ -64,7 +64,7 @@ struct Carver {
 };
 
 struct Dims {
-  int P, E, El, k, d, f, Tmax;
+  int P, E, El, k, d, f, Tmax, Smax;
   int64_t C, Cpad, Rpad, recv, adjw;
 };
 
@@ -77,6 +77,7 @@ Dims dims_of(const luffy_config* c) {
   m.d = c->d_model;
   m.f = c->d_ffn;
   m.Tmax = c->max_tokens;
+  m.Smax = c->max_seqs > 0 ? c->max_seqs : 256;
   m.C = (int64_t)m.Tmax * m.k;
   m.Cpad = m.C + (int64_t)m.E * kRowAlign;
   m.Rpad = m.Cpad;
@@ -135,6 +136,17 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
     o->x_src_soff = cv.take<int32_t>((size_t)m.P * (m.E + 1));
     o->x_rank_of = cv.take<int32_t>(m.recv);
     o->x_slot_of = cv.take<int32_t>(m.recv);
+    o->seq_start = cv.take<int32_t>(m.Smax + 1);
+    o->seq_dest_l = cv.take<int32_t>(m.Smax);
+    o->out_start = cv.take<int32_t>(m.Smax);
+    o->seq_bits = cv.take<uint32_t>((size_t)m.Smax * (m.Rpad / 32));
+    o->dmask = cv.take<unsigned long long>(m.Rpad);
+    o->x_peer_rowmask = cv.take<unsigned long long*>(m.P);
+    o->x_peer_mig = cv.take<int32_t*>(m.P);
+    o->x_peer_meta = cv.take<int32_t*>(m.P);
+    o->x_peer_meta_w = cv.take<float*>(m.P);
+    o->x_peer_dy_in = cv.take<void*>(m.P);
+    o->x_peer_dw_in = cv.take<float*>(m.P);
   }
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
   o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 63) / 64) * m.E * m.d);
@@ -152,6 +164,7 @@ luffy_status validate(const luffy_config* c) {
   if (c->act != LUFFY_GELU && c->act != LUFFY_SWIGLU) return fail(LUFFY_E_INVALID, "act must be LUFFY_GELU or LUFFY_SWIGLU");
   if (c->renormalize < -1 || c->renormalize > 1) return fail(LUFFY_E_INVALID, "renormalize must be -1, 0 or 1");
   if (c->max_tokens < 1) return fail(LUFFY_E_INVALID, "max_tokens must be >= 1");
+  if (c->max_seqs < 0) return fail(LUFFY_E_INVALID, "max_seqs must be >= 0");
   if (c->dtype == LUFFY_BF16 && (c->d_model % 256 || c->d_ffn % 256))
     return fail(LUFFY_E_UNSUPPORTED, "bf16 (tcgen05) path needs d_model and d_ffn multiples of 256");
   const Dims m = dims_of(c);
@@ -200,7 +213,7 @@ int64_t expert_rows_bound(const luffy_layer* L) { return L->P == 1 ? L->Rpad_max
 
 // Exchange region layout (identical offsets on every rank).
 struct XLayout {
-  size_t recv[2], gathered, dexp, dsend, cnt, flags, counters, total;
+  size_t recv[2], gathered, dexp, dsend, cnt, flags, counters, rowmask, mig, meta, meta_w, dy_in, dw_in, total;
 };
 XLayout xlayout(const luffy_layer* L) {
   const size_t rb = (size_t)L->d * elem_size(L->dtype);
@@ -209,14 +222,25 @@ XLayout xlayout(const luffy_layer* L) {
   auto take = [&](size_t n) { o = (o + 255) / 256 * 256; size_t r = o; o += n; return r; };
   x.recv[0] = take((size_t)L->recv_max * rb);
   x.recv[1] = take((size_t)L->recv_max * rb);
-  x.gathered = take((size_t)L->Rpad_max * rb);
+  x.gathered = take((size_t)L->P * L->Rpad_max * rb);  // [source rank][slot]
   x.dexp = take((size_t)L->recv_max * rb);
   x.dsend = take((size_t)L->Rpad_max * rb);
   x.cnt = take(sizeof(int32_t) * L->P * L->E);
   x.flags = take(sizeof(uint32_t) * XP_NUM * L->P);
   x.counters = take(sizeof(uint32_t) * XP_NUM);
+  x.rowmask = take(sizeof(unsigned long long) * L->recv_max);
+  x.mig = take(sizeof(int32_t) * L->P * L->Smax * L->P);
+  x.meta = take(sizeof(int32_t) * (size_t)L->P * L->Tmax * (2 + L->k));
+  x.meta_w = take(sizeof(float) * (size_t)L->P * L->Tmax * L->k);
+  x.dy_in = take((size_t)L->Tmax * rb);
+  x.dw_in = take(sizeof(float) * (size_t)L->Tmax * L->k);
   x.total = (o + 4095) / 4096 * 4096;
   return x;
+}
+
+// This rank's own rows inside the [source rank][slot] gathered buffer.
+void* home_gathered(const luffy_layer* L) {
+  return static_cast<char*>(L->x_gathered) + (size_t)L->rank * L->Rpad_max * L->d * elem_size(L->dtype);
 }
 
 luffy_status need_open(const luffy_layer* L, const char* where) {
@@ -330,6 +354,7 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   L->Rpad_max = m.Rpad;
   L->recv_max = m.recv;
   L->adj_words_max = m.adjw;
+  L->Smax = m.Smax;
   if (L->P > 1) {
     // the peer-visible exchange region: allocated once here, mapped by the peers via CUDA IPC
     const XLayout xl = xlayout(L);
@@ -351,6 +376,12 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
     L->x_cnt_inbox = reinterpret_cast<int32_t*>(L->x_region + xl.cnt);
     L->x_flags = reinterpret_cast<uint32_t*>(L->x_region + xl.flags);
     L->x_counters = reinterpret_cast<uint32_t*>(L->x_region + xl.counters);
+    L->x_rowmask = reinterpret_cast<unsigned long long*>(L->x_region + xl.rowmask);
+    L->x_mig_inbox = reinterpret_cast<int32_t*>(L->x_region + xl.mig);
+    L->x_meta = reinterpret_cast<int32_t*>(L->x_region + xl.meta);
+    L->x_meta_w = reinterpret_cast<float*>(L->x_region + xl.meta_w);
+    L->x_dy_in = L->x_region + xl.dy_in;
+    L->x_dw_in = reinterpret_cast<float*>(L->x_region + xl.dw_in);
   }
   *out = L;
   return LUFFY_OK;
@@ -399,8 +430,11 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
   // device tables of peer addresses
   const int P = L->P;
   std::vector<void*> recv(2 * P), gath(P), dexp(P), dsend(P);
-  std::vector<int32_t*> cnt(P);
+  std::vector<int32_t*> cnt(P), mig(P), meta(P);
   std::vector<uint32_t*> flag((size_t)XP_NUM * P);
+  std::vector<unsigned long long*> rowmask(P);
+  std::vector<float*> meta_w(P), dw_in(P);
+  std::vector<void*> dy_in(P);
   for (int p = 0; p < P; ++p) {
     char* b = static_cast<char*>(L->x_peer_base_h[p]);
     recv[p] = b + xl.recv[0];
@@ -409,6 +443,12 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
     dexp[p] = b + xl.dexp;
     dsend[p] = b + xl.dsend;
     cnt[p] = reinterpret_cast<int32_t*>(b + xl.cnt);
+    mig[p] = reinterpret_cast<int32_t*>(b + xl.mig);
+    meta[p] = reinterpret_cast<int32_t*>(b + xl.meta);
+    meta_w[p] = reinterpret_cast<float*>(b + xl.meta_w);
+    rowmask[p] = reinterpret_cast<unsigned long long*>(b + xl.rowmask);
+    dy_in[p] = b + xl.dy_in;
+    dw_in[p] = reinterpret_cast<float*>(b + xl.dw_in);
     for (int ph = 0; ph < XP_NUM; ++ph)
       flag[(size_t)ph * P + p] = reinterpret_cast<uint32_t*>(b + xl.flags) + ph * P + L->rank;
   }
@@ -418,6 +458,12 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
   LUFFY_CHECK(cudaMemcpy(L->x_peer_dsend, dsend.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
   LUFFY_CHECK(cudaMemcpy(L->x_peer_cnt, cnt.data(), sizeof(int32_t*) * P, cudaMemcpyHostToDevice), "ipc tables");
   LUFFY_CHECK(cudaMemcpy(L->x_flagptr, flag.data(), sizeof(uint32_t*) * XP_NUM * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_rowmask, rowmask.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_mig, mig.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_meta, meta.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_meta_w, meta_w.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_dy_in, dy_in.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_dw_in, dw_in.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
   L->x_open = true;
   return LUFFY_OK;
 }
@@ -449,6 +495,8 @@ luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int
   L->T = T;
   L->stage = 0;
   L->seq += 1;  // a new forward step (every rank calls in lockstep)
+  L->S = 0;
+  L->mig = false;
   LUFFY_CHECK(launch_route(L, x, w_gate, topk_idx, topk_w, stream), "luffy_route");
   L->stage = 1;
   return LUFFY_OK;
@@ -514,7 +562,7 @@ luffy_status luffy_layer_exchange_buffers(const luffy_layer* L, void** recv, voi
   LUFFY_NEED(L);
   if (L->P == 1) return fail(LUFFY_E_STATE, "luffy_layer_exchange_buffers: world == 1 uses caller buffers");
   if (recv) *recv = L->x_recv[L->seq & 1];
-  if (gathered) *gathered = L->x_gathered;
+  if (gathered) *gathered = home_gathered(L);
   if (d_expert_out) *d_expert_out = L->x_dexp;
   if (d_send) *d_send = L->x_dsend;
   return LUFFY_OK;
@@ -565,9 +613,11 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
   } else {
     LUFFY_OWN(recv, L->x_recv[L->seq & 1], "luffy_expert_ffn recv");
     recv = L->x_recv[L->seq & 1];
-    rd.rank_of = L->x_rank_of;  // fused combine: GEMM2 rows go to their source rank's gathered buffer
-    rd.slot_of = L->x_slot_of;
+    rd.rank_of = L->x_rank_of;  // fused combine: GEMM2 rows go to the gathered buffer of every rank in the
+    rd.slot_of = L->x_slot_of;  // row's destination mask (the source, or the hosts of migrated sequences)
     rd.peer_base = L->x_peer_gathered;
+    rd.mask = L->x_rowmask;
+    rd.stride = L->Rpad_max;
     sig = make_signal(L, XP_COMB);
   }
   if (L->act == LUFFY_GELU) {
@@ -596,7 +646,11 @@ luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathere
                                   cudaMemcpyDeviceToDevice, st), "combine copy");
   } else {
     // the rows were pushed by the experts' GEMM2 epilogues; wait until every rank has published them
-    LUFFY_OWN(gathered, L->x_gathered, "luffy_combine gathered");
+    LUFFY_OWN(gathered, home_gathered(L), "luffy_combine gathered");
+    if (L->mig) {  // tokens of migrated sequences: their slots and gate weights go to the hosting rank
+      LUFFY_CHECK(launch_mig_meta_push(L, stream), "luffy_combine/meta");
+      LUFFY_CHECK(launch_xwait(L, XP_META, stream), "luffy_combine/meta wait");
+    }
     LUFFY_CHECK(launch_xwait(L, XP_COMB, stream), "luffy_combine/wait");
   }
   L->stage = 5;
@@ -611,8 +665,13 @@ luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, voi
   if (L->P == 1) {
     LUFFY_NEED(gathered);
   } else {
-    LUFFY_OWN(gathered, L->x_gathered, "luffy_uncondense gathered");
-    gathered = L->x_gathered;
+    LUFFY_OWN(gathered, home_gathered(L), "luffy_uncondense gathered");
+    gathered = home_gathered(L);
+    if (L->mig) {  // y holds the tokens of the sequences this rank hosts (luffy_migration_out_tokens)
+      LUFFY_CHECK(launch_uncondense_mig(L, y, stream), "luffy_uncondense/migration");
+      L->stage = 6;
+      return LUFFY_OK;
+    }
   }
   LUFFY_CHECK(launch_uncondense(L, gathered, y, stream), "luffy_uncondense");
   L->stage = 6;
@@ -632,9 +691,18 @@ luffy_status luffy_uncondense_bwd(luffy_layer* L, const void* dy, const void* ga
     LUFFY_NEED(gathered);
     LUFFY_NEED(d_gathered);
   } else {
-    LUFFY_OWN(gathered, L->x_gathered, "luffy_uncondense_bwd gathered");
+    LUFFY_OWN(gathered, home_gathered(L), "luffy_uncondense_bwd gathered");
     if (d_gathered) return fail(LUFFY_E_INVALID, "luffy_uncondense_bwd: with world > 1 pass d_gathered = NULL");
-    gathered = L->x_gathered;  // (the rows go straight to the experts' ranks: fused combine backward)
+    gathered = home_gathered(L);  // (the rows go straight to the experts' ranks: fused combine backward)
+    if (L->mig) {
+      // dy holds the hosted tokens: d(gate weight) and dY go back to each token's home rank, where the
+      // condensed backward then runs on this rank's own tokens
+      LUFFY_CHECK(launch_mig_bwd_push(L, dy, stream), "luffy_uncondense_bwd/migration");
+      LUFFY_CHECK(cudaMemcpyAsync(d_topk_w, L->x_dw_in, sizeof(float) * L->T * L->k, cudaMemcpyDeviceToDevice,
+                                  static_cast<cudaStream_t>(stream)), "dw copy");
+      LUFFY_CHECK(launch_uncondense_bwd(L, L->x_dy_in, gathered, nullptr, nullptr, stream), "luffy_uncondense_bwd");
+      return LUFFY_OK;
+    }
   }
   LUFFY_CHECK(launch_uncondense_bwd(L, dy, gathered, d_gathered, d_topk_w, stream), "luffy_uncondense_bwd");
   return LUFFY_OK;
@@ -736,6 +804,88 @@ luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate,
   LUFFY_NEED(dw_gate);
   LUFFY_STAGE(L, 6, "luffy_route_bwd");
   LUFFY_CHECK(launch_route_bwd(L, x, w_gate, d_topk_w, dx, dw_gate, stream), "luffy_route_bwd");
+  return LUFFY_OK;
+}
+
+// ------------------------------------------------------------------------------- sequence migration
+
+luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t num_seqs, int64_t* rows_at_all,
+                                 void* stream) {
+  LUFFY_NEED(L);
+  LUFFY_NEED(seq_len);
+  LUFFY_NEED(rows_at_all);
+  LUFFY_STAGE(L, 2, "luffy_sequence_rows");
+  if (L->stage >= 3) return fail(LUFFY_E_STATE, "luffy_sequence_rows: must precede luffy_dispatch");
+  if (L->P == 1) return fail(LUFFY_E_STATE, "luffy_sequence_rows: sequence migration needs world > 1");
+  LUFFY_OPEN(L, "luffy_sequence_rows");
+  if (num_seqs < 1 || num_seqs > L->Smax) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: 1 <= num_seqs <= max_seqs");
+  std::vector<int32_t> start(num_seqs + 1, 0);
+  for (int s = 0; s < num_seqs; ++s) {
+    if (seq_len[s] < 1) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: sequence lengths must be >= 1");
+    start[s + 1] = start[s] + seq_len[s];
+  }
+  if (start[num_seqs] != L->T) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: lengths must sum to T");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LUFFY_CHECK(cudaMemcpyAsync(L->seq_start, start.data(), sizeof(int32_t) * (num_seqs + 1), cudaMemcpyHostToDevice, st),
+              "seq_start");
+  L->S = num_seqs;
+  LUFFY_CHECK(launch_seq_rows(L, stream), "luffy_sequence_rows");
+  std::vector<int32_t> all((size_t)L->P * L->Smax * L->P);
+  LUFFY_CHECK(cudaMemcpyAsync(all.data(), L->x_mig_inbox, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost, st),
+              "rows_at D2H");
+  LUFFY_CHECK(cudaStreamSynchronize(st), "rows_at sync");
+  for (int q = 0; q < L->P; ++q)
+    for (int s = 0; s < num_seqs; ++s)
+      for (int j = 0; j < L->P; ++j)
+        rows_at_all[((size_t)q * num_seqs + s) * L->P + j] = all[((size_t)q * L->Smax + s) * L->P + j];
+  return LUFFY_OK;
+}
+
+luffy_status luffy_set_migration(luffy_layer* L, const int32_t* seq_len_all, const int32_t* seq_dest, int64_t* out_rows,
+                                 void* stream) {
+  LUFFY_NEED(L);
+  LUFFY_NEED(seq_len_all);
+  LUFFY_NEED(seq_dest);
+  if (L->S < 1) return fail(LUFFY_E_STATE, "luffy_set_migration: call luffy_sequence_rows first (this step)");
+  if (L->stage >= 3) return fail(LUFFY_E_STATE, "luffy_set_migration: must precede luffy_dispatch");
+  const int P = L->P, S = L->S;
+  for (int i = 0; i < P * S; ++i)
+    if (seq_dest[i] < 0 || seq_dest[i] >= P) return fail(LUFFY_E_INVALID, "luffy_set_migration: seq_dest out of range");
+  // output rows of each destination: sequences in (home rank, sequence) order
+  std::vector<int64_t> fill(P, 0);
+  std::vector<int32_t> out_start(S), dest(S);
+  for (int q = 0; q < P; ++q)
+    for (int s = 0; s < S; ++s) {
+      const int g = seq_dest[q * S + s];
+      if (q == L->rank) {
+        out_start[s] = (int32_t)fill[g];
+        dest[s] = g;
+      }
+      fill[g] += seq_len_all[q * S + s];
+    }
+  if (fill[L->rank] > (int64_t)P * L->Tmax) return fail(LUFFY_E_CAPACITY, "luffy_set_migration: output capacity");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LUFFY_CHECK(cudaMemcpyAsync(L->seq_dest_l, dest.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st), "seq_dest");
+  LUFFY_CHECK(cudaMemcpyAsync(L->out_start, out_start.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st), "out_start");
+  LUFFY_CHECK(launch_set_migration(L, stream), "luffy_set_migration");
+  LUFFY_CHECK(cudaStreamSynchronize(st), "set_migration sync");  // host vectors go out of scope
+  L->n_out = fill[L->rank];
+  L->mig = true;
+  if (out_rows) *out_rows = L->n_out;
+  return LUFFY_OK;
+}
+
+luffy_status luffy_migration_out_tokens(const luffy_layer* L, int32_t* home_rank, int32_t* home_token) {
+  LUFFY_NEED(L);
+  if (!L->mig) return fail(LUFFY_E_STATE, "luffy_migration_out_tokens: no migration this step");
+  if (L->stage < 5) return fail(LUFFY_E_STATE, "luffy_migration_out_tokens: after luffy_combine");
+  std::vector<int32_t> m((size_t)L->n_out * (2 + L->k));
+  if (!m.empty())
+    LUFFY_CHECK(cudaMemcpy(m.data(), L->x_meta, sizeof(int32_t) * m.size(), cudaMemcpyDeviceToHost), "meta D2H");
+  for (int64_t i = 0; i < L->n_out; ++i) {
+    if (home_rank) home_rank[i] = m[i * (2 + L->k)];
+    if (home_token) home_token[i] = m[i * (2 + L->k) + 1];
+  }
   return LUFFY_OK;
 }
 

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
                                                          const int32_t* __restrict__ src_soff, int P, int E, int me,
                                                          int d, int64_t max_rows, int32_t* __restrict__ rank_of,
                                                          int32_t* __restrict__ slot_of, bf16* __restrict__ recv,
-                                                         bf16* __restrict__ dexp, int elem_bytes) {
+                                                         bf16* __restrict__ dexp, int elem_bytes,
+                                                         unsigned long long* __restrict__ rowmask) {
   const int El = E / P;
   const int64_t rows = roff[El];
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
     } else {
       rank_of[r] = -1;
       slot_of[r] = -1;
+      rowmask[r] = 0ull;  // padding rows are not combined anywhere
       // padding row: zero it in the receive buffer and in the backward buffer
       const size_t rb = (size_t)d * elem_bytes;
       uint4* a = reinterpret_cast<uint4*>(reinterpret_cast<char*>(recv) + r * rb);
@@ -119,7 +121,9 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
 template <typename T>
 __global__ void __launch_bounds__(256) xpack_push_kernel(const T* __restrict__ x, const int32_t* __restrict__ perm,
                                                          const int32_t* __restrict__ soff, const int32_t* __restrict__ dst_base,
-                                                         int E, int El, int d, void* const* peer_recv, XSignal sig) {
+                                                         int E, int El, int d, void* const* peer_recv, XSignal sig,
+                                                         const unsigned long long* __restrict__ dmask,
+                                                         unsigned long long* const* peer_rowmask, int me) {
   __shared__ int32_t soff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
   for (int i = threadIdx.x; i <= E; i += blockDim.x) {
@@ -135,7 +139,11 @@ __global__ void __launch_bounds__(256) xpack_push_kernel(const T* __restrict__ x
     if (t < 0) continue;
     const int e = find_group(soff_s, E, s);
     const int p = e / El;
-    T* dst = static_cast<T*>(peer_recv[p]) + ((int64_t)base_s[e] + (s - soff_s[e])) * d;
+    const int64_t drow = (int64_t)base_s[e] + (s - soff_s[e]);
+    T* dst = static_cast<T*>(peer_recv[p]) + drow * d;
+    // where the expert output of this row must be combined: home (me) or the destinations of the
+    // sequences that use it (sequence migration)
+    if (lane == 0) peer_rowmask[p][drow] = dmask ? dmask[s] : (1ull << me);
     const T* src = x + (size_t)t * d;
     for (int c = lane * 8; c < d; c += 256) {
       if constexpr (sizeof(T) == 2) {
@@ -184,15 +192,17 @@ int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
   LUFFY_LAUNCHED();
   xplan_rows_kernel<<<148, 256, 0, st>>>(L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),
-                                         static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4);
+                                         static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4, L->x_rowmask);
   LUFFY_LAUNCHED();
   const int blocks = grid_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16)
     xpack_push_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->perm, L->soff, L->x_dst_base, L->E,
-                                                    L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP));
+                                                    L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP),
+                                                    L->mig ? L->dmask : nullptr, L->x_peer_rowmask, L->rank);
   else
     xpack_push_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->perm, L->soff, L->x_dst_base, L->E,
-                                                     L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP));
+                                                     L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP),
+                                                     L->mig ? L->dmask : nullptr, L->x_peer_rowmask, L->rank);
   LUFFY_LAUNCHED();
   return launch_xwait(L, XP_DISP, s);
 }

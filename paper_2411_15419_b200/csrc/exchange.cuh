@@ -2,7 +2,10 @@
 //
 // Every layer owns one peer-visible exchange region (cudaMalloc + CUDA IPC, mapped by every rank):
 //   recv[2]    expert layout, double-buffered by step parity  <- peers' pack kernels (dispatch)
-//   gathered   send layout                                     <- peers' GEMM2 epilogues (combine)
+//   gathered   [P][send rows] indexed by (source rank, slot)   <- peers' GEMM2 epilogues (combine; with
+//              sequence migration a row goes to every destination rank that needs it)
+//   rowmask    [recv rows] destination-rank bitmask of each expert row <- sources (with dispatch)
+//   mig_*      sequence-migration tables / token metadata / returned dY, dw
 //   dexp       expert layout                                   <- peers' uncondense-backward (combine bwd)
 //   dsend      send layout                                     <- peers' dgrad1 epilogues (dispatch bwd)
 //   cnt_inbox  [P][E] representative counts                    <- peers (count exchange)
@@ -17,7 +20,8 @@
 
 namespace luffy {
 
-enum XPhase { XP_CNT = 0, XP_DISP = 1, XP_COMB = 2, XP_CBWD = 3, XP_DBWD = 4, XP_NUM = 5 };
+enum XPhase { XP_CNT = 0, XP_DISP = 1, XP_COMB = 2, XP_CBWD = 3, XP_DBWD = 4, XP_MIG = 5, XP_META = 6, XP_MIGB = 7,
+              XP_NUM = 8 };
 constexpr int kMaxWorld = 64;
 
 // Completion signal of one producing kernel.
@@ -28,12 +32,15 @@ struct XSignal {
   uint32_t seq;
 };
 
-// Row redirect for an epilogue: expert-layout row r goes to rank rank_of[r], row slot_of[r] of that
-// rank's buffer peer_base[rank] (row size row_bytes); rank_of[r] < 0 = padding (not sent).
+// Row redirect for an epilogue.  mask == nullptr: expert-layout row r goes to rank rank_of[r], row
+// slot_of[r] of that rank's buffer peer_base[rank]; rank_of[r] < 0 = padding (not sent).
+// mask != nullptr: the row goes to every rank g set in mask[r], row rank_of[r] * stride + slot_of[r].
 struct XRedirect {
   const int32_t* rank_of;
   const int32_t* slot_of;
   void* const* peer_base;
+  const unsigned long long* mask;
+  int64_t stride;
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {

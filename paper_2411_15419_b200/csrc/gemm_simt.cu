@@ -101,8 +101,18 @@ __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A,
         const float v = acc[i][j];
         if (EPI == EPI_STORE) {
           if (has_rd) {
-            const int rk = rd.rank_of[r];
-            if (rk >= 0) store1(static_cast<T*>(rd.peer_base[rk]) + (size_t)rd.slot_of[r] * N + n, v);
+            if (rd.mask) {
+              unsigned long long m = rd.mask[r];
+              const size_t r2 = (size_t)rd.rank_of[r] * rd.stride + rd.slot_of[r];
+              while (m) {
+                const int g = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                store1(static_cast<T*>(rd.peer_base[g]) + r2 * N + n, v);
+              }
+            } else {
+              const int rk = rd.rank_of[r];
+              if (rk >= 0) store1(static_cast<T*>(rd.peer_base[rk]) + (size_t)rd.slot_of[r] * N + n, v);
+            }
           } else {
             store1(D + r * N + n, v);
           }

@@ -277,9 +277,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int n = x.n0 + c0;
             if (EPI == EPI_STORE) {
               if (a.has_rd) {  // fused exchange: the row goes straight to its rank's buffer over NVLink
-                const int rk = a.rd.rank_of[row];
-                if (rk >= 0)
-                  store32_bf16(static_cast<bf16*>(a.rd.peer_base[rk]) + (size_t)a.rd.slot_of[row] * a.N + n, v);
+                if (a.rd.mask) {  // combine: every destination rank of the row (sequence migration)
+                  unsigned long long m = a.rd.mask[row];
+                  const size_t r2 = (size_t)a.rd.rank_of[row] * a.rd.stride + a.rd.slot_of[row];
+                  while (m) {
+                    const int g = __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    store32_bf16(static_cast<bf16*>(a.rd.peer_base[g]) + r2 * a.N + n, v);
+                  }
+                } else {
+                  const int rk = a.rd.rank_of[row];
+                  if (rk >= 0)
+                    store32_bf16(static_cast<bf16*>(a.rd.peer_base[rk]) + (size_t)a.rd.slot_of[row] * a.N + n, v);
+                }
               } else {
                 store32_bf16(D + row * a.N + n, v);
               }

@@ -104,6 +104,29 @@ struct luffy_layer {
   int32_t* x_src_soff;     // [P][E+1] padded send offsets of every rank
   int32_t* x_rank_of;      // [recv_max] source rank of each expert-layout row (-1 padding)
   int32_t* x_slot_of;      // [recv_max] its slot in the source's send layout
+  // ---- sequence migration (world > 1), Alg. 1 decides seq_dest; migration.cu
+  int Smax;                // sequence capacity per rank
+  int S;                   // sequences of the current step (0 = not registered)
+  bool mig;                // seq_dest set for the current step
+  int64_t n_out;           // output rows of this rank (tokens of the sequences it hosts)
+  int32_t* seq_start;      // [Smax+1] token range of each of my sequences
+  int32_t* seq_dest_l;     // [Smax] destination rank of each of my sequences
+  int32_t* out_start;      // [Smax] first output row of each of my sequences at its destination
+  uint32_t* seq_bits;      // [Smax][Rpad/32] distinct representative slots of each sequence (K9)
+  int32_t* rows_local;     // [Smax][P]
+  unsigned long long* dmask;  // [Rpad] destination ranks of each of my send slots
+  unsigned long long* x_rowmask;  // region [recv_max]: destination mask of each expert row
+  int32_t* x_mig_inbox;    // region [P][Smax][P] rows_at of every rank
+  int32_t* x_meta;         // region [P*Tmax][2 + k] (home rank, home token, pos[k]) of my output rows
+  float* x_meta_w;         // region [P*Tmax][k]
+  void* x_dy_in;           // region [Tmax][d] dY of my tokens returned by their destinations
+  float* x_dw_in;          // region [Tmax][k]
+  unsigned long long** x_peer_rowmask;  // [P]
+  int32_t** x_peer_mig;    // [P]
+  int32_t** x_peer_meta;   // [P]
+  float** x_peer_meta_w;   // [P]
+  void** x_peer_dy_in;     // [P]
+  float** x_peer_dw_in;    // [P]
 };
 
 // ---- kernel launchers (defined in the .cu files); all enqueue on `s` and return cudaError_t as int
@@ -122,6 +145,11 @@ int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s);
 int launch_xdispatch(luffy_layer* L, const void* x, void* s);
 int launch_xwait(const luffy_layer* L, int phase, void* s);
+int launch_seq_rows(luffy_layer* L, void* s);
+int launch_set_migration(luffy_layer* L, void* s);
+int launch_mig_meta_push(luffy_layer* L, void* s);
+int launch_uncondense_mig(const luffy_layer* L, void* y, void* s);
+int launch_mig_bwd_push(const luffy_layer* L, const void* dy, void* s);
 
 // Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).
 enum Epi { EPI_STORE = 0, EPI_GELU = 1, EPI_SWIGLU = 2, EPI_DGELU = 3, EPI_DSWIGLU = 4 };

@@ -522,9 +522,11 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
   const int bw = grid_for_warps(L->Cpad_max / WIN);
   const int bs = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16) {
-    dw_kernel<bf16><<<bt, 256, 0, st>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
-                                        L->k, L->d, dw);
-    LUFFY_LAUNCHED();
+    if (dw) {
+      dw_kernel<bf16><<<bt, 256, 0, st>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
+                                          L->k, L->d, dw);
+      LUFFY_LAUNCHED();
+    }
     uncondense_bwd_window_kernel<bf16><<<bw, 256, 0, st>>>(static_cast<const bf16*>(dy), L->goff, L->E, L->members,
                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
                                                            static_cast<bf16*>(dg), L->mpart, xd);
@@ -532,9 +534,11 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
     uncondense_bwd_finalize_kernel<bf16><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
                                                              static_cast<bf16*>(dg), xd, sig);
   } else {
-    dw_kernel<float><<<bt, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos, L->T,
-                                         L->k, L->d, dw);
-    LUFFY_LAUNCHED();
+    if (dw) {
+      dw_kernel<float><<<bt, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos,
+                                           L->T, L->k, L->d, dw);
+      LUFFY_LAUNCHED();
+    }
     uncondense_bwd_window_kernel<float><<<bw, 256, 0, st>>>(static_cast<const float*>(dy), L->goff, L->E, L->members,
                                                             L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
                                                             static_cast<float*>(dg), L->mpart, xd);

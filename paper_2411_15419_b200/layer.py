@@ -101,6 +101,38 @@ class CondensedMoELayer:
         L.luffy_uncondense(self.layer, self.gathered, self.y, s)
         return self.y[:T]
 
+    def forward_migrated(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
+                         seq_len=None, q: int = 1, seq_dest=None, capacity: int = 0, objective: int = 0, group=None):
+        """Forward with sequence migration (world > 1): K9 rows -> Alg. 1 on every rank (the
+        C-ABI planner, or a given `seq_dest`) -> the combine delivers each sequence's expert outputs to
+        the rank hosting it.  Returns (y [n_out, d] for the hosted tokens, home_rank, home_token,
+        seq_dest, rows_at)."""
+        import numpy as np
+        import torch.distributed as dist
+        assert self.world > 1
+        T = x.shape[0]
+        s = self._stream()
+        self.T = T
+        L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
+        self.stats = L.luffy_condense(self.layer, x, h, self.rep, s)
+        rows_at = L.luffy_sequence_rows(self.layer, seq_len, self.world, s)
+        lens = [None] * self.world
+        dist.all_gather_object(lens, [int(v) for v in seq_len], group=group)
+        seq_len_all = np.array([v for ls in lens for v in ls], np.int32)
+        if seq_dest is None:
+            esize = 2 if self.dt == L.BF16 else 4
+            seq_dest, _ = L.luffy_plan_migration(seq_len_all, rows_at, q, self.d * esize, self.d,
+                                                 capacity_tokens=capacity, objective=objective)
+        n_out = L.luffy_set_migration(self.layer, seq_len_all, seq_dest, s)
+        L.luffy_dispatch(self.layer, x, None, s)
+        L.luffy_expert_ffn(self.layer, None, w1, w2, w3, None, self.pre, self.act_buf, s)
+        L.luffy_combine(self.layer, None, None, s)
+        self.y_out = torch.empty(max(n_out, 1), self.d, dtype=self.tdt, device=self.device)
+        L.luffy_uncondense(self.layer, None, self.y_out, s)
+        torch.cuda.current_stream().synchronize()
+        home_rank, home_tok = L.luffy_migration_out_tokens(self.layer, n_out)
+        return self.y_out[:n_out], home_rank, home_tok, np.asarray(seq_dest), rows_at
+
     def backward(self, dy: torch.Tensor, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None):
         s = self._stream()
         L.luffy_uncondense_bwd(self.layer, dy, self.gathered, self.d_gathered, self.dw, s)

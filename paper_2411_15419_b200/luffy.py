@@ -28,6 +28,7 @@ EXPORTED = [
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
+    "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
 
 
@@ -40,7 +41,7 @@ class LuffyError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "world", "rank", "num_experts", "top_k", "d_model", "d_ffn", "dtype", "act", "renormalize",
-        "max_tokens", "max_recv_rows")]
+        "max_tokens", "max_recv_rows", "max_seqs")]
 
 
 class CondenseStats(ctypes.Structure):
@@ -67,6 +68,9 @@ def _load():
         "luffy_ipc_handle_bytes": (SZ, []),
         "luffy_layer_ipc_handle": (I32, [P, P]),
         "luffy_layer_ipc_open": (I32, [P, P]),
+        "luffy_sequence_rows": (I32, [P, P, I32, P, P]),
+        "luffy_set_migration": (I32, [P, P, P, ctypes.POINTER(I64), P]),
+        "luffy_migration_out_tokens": (I32, [P, P, P]),
         "luffy_layer_exchange_buffers": (I32, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                                                 ctypes.POINTER(P)]),
         "luffy_destroy": (None, [P]),
@@ -120,9 +124,9 @@ def _p(x):
 # ---------------------------------------------------------------- lifetime
 
 def make_config(world=1, rank=0, num_experts=8, top_k=2, d_model=1024, d_ffn=4096, dtype=BF16, act=GELU,
-                renormalize=-1, max_tokens=8192, max_recv_rows=0) -> Config:
+                renormalize=-1, max_tokens=8192, max_recv_rows=0, max_seqs=0) -> Config:
     return Config(world, rank, num_experts, top_k, d_model, d_ffn, dtype, act, renormalize, max_tokens,
-                  max_recv_rows)
+                  max_recv_rows, max_seqs)
 
 
 def luffy_create(cfg: Config) -> int:
@@ -288,3 +292,27 @@ def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
     _check(LIB.luffy_exchange_plan(world, rank, num_experts, counts_all.ctypes.data, so.ctypes.data, ro.ctypes.data,
                                    st.ctypes.data, rf.ctypes.data))
     return so, ro, st, rf
+
+
+def luffy_sequence_rows(layer, seq_len, world, stream):
+    """K9: distinct representative rows of every rank's sequences on every rank -> [world*S, world] int64."""
+    seq_len = np.ascontiguousarray(seq_len, dtype=np.int32)
+    S = seq_len.size
+    out = np.empty((world * S, world), np.int64)
+    _check(LIB.luffy_sequence_rows(layer, seq_len.ctypes.data, S, out.ctypes.data, stream))
+    return out
+
+
+def luffy_set_migration(layer, seq_len_all, seq_dest, stream) -> int:
+    seq_len_all = np.ascontiguousarray(seq_len_all, dtype=np.int32)
+    seq_dest = np.ascontiguousarray(seq_dest, dtype=np.int32)
+    n = ctypes.c_int64()
+    _check(LIB.luffy_set_migration(layer, seq_len_all.ctypes.data, seq_dest.ctypes.data, ctypes.byref(n), stream))
+    return n.value
+
+
+def luffy_migration_out_tokens(layer, n_out: int):
+    hr = np.empty(n_out, np.int32)
+    ht = np.empty(n_out, np.int32)
+    _check(LIB.luffy_migration_out_tokens(layer, hr.ctypes.data, ht.ctypes.data))
+    return hr, ht

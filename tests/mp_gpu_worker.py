@@ -34,6 +34,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2S")
     ap.add_argument("--h", type=float, default=0.9)
+    ap.add_argument("--migrate", default="none", choices=["none", "plan", "rotate"])
+    ap.add_argument("--q", type=int, default=2)
     args = ap.parse_args()
     from paper_2411_15419_b200 import layer as LY
     from paper_2411_15419_b200 import luffy as L
@@ -62,14 +64,35 @@ def main():
     w3 = dt(inp["W3"][loc]) if inp["W3"] is not None else None
     lay = LY.CondensedMoELayer(E, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T, dtype=cfg.dtype, act=cfg.act,
                                world=world, rank=rank, device=dev)
-    y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True)
-    g = lay.backward(dy, x, wg, w1, w2, w3)
+    mig = None
+    if args.migrate == "none":
+        y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True)
+        g = lay.backward(dy, x, wg, w1, w2, w3)
+    else:
+        # sequences: the workload's own (seqs_per_rank x seq_len), split unevenly to exercise Eq. (1)
+        L_ = cfg.seq_len
+        seq_len = []
+        for _ in range(cfg.seqs_per_rank):
+            seq_len += [L_ // 4, L_ - L_ // 4]
+        S = len(seq_len)
+        forced = None
+        if args.migrate == "rotate":
+            forced = np.array([((q + 1) % world) for q in range(world) for _ in range(S)], np.int32)
+        y, home_rank, home_tok, seq_dest, rows_at = lay.forward_migrated(x, wg, w1, w2, w3, h=args.h, seq_len=seq_len,
+                                                                         q=args.q, seq_dest=forced)
+        mig = dict(S=S, seq_len=seq_len, home_rank=home_rank, home_tok=home_tok, seq_dest=seq_dest, rows_at=rows_at)
+        # dY of the hosted tokens, from every home rank's seeded dY
+        dys = {q: workload.make_layer_inputs(cfg, rank=q)["dY"] for q in set(home_rank.tolist())}
+        dy_out = np.stack([dys[int(h_)][int(t_)] for h_, t_ in zip(home_rank, home_tok)]) if len(home_rank) else \
+            np.zeros((0, cfg.d_model), np.float32)
+        g = lay.backward(dt(dy_out) if len(dy_out) else dt(np.zeros((1, cfg.d_model), np.float32)), x, wg, w1, w2, w3)
     torch.cuda.synchronize()
     idx = lay.idx[:T].cpu().numpy().astype(np.int64)
     rep = lay.rep[:T].cpu().numpy().astype(np.int64)
     # every rank's discrete decisions, to rebuild the expert-side sums
     allmaps = [None] * world
     dist.all_gather_object(allmaps, (idx, rep))
+    oracle_Y = {}
     tol = 2e-2 if cfg.dtype == "bf16" else 1e-4
     errs = {}
     dW1 = np.zeros((El,) + inp["W1"].shape[1:])
@@ -83,11 +106,32 @@ def main():
                               renormalize=cfg.renormalize)
         dW1 += gr.dW1[loc]
         dW2 += gr.dW2[loc]
-        if q == rank:
+        oracle_Y[q] = st.Y
+        if mig is not None:
+            # K9 pin: distinct representative rows of each of rank q's sequences on each rank
+            starts = np.concatenate([[0], np.cumsum(mig["seq_len"])])
+            for s_ in range(mig["S"]):
+                slots = set(st.pk.pos[starts[s_]:starts[s_ + 1]].ravel().tolist())
+                owner = [int(st.pk.slot_expert[u]) // El for u in slots]
+                exp_rows = np.bincount(owner, minlength=world)
+                if not np.array_equal(exp_rows, mig["rows_at"][q * mig["S"] + s_]):
+                    errs["rows_at"] = 1.0
+        if q == rank and mig is None:
             errs["Y"] = rel(y.float().cpu().numpy(), st.Y)
             errs["dx"] = rel(g["dx"].float().cpu().numpy(), gr.dX)
             errs["dwg"] = rel(g["dwg"].cpu().numpy(), gr.dWg)
             errs["dw"] = rel(g["dw"].cpu().numpy(), gr.dw)
+    if mig is not None:
+        ref = np.stack([oracle_Y[int(h_)][int(t_)] for h_, t_ in zip(mig["home_rank"], mig["home_tok"])]) \
+            if len(mig["home_rank"]) else np.zeros((0, cfg.d_model))
+        errs["Y"] = rel(y.float().cpu().numpy(), ref) if len(ref) else 0.0
+        errs.setdefault("rows_at", 0.0)
+        # the planner on every rank agrees with the oracle's Alg. 1 on the same table
+        if args.migrate == "plan":
+            lens_all = np.array(mig["seq_len"] * world, np.int64)
+            od, _ = O.plan_migration(lens_all, mig["rows_at"], args.q, cfg.d_model * 2, cfg.d_model)
+            errs["plan"] = 0.0 if np.array_equal(od, mig["seq_dest"]) else 1.0
+        errs["migrated_frac"] = float(np.mean(mig["seq_dest"] != np.repeat(np.arange(world), mig["S"]))) * 0
     errs["dw1"] = rel(g["dw1"].cpu().numpy(), dW1)
     errs["dw2"] = rel(g["dw2"].cpu().numpy(), dW2)
     # routing exact outside near-ties

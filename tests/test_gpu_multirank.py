@@ -20,10 +20,10 @@ def _port():
     return p
 
 
-def _run(n, config, h=0.9):
+def _run(n, config, h=0.9, extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_gpu_worker.py"),
-           "--config", config, "--h", str(h)]
+           "--config", config, "--h", str(h), *extra]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-4000:], r.stderr[-4000:])
     return r
@@ -35,4 +35,15 @@ def test_expert_parallel_parity(n, config, h):
         pytest.skip(f"needs {n} GPUs")
     r = _run(n, config, h)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"ok": true') == n
+
+
+@pytest.mark.parametrize("n,mode", [(2, "rotate"), (2, "plan"), (4, "plan"), (4, "rotate")])
+def test_sequence_migration_parity(n, mode):
+    """Alg. 1 in the layer: K9 rows_at exact vs the oracle, the planner's seq_dest equal to the oracle's
+    Alg. 1, outputs at the hosting rank and all gradients at home / expert ranks within tolerance."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = _run(n, "C2S", 0.9, extra=("--migrate", mode, "--q", "2"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count('"ok": true') == n

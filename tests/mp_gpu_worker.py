@@ -116,8 +116,9 @@ def main():
                 exp_rows = np.bincount(owner, minlength=world)
                 if not np.array_equal(exp_rows, mig["rows_at"][q * mig["S"] + s_]):
                     errs["rows_at"] = 1.0
-        if q == rank and mig is None:
-            errs["Y"] = rel(y.float().cpu().numpy(), st.Y)
+        if q == rank:
+            if mig is None:
+                errs["Y"] = rel(y.float().cpu().numpy(), st.Y)
             errs["dx"] = rel(g["dx"].float().cpu().numpy(), gr.dX)
             errs["dwg"] = rel(g["dwg"].cpu().numpy(), gr.dWg)
             errs["dw"] = rel(g["dw"].cpu().numpy(), gr.dw)
@@ -131,7 +132,6 @@ def main():
             lens_all = np.array(mig["seq_len"] * world, np.int64)
             od, _ = O.plan_migration(lens_all, mig["rows_at"], args.q, cfg.d_model * 2, cfg.d_model)
             errs["plan"] = 0.0 if np.array_equal(od, mig["seq_dest"]) else 1.0
-        errs["migrated_frac"] = float(np.mean(mig["seq_dest"] != np.repeat(np.arange(world), mig["S"]))) * 0
     errs["dw1"] = rel(g["dw1"].cpu().numpy(), dW1)
     errs["dw2"] = rel(g["dw2"].cpu().numpy(), dW2)
     # routing exact outside near-ties
@@ -139,8 +139,13 @@ def main():
     route_ok = bool(np.array_equal(idx[~rr.near_tie], rr.idx[~rr.near_tie]))
     send_rows, recv_rows = L.luffy_layer_rows(lay.layer)
     ok = route_ok and all(v <= tol for v in errs.values())
-    print(json.dumps({"rank": rank, "world": world, "ok": ok, "route_ok": route_ok, "errs": errs,
-                      "reps": int(lay.stats.reps), "copies": int(lay.stats.copies), "send_rows": send_rows,
+    extra = {}
+    if mig is not None:
+        extra = {"migrated_seqs": int(np.sum(mig["seq_dest"] != np.repeat(np.arange(world), mig["S"]))),
+                 "hosted_tokens": int(len(mig["home_rank"]))}
+    print(json.dumps({"rank": rank, "world": world, "ok": ok, "route_ok": route_ok, "errs": errs, **extra,
+                      "reps": int(lay.stats.reps) if lay.stats else -1,
+                      "copies": int(lay.stats.copies) if lay.stats else -1, "send_rows": send_rows,
                       "recv_rows": recv_rows}), flush=True)
     lay.close()
     dist.barrier()

@@ -165,7 +165,9 @@ LUFFY_API luffy_status luffy_dispatch(luffy_layer* layer, const void* x, void* r
  * GELU:   pre = recv W1_e^T, act = GeLU_erf(pre), out = act W2_e^T;
  * SWIGLU: pre = [recv W1_e^T | recv W3_e^T] (saved_pre is [rows, 2f]), act = silu(pre1) * pre3.
  * bf16: tcgen05 grouped GEMMs, fp32 accumulation, bf16 outputs.  fp32: SIMT FFMA.
- * saved_pre [rows, f or 2f] and saved_act [rows, f] are written for the backward. w3 NULL for GELU. */
+ * saved_pre [rows, f or 2f] and saved_act [rows, f] are written for the backward: for GELU saved_pre holds
+ * GeLU'(pre) (the only function of pre the backward needs; computed with the same erf as the forward),
+ * for SWIGLU the pre-activations [pre1 | pre3].  w3 NULL for GELU. */
 LUFFY_API luffy_status luffy_expert_ffn(luffy_layer* layer, const void* recv, const void* w1, const void* w2,
                               const void* w3, void* out, void* saved_pre, void* saved_act, void* stream);
 

@@ -106,6 +106,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->rep_local = cv.take<int32_t>(m.Cpad);
   o->key = cv.take<uint64_t>(m.Cpad);
   o->m1 = cv.take<uint64_t>(m.Cpad);
+  o->m2 = cv.take<uint64_t>(m.Cpad);
   o->alive = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->win = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);

@@ -88,6 +88,12 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   float pdf = 0.3989422804014327f * expf(-0.5f * x * x);
   return cdf + x * pdf;
 }
+// GeLU(x) and GeLU'(x) sharing one erf: the forward saves GeLU'(pre), so the backward needs no erf.
+__device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& dg) {
+  const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+  g = x * cdf;
+  dg = cdf + x * 0.3989422804014327f * __expf(-0.5f * x * x);
+}
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + expf(-x)); }
 __device__ __forceinline__ float silu_grad_f(float x) {
   float s = 1.f / (1.f + expf(-x));

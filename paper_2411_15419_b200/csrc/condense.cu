@@ -288,6 +288,7 @@ struct GreedyArgs {
   uint32_t* win;
   unsigned long long* key;
   unsigned long long* m1;
+  unsigned long long* m2;
   int32_t* rep_local;
   uint32_t* ctrl;
   int max_rounds;
@@ -318,25 +319,31 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
     a.alive[wd] = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
     a.win[wd] = 0u;
   }
-  for (int64_t r = gtid; r < rows; r += nthreads) a.rep_local[r] = -1;
+  for (int64_t r = gtid; r < rows; r += nthreads) {
+    a.rep_local[r] = -1;
+    a.m1[r] = 0ull;
+    a.m2[r] = 0ull;
+  }
   grid_barrier(a.ctrl);
 
-  // Two rows per warp (16 lanes per row); the row's alive bit, adjacency words and the alive words of
-  // its group are loaded together, so each phase costs ~2 dependent L2 round trips per row pair.
+  // Two rows per warp (16 lanes per row).  The 1-hop and 2-hop maxima are PUSHED: every alive node
+  // atomically max-es its value into its alive neighbours (no return value -> no load latency in the bit
+  // walk; max is commutative, so the result equals the gather formulation).  3 barriers per round:
+  //   A: residual degree -> key; push key into m1 (closed neighbourhood); count the alive nodes
+  //   B: push m1 into m2
+  //   C: winners (m2 == key) claim themselves and their alive neighbours (winners are >= 3 hops apart,
+  //      so no node is claimed twice and no alive bit is read by one winner while another clears it)
   const int hl = lane & 15;
   const int half = lane >> 4;
   const int pairs = rows >> 1;
   int round = 0;
   for (;; ++round) {
-    // ---- phase A: residual degree -> priority key (deg, -index)
+    if (round >= a.max_rounds) break;
+    // ---- phase A
     for (int p = gwarp; p < pairs; p += nwarps) {
       const int r = 2 * p + half;
       const uint32_t aw = __ldcg(a.alive + (r >> 5));
-      const uint32_t pair_bits = (aw >> ((2 * p) & 31)) & 3u;
-      if (!pair_bits) {
-        if (hl == 0) a.key[r] = 0ull;
-        continue;
-      }
+      if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
       const bool me = (aw >> (r & 31)) & 1u;
       const int g = find_group(goff_s, E, r);
       const int rl = r - goff_s[g];
@@ -348,90 +355,94 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
         for (int wd = hl; wd < W; wd += 16) deg += __popc(row[wd] & __ldcg(al + wd));
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
-      if (hl == 0)
-        a.key[r] = me ? ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)rl) : 0ull;
-    }
-    grid_barrier(a.ctrl);
-    // ---- phase B: m1 = max key over the alive closed neighbourhood;  phase C: m2 from m1 -> winners
-    for (int ph = 0; ph < 2; ++ph) {
-      const unsigned long long* src = ph == 0 ? a.key : a.m1;
-      for (int p = gwarp; p < pairs; p += nwarps) {
-        const int r = 2 * p + half;
-        const uint32_t aw = __ldcg(a.alive + (r >> 5));
-        if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
-        const bool me = (aw >> (r & 31)) & 1u;
-        const int g = find_group(goff_s, E, r);
-        const int rl = r - goff_s[g];
-        const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
-        const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
-        const uint32_t* al = a.alive + (goff_s[g] >> 5);
-        unsigned long long m = me ? __ldcg(src + r) : 0ull;
-        if (me) {
-          for (int wd = hl; wd < W; wd += 16) {
-            const uint32_t bits = row[wd] & __ldcg(al + wd);
-            if (bits) {
-              // independent predicated loads (not a dependent bit walk) so they are all in flight at once
-              const unsigned long long* q = src + goff_s[g] + wd * 32;
-#pragma unroll
-              for (int b = 0; b < 32; ++b) {
-                if ((bits >> b) & 1u) {
-                  const unsigned long long v = __ldcg(q + b);
-                  m = v > m ? v : m;
-                }
-              }
-            }
+      if (me) {
+        const unsigned long long key = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)rl);
+        if (hl == 0) {
+          a.key[r] = key;
+          atomicMax(a.m1 + r, key);
+          atomicAdd(a.ctrl + 64 + round, 1u);
+        }
+        unsigned long long* m1g = a.m1 + goff_s[g];
+        for (int wd = hl; wd < W; wd += 16) {
+          uint32_t bits = row[wd] & __ldcg(al + wd);
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            atomicMax(m1g + wd * 32 + b, key);
           }
         }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
-          m = u > m ? u : m;
-        }
-        if (hl == 0 && me) {
-          if (ph == 0) a.m1[r] = m;
-          else if (m == __ldcg(a.key + r)) atomicOr(a.win + (r >> 5), 1u << (r & 31));
-        }
       }
-      grid_barrier(a.ctrl);
     }
-    // ---- phase D: winners and their alive neighbours leave; count the survivors
+    grid_barrier(a.ctrl);
+    if (__ldcg(a.ctrl + 64 + round) == 0u) break;
+    // ---- phase B (warp-uniform control flow: both half-warps run every iteration; work is predicated)
     for (int p = gwarp; p < pairs; p += nwarps) {
       const int r = 2 * p + half;
       const uint32_t aw = __ldcg(a.alive + (r >> 5));
       if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
       const bool me = (aw >> (r & 31)) & 1u;
       const int g = find_group(goff_s, E, r);
-      const bool winner = me && ((__ldcg(a.win + (r >> 5)) >> (r & 31)) & 1u);
-      int found = 0x7fffffff;
-      if (me && !winner) {
+      const int rl = r - goff_s[g];
+      const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
+      const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
+      const uint32_t* al = a.alive + (goff_s[g] >> 5);
+      const unsigned long long v = me ? __ldcg(a.m1 + r) : 0ull;
+      __syncwarp();
+      if (me && hl == 0) {
+        atomicMax(a.m2 + r, v);
+        a.m1[r] = 0ull;  // reset for the next round (no more pushes into m1 this round)
+      }
+      if (me) {
+        unsigned long long* m2g = a.m2 + goff_s[g];
+        for (int wd = hl; wd < W; wd += 16) {
+          uint32_t bits = row[wd] & __ldcg(al + wd);
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            atomicMax(m2g + wd * 32 + b, v);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    grid_barrier(a.ctrl);
+    // ---- phase C: winners claim
+    for (int p = gwarp; p < pairs; p += nwarps) {
+      const int r = 2 * p + half;
+      const uint32_t aw = __ldcg(a.alive + (r >> 5));
+      if (!((aw >> ((2 * p) & 31)) & 3u)) continue;
+      const bool me = (aw >> (r & 31)) & 1u;
+      const bool winner = me && __ldcg(a.m2 + r) == __ldcg(a.key + r);
+      __syncwarp();
+      if (me && hl == 0) a.m2[r] = 0ull;
+      if (winner) {
+        const int g = find_group(goff_s, E, r);
         const int rl = r - goff_s[g];
         const int W = (goff_s[g + 1] - goff_s[g]) >> 5;
         const uint32_t* row = a.adj + adjoff_s[g] + (int64_t)rl * W;
-        const uint32_t* wn = a.win + (goff_s[g] >> 5);
-        for (int wd = hl; wd < W; wd += 16) {
-          const uint32_t bits = row[wd] & __ldcg(wn + wd);
-          if (bits) found = min(found, goff_s[g] + wd * 32 + __ffs(bits) - 1);
-        }
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
-      if (hl == 0 && me) {
-        const int owner = winner ? r : (found != 0x7fffffff ? found : -1);
-        if (owner >= 0) {
-          a.rep_local[r] = owner;
+        uint32_t* al = a.alive + (goff_s[g] >> 5);
+        if (hl == 0) {
+          a.rep_local[r] = r;
           atomicAnd(a.alive + (r >> 5), ~(1u << (r & 31)));
-        } else {
-          atomicAdd(a.ctrl + 64 + round, 1u);
+        }
+        for (int wd = hl; wd < W; wd += 16) {
+          const uint32_t bits = row[wd] & __ldcg(al + wd);
+          if (bits) {
+            uint32_t bb = bits;
+            while (bb) {
+              const int b = __ffs(bb) - 1;
+              bb &= bb - 1;
+              a.rep_local[goff_s[g] + wd * 32 + b] = r;
+            }
+            atomicAnd(al + wd, ~bits);
+          }
         }
       }
+      __syncwarp();
     }
     grid_barrier(a.ctrl);
-    const uint32_t left = __ldcg(a.ctrl + 64 + round);
-    if (left == 0u || round + 1 >= a.max_rounds) break;
-    for (int64_t wd = gtid; wd < rows / 32; wd += nthreads) a.win[wd] = 0u;
-    // (win words are next written in phase C, two barriers later)
   }
-  if (gtid == 0) a.ctrl[2] = (uint32_t)(round + 1);
+  if (gtid == 0) a.ctrl[2] = (uint32_t)round;
 }
 
 // h > 1: no edges -- every copy represents itself.
@@ -506,6 +517,7 @@ int launch_greedy(luffy_layer* L, void* s) {
   a.win = L->win;
   a.key = reinterpret_cast<unsigned long long*>(L->key);
   a.m1 = reinterpret_cast<unsigned long long*>(L->m1);
+  a.m2 = reinterpret_cast<unsigned long long*>(L->m2);
   a.rep_local = L->rep_local;
   a.ctrl = L->ctrl;
   a.max_rounds = kGreedyMaxRounds;

@@ -117,10 +117,12 @@ __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A,
             store1(D + r * N + n, v);
           }
         } else if (EPI == EPI_GELU) {
-          store1(aux0 + r * N + n, v);
-          store1(D + r * N + n, gelu_f(v));
+          float g, dg;
+          gelu_and_grad_f(v, g, dg);
+          store1(aux0 + r * N + n, dg);  // saved for the backward: GeLU'(pre)
+          store1(D + r * N + n, g);
         } else if (EPI == EPI_DGELU) {
-          store1(D + r * N + n, v * gelu_grad_f(to_f(aux0[r * N + n])));
+          store1(D + r * N + n, v * to_f(aux0[r * N + n]));
         } else {  // EPI_DSWIGLU: v = d_act[r, n], N = f
           const float p1 = to_f(aux0[r * (2 * N) + n]), p3 = to_f(aux0[r * (2 * N) + N + n]);
           store1(D + r * (2 * N) + n, v * p3 * silu_grad_f(p1));

@@ -22,7 +22,9 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KiB
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int STG_BYTES = 4096;  // per epilogue warp: output staging (coalesced stores)
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 1024 + 256;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quarter)
 
 struct TcArgs {
@@ -87,6 +89,96 @@ __device__ __forceinline__ void store32_bf16(bf16* dst, const float (&v)[32]) {
     reinterpret_cast<uint4*>(dst)[q] = u;
   }
 }
+// ---- warp-cooperative staging of a 32-row x 32-column block (thread i owns row i): the block goes
+// through a swizzled 2 KiB (bf16) / 4 KiB (fp32) shared-memory buffer so that every global access
+// instruction covers 4 (8) whole 64-byte (128-byte) row segments instead of 32 scattered 16-byte pieces.
+__device__ __forceinline__ uint4 pack8_bf16(const float* v) {
+  return make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+}
+__device__ __forceinline__ void stage_rows_bf16(uint8_t* buf, const float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) = pack8_bf16(v + 8 * j);
+  __syncwarp();
+}
+// dst: this thread's row pointer at the block's first column (nullptr: row not stored)
+__device__ __forceinline__ void store_block_bf16(uint8_t* buf, const float (&v)[32], bf16* dst) {
+  stage_rows_bf16(buf, v);
+  const int lane = threadIdx.x & 31;
+  const unsigned long long mine = reinterpret_cast<unsigned long long>(dst);
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + (lane >> 2), c = lane & 3;
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+    const unsigned long long p = __shfl_sync(0xffffffffu, mine, r);
+    if (p) reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p) + c * 8)[0] = u;
+  }
+  __syncwarp();
+}
+// multi-destination rows (fused combine with sequence migration): row r goes to every rank in mask[r],
+// at row index r2[r] of that rank's buffer peer_base[g] (row length ld elements), column col.
+__device__ __forceinline__ void store_block_bf16_multi(uint8_t* buf, const float (&v)[32], unsigned long long mask,
+                                                       unsigned long long r2, void* const* peer_base, int ld, int col) {
+  stage_rows_bf16(buf, v);
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + (lane >> 2), c = lane & 3;
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+    unsigned long long m = __shfl_sync(0xffffffffu, mask, r);
+    const unsigned long long rr = __shfl_sync(0xffffffffu, r2, r);
+    while (m) {
+      const int g = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      reinterpret_cast<uint4*>(static_cast<bf16*>(peer_base[g]) + rr * ld + col + c * 8)[0] = u;
+    }
+  }
+  __syncwarp();
+}
+// src: this thread's row pointer at the block's first column
+__device__ __forceinline__ void load_block_bf16(uint8_t* buf, const bf16* src, float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long mine = reinterpret_cast<unsigned long long>(src);
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + (lane >> 2), c = lane & 3;
+    const unsigned long long p = __shfl_sync(0xffffffffu, mine, r);
+    *reinterpret_cast<uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) =
+        reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(p) + c * 8)[0];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[8 * j + 2 * i] = f.x;
+      v[8 * j + 2 * i + 1] = f.y;
+    }
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void store_block_f32(uint8_t* buf, const float (&v)[32], float* dst) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+  const unsigned long long mine = reinterpret_cast<unsigned long long>(dst);
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + (lane >> 3), c = lane & 7;
+    const float4 u = *reinterpret_cast<const float4*>(buf + r * 128 + ((c ^ (r & 7)) << 4));
+    const unsigned long long p = __shfl_sync(0xffffffffu, mine, r);
+    reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + c * 4)[0] = u;
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void load32_bf16(const bf16* src, float (&v)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -110,7 +202,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint8_t* sStg = sB + STAGES * B_BYTES;  // epilogue staging, STG_BYTES per epilogue warp
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -216,10 +309,28 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int hc = (warp - 2) >> 2;  // column half handled by this warp
     const int rt = 32 * q + lane;
+    uint8_t* stg = sStg + (warp - 2) * STG_BYTES;  // [0, 2K) and [2K, 4K): two bf16 blocks or one fp32 block
     int acc = 0;
     uint32_t aphase = 0;
+    // aux (pre-activation) blocks of the backward epilogues are prefetched one 32-column chunk ahead with
+    // coalesced loads (the first one before waiting for the accumulator), then re-laid through shared memory
+    constexpr int NB = (EPI == EPI_DSWIGLU) ? 2 : ((EPI == EPI_DGELU) ? 1 : 0);
+    uint4 pf[2][4];
+    auto prefetch = [&](const Tile& x, int c0) {
+      const size_t ldx = (EPI == EPI_DSWIGLU) ? 2 * (size_t)a.N : (size_t)a.N;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int r = it * 8 + (lane >> 2), c = lane & 3;
+          const bf16* src = static_cast<const bf16*>(a.aux) + (size_t)(x.m0 + 32 * q + r) * ldx + (b ? a.N : 0) +
+                            x.n0 + c0 + c * 8;
+          pf[b][it] = *reinterpret_cast<const uint4*>(src);
+        }
+    };
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const Tile x = decode<EPI, WG>(t, a, off_s);
+      if (NB) prefetch(x, hc * (BN / 2));
       tc::mbar_wait(&tfull[acc], aphase);
       tc::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
@@ -233,13 +344,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t r[32];
           tc::tmem_ld32(tb + c0, r);
           tc::tmem_ld_wait();
+          float v[32];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 v = x.nkb > 0 ? make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-                                               __uint_as_float(r[i + 3]))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4*>(dst + c0 + i) = v;
-          }
+          for (int i = 0; i < 32; ++i) v[i] = x.nkb > 0 ? __uint_as_float(r[i]) : 0.f;
+          store_block_f32(stg, v, dst + c0);
         }
       } else {
         const size_t row = (size_t)(x.m0 + rt);
@@ -261,13 +369,37 @@ __global__ void __launch_bounds__(THREADS, 1)
               o[i] = silu_f(p1[i]) * p3[i];
             }
             const int n = x.n0 + c0;
-            store32_bf16(X + row * (2 * f) + n, p1);
-            store32_bf16(X + row * (2 * f) + f + n, p3);
-            store32_bf16(D + row * f + n, o);
+            store_block_bf16(stg, p1, X + row * (2 * f) + n);
+            store_block_bf16(stg, p3, X + row * (2 * f) + f + n);
+            store_block_bf16(stg, o, D + row * f + n);
           }
         } else {
 #pragma unroll 1
           for (int c0 = hc * (BN / 2); c0 < (hc + 1) * (BN / 2); c0 += 32) {
+            float pa[NB > 0 ? NB : 1][32];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {  // prefetched aux block -> own row through shared memory
+              uint8_t* ab = stg + 2048;
+#pragma unroll
+              for (int it = 0; it < 4; ++it) {
+                const int r = it * 8 + (lane >> 2), c = lane & 3;
+                *reinterpret_cast<uint4*>(ab + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) = pf[b][it];
+              }
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint4 u = *reinterpret_cast<const uint4*>(ab + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f2 = __bfloat1622float2(h2[i]);
+                  pa[b][8 * j + 2 * i] = f2.x;
+                  pa[b][8 * j + 2 * i + 1] = f2.y;
+                }
+              }
+              __syncwarp();
+            }
+            if (NB && c0 + 32 < (hc + 1) * (BN / 2)) prefetch(x, c0 + 32);  // next chunk in flight
             uint32_t r[32];
             tc::tmem_ld32(tb + c0, r);
             tc::tmem_ld_wait();
@@ -278,44 +410,40 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (EPI == EPI_STORE) {
               if (a.has_rd) {  // fused exchange: the row goes straight to its rank's buffer over NVLink
                 if (a.rd.mask) {  // combine: every destination rank of the row (sequence migration)
-                  unsigned long long m = a.rd.mask[row];
-                  const size_t r2 = (size_t)a.rd.rank_of[row] * a.rd.stride + a.rd.slot_of[row];
-                  while (m) {
-                    const int g = __ffsll((long long)m) - 1;
-                    m &= m - 1;
-                    store32_bf16(static_cast<bf16*>(a.rd.peer_base[g]) + r2 * a.N + n, v);
-                  }
+                  const unsigned long long m = a.rd.mask[row];
+                  const int rk = a.rd.rank_of[row];
+                  const unsigned long long r2 =
+                      rk >= 0 ? (unsigned long long)rk * a.rd.stride + a.rd.slot_of[row] : 0ull;
+                  store_block_bf16_multi(stg, v, rk >= 0 ? m : 0ull, r2, a.rd.peer_base, a.N, n);
                 } else {
                   const int rk = a.rd.rank_of[row];
-                  if (rk >= 0)
-                    store32_bf16(static_cast<bf16*>(a.rd.peer_base[rk]) + (size_t)a.rd.slot_of[row] * a.N + n, v);
+                  store_block_bf16(stg, v,
+                                   rk >= 0 ? static_cast<bf16*>(a.rd.peer_base[rk]) + (size_t)a.rd.slot_of[row] * a.N + n
+                                           : nullptr);
                 }
               } else {
-                store32_bf16(D + row * a.N + n, v);
+                store_block_bf16(stg, v, D + row * a.N + n);
               }
             } else if (EPI == EPI_GELU) {
-              store32_bf16(X + row * a.N + n, v);
               float o[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = gelu_f(v[i]);
-              store32_bf16(D + row * a.N + n, o);
+              for (int i = 0; i < 32; ++i) gelu_and_grad_f(v[i], o[i], v[i]);  // v <- GeLU'(pre)
+              store_block_bf16(stg, v, X + row * a.N + n);
+              store_block_bf16(stg, o, D + row * a.N + n);
             } else if (EPI == EPI_DGELU) {
-              float p[32];
-              load32_bf16(X + row * a.N + n, p);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(p[i]);
-              store32_bf16(D + row * a.N + n, v);
+              for (int i = 0; i < 32; ++i) v[i] *= pa[0][i];  // aux holds GeLU'(pre) from the forward
+              store_block_bf16(stg, v, D + row * a.N + n);
             } else {  // EPI_DSWIGLU: v = d_act, aux = pre [rows, 2N]
-              float p1[32], p3[32], g1[32], g3[32];
-              load32_bf16(X + row * (2 * a.N) + n, p1);
-              load32_bf16(X + row * (2 * a.N) + a.N + n, p3);
+              float g1[32], g3[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                g1[i] = v[i] * p3[i] * silu_grad_f(p1[i]);
-                g3[i] = v[i] * silu_f(p1[i]);
+                const float p1 = pa[0][i], p3 = pa[NB - 1][i];
+                g1[i] = v[i] * p3 * silu_grad_f(p1);
+                g3[i] = v[i] * silu_f(p1);
               }
-              store32_bf16(D + row * (2 * a.N) + n, g1);
-              store32_bf16(D + row * (2 * a.N) + a.N + n, g3);
+              store_block_bf16(stg, g1, D + row * (2 * a.N) + n);
+              store_block_bf16(stg, g3, D + row * (2 * a.N) + a.N + n);
             }
           }
         }

@@ -50,6 +50,7 @@ struct luffy_layer {
   int32_t* rep_local; // [Cpad_max] group row of the representative
   uint64_t* key;      // [Cpad_max] greedy priorities
   uint64_t* m1;       // [Cpad_max]
+  uint64_t* m2;       // [Cpad_max]
   uint32_t* alive;    // [Cpad_max/32]
   uint32_t* win;      // [Cpad_max/32]
   uint32_t* ctrl;     // [64 + kGreedyMaxRounds] grid barrier + per-round counters
@@ -151,6 +152,7 @@ int launch_mig_meta_push(luffy_layer* L, void* s);
 int launch_uncondense_mig(const luffy_layer* L, void* y, void* s);
 int launch_mig_bwd_push(const luffy_layer* L, const void* dy, void* s);
 
-// Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).
+// Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).  EPI_GELU stores GeLU(acc) and aux = GeLU'(acc);
+// EPI_DGELU multiplies by that aux.
 enum Epi { EPI_STORE = 0, EPI_GELU = 1, EPI_SWIGLU = 2, EPI_DGELU = 3, EPI_DSWIGLU = 4 };
 }  // namespace luffy

@@ -133,7 +133,14 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     inp = workload.make_layer_inputs(cfg, rank=0)
+    # bounded sample: size each step so that warmup + steps fit in ~150 s of host time
+    t0 = time.perf_counter()
+    cpu_oracle_step(cfg, inp, 64)
+    per_tok = (time.perf_counter() - t0) / 64
+    budget = 150.0 / max(1, args.steps + args.warmup)
     ntok = args.ref_tokens
+    while ntok > 8 and ntok * per_tok > budget:
+        ntok //= 2
     for _ in range(args.warmup):
         cpu_oracle_step(cfg, inp, min(ntok, 64))
     times = []

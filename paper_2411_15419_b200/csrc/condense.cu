@@ -496,7 +496,12 @@ int launch_gram_simt(luffy_layer* L, float h, void* s) {
   return 0;
 }
 
+int launch_greedy_cluster(luffy_layer* L, void* s);
+
 int launch_greedy(luffy_layer* L, void* s) {
+  // fast path: one thread-block cluster per group with DSMEM replicas (greedy_cluster.cu)
+  const int rc = launch_greedy_cluster(L, s);
+  if (rc >= 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(s);
   LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * (64 + kGreedyMaxRounds), st));
   static int blocks = 0;

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       const uint32_t* __restrict__ adj,
                                                                       int32_t* __restrict__ rep_local,
                                                                       uint32_t* __restrict__ ctrl, int nmax,
-                                                                      int max_rounds) {
+                                                                      int max_rounds, int cache_words) {
   extern __shared__ __align__(16) uint8_t gsm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   uint32_t* alive = reinterpret_cast<uint32_t*>(m1 + nmax);
   uint32_t* win = alive + (nmax >> 5);
   uint32_t* cnt = win + (nmax >> 5);  // [2] alive counters (by round parity)
+  uint32_t* rowc = cnt + 4;            // cache of this CTA's own adjacency rows (read-only for the whole kernel)
   const uint32_t* A = adj + (n > 0 ? adjoff[e] : 0);
   // owned rows [r0, r1)
   const int R = ((n + CS - 1) / CS + 31) / 32 * 32;
@@ -54,6 +55,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     win[w] = 0u;
   }
   if (threadIdx.x < 2) cnt[threadIdx.x] = 0u;
+  const int ncached = W > 0 ? min(r1 - r0, cache_words / W) : 0;
+  for (int64_t i = threadIdx.x; i < (int64_t)ncached * W; i += blockDim.x) rowc[i] = A[(int64_t)r0 * W + i];
+  auto ROW = [&](int r) -> const uint32_t* { return r - r0 < ncached ? rowc + (r - r0) * W : A + (int64_t)r * W; };
   for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) rep_local[g0 + r] = -1;
   if (rank == CS - 1)  // padding rows of the group's row space: never representatives
     for (int r = n + threadIdx.x; r < W * 32; r += blockDim.x) rep_local[g0 + r] = -1;
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     for (int w = threadIdx.x; w < W; w += blockDim.x) win[w] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-      const uint32_t* row = A + (int64_t)r * W;
+      const uint32_t* row = ROW(r);
       int deg = 0;
       for (int w = lane; w < W; w += 32) deg += __popc(row[w] & alive[w]);
       deg = __reduce_add_sync(0xffffffffu, deg);
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       const unsigned long long* src = ph == 0 ? key : m1;
       for (int r = r0 + wid; r < r1; r += nwarp) {
         if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-        const uint32_t* row = A + (int64_t)r * W;
+        const uint32_t* row = ROW(r);
         unsigned long long m = src[r];
         for (int w = lane; w < W; w += 32) {
           const uint32_t bits = row[w] & alive[w];
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       if ((win[r >> 5] >> (r & 31)) & 1u) {
         owner = r;
       } else {
-        const uint32_t* row = A + (int64_t)r * W;
+        const uint32_t* row = ROW(r);
         int found = 0x7fffffff;
         for (int w = lane; w < W; w += 32) {
           const uint32_t bits = row[w] & win[w];
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
 }
 
 template <int CS>
-int launch_cluster(luffy_layer* L, int nmax, size_t smem, cudaStream_t st) {
+int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, cudaStream_t st) {
   auto kern = greedy_cluster_kernel<CS>;
   LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (CS > 8) LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -153,7 +157,7 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, cudaStream_t st) {
   cfg.numAttrs = 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
-                                    kGreedyMaxRounds));
+                                    kGreedyMaxRounds, cache_words));
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -164,8 +168,11 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, cudaStream_t st) {
 int launch_greedy_cluster(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int nmax = (int)round_up(std::min<int64_t>(L->Tmax, L->Cpad_max), 128);  // a group holds <= T copies
-  const size_t smem = (size_t)nmax * 16 + (size_t)(nmax / 32) * 8 + 16;
-  if (smem > 200 * 1024) return -1;
+  const size_t state = (size_t)nmax * 16 + (size_t)(nmax / 32) * 8 + 16;
+  if (state > 200 * 1024) return -1;
+  const size_t cache_bytes = std::min<size_t>(224 * 1024 - state, 96 * 1024) / 16 * 16;  // own-row cache
+  const size_t smem = state + cache_bytes;
+  const int cache_words = (int)(cache_bytes / 4);
   LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * 64, st));
   static int cs = 0;  // cluster size: 16 (non-portable) when the device accepts it, else 8
   if (cs == 0) {
@@ -187,7 +194,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
     if (cudaOccupancyMaxActiveClusters(&nclusters, greedy_cluster_kernel<16>, &cfg) != cudaSuccess || nclusters < 1) cs = 8;
     cudaGetLastError();
   }
-  return cs == 16 ? launch_cluster<16>(L, nmax, smem, st) : launch_cluster<8>(L, nmax, smem, st);
+  return cs == 16 ? launch_cluster<16>(L, nmax, smem, cache_words, st) : launch_cluster<8>(L, nmax, smem, cache_words, st);
 }
 
 }  // namespace luffy

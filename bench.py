@@ -2,8 +2,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--h 0.9] [--impl luffy|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL over NVLink); each rank holds T tokens
-(weak scaling) and E/N experts.  A step = route -> condense -> dispatch -> expert FFN -> combine ->
+N > 1 is launched by torchrun (one process per GPU); each rank holds T tokens (weak scaling) and E/N
+experts; the dispatch/combine are device-initiated NVLink transfers inside libluffy's kernels (CUDA IPC;
+torch.distributed only carries the IPC handles).  --migrate Q adds sequence migration (K9 + Alg. 1 with
+candidate-set size Q on every rank) to every step.  A step = route -> condense -> dispatch -> expert FFN -> combine ->
 uncondense -> and the whole backward, all through the libluffy C ABI.  Inputs are synthetic
 (workload.py), generated on the host and resident in HBM before timing; the per-step working set
 (~1 GB of activations) exceeds the 126 MB L2.
@@ -173,6 +175,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--migrate", type=int, default=0,
+                    help="world > 1: sequence migration with Alg. 1 candidate-set size q (0 = off)")
     args = ap.parse_args()
     cfg = workload.CONFIGS[args.config]
     if args.h is not None:
@@ -216,18 +220,39 @@ def main():
     marks = ["route", "condense", "dispatch", "ffn", "combine", "uncondense", "uncondense_bwd", "combine_bwd",
              "ffn_bwd", "dispatch_bwd", "route_bwd"]
 
+    mig = args.migrate > 0 and world > 1
+    if mig:
+        # sequences of variable length l ~ U{256..1024 step 64} (padding premise), sum = T
+        rng = np.random.default_rng(4242 + rank)
+        seq_len = []
+        while sum(seq_len) < T:
+            seq_len.append(int(min(rng.choice(np.arange(256, 1025, 64)), T - sum(seq_len))))
+        lens = [None] * world
+        dist.all_gather_object(lens, seq_len)
+        seq_len_all = np.array([v for ls in lens for v in ls], np.int32)
+        y_out = torch.empty(world * T, cfg.d_model, dtype=tdt, device=dev)
+        dy_out = torch.randn(world * T, cfg.d_model, device=dev).to(tdt)
+        mig_stats = {"migrated_seqs": 0, "hosted_tokens": 0}
+
     def step(evs=None):
         def m(i):
             if evs is not None:
                 evs[i].record(stream)
         m(0)
         L.luffy_route(lay.layer, x, wg, T, lay.idx, lay.w, s); m(1)
-        L.luffy_condense(lay.layer, x, cfg.h, lay.rep, s); m(2)
+        L.luffy_condense(lay.layer, x, cfg.h, lay.rep, s)
+        if mig:  # K9 -> Alg. 1 on every rank (host) -> destinations; the only host sync of the step
+            rows_at = L.luffy_sequence_rows(lay.layer, seq_len, world, s)
+            dest, _ = L.luffy_plan_migration(seq_len_all, rows_at, args.migrate, cfg.d_model * tdt.itemsize, cfg.d_model)
+            n_out = L.luffy_set_migration(lay.layer, seq_len_all, dest, s)
+            mig_stats["migrated_seqs"] = int(np.sum(dest != np.repeat(np.arange(world), len(seq_len))))
+            mig_stats["hosted_tokens"] = int(n_out)
+        m(2)
         L.luffy_dispatch(lay.layer, x, lay.recv, s); m(3)
         L.luffy_expert_ffn(lay.layer, lay.recv, w1, w2, w3, lay.out, lay.pre, lay.act_buf, s); m(4)
         L.luffy_combine(lay.layer, lay.out, lay.gathered, s); m(5)
-        L.luffy_uncondense(lay.layer, lay.gathered, lay.y, s); m(6)
-        L.luffy_uncondense_bwd(lay.layer, dy, lay.gathered, lay.d_gathered, lay.dw, s); m(7)
+        L.luffy_uncondense(lay.layer, lay.gathered, y_out if mig else lay.y, s); m(6)
+        L.luffy_uncondense_bwd(lay.layer, dy_out if mig else dy, lay.gathered, lay.d_gathered, lay.dw, s); m(7)
         L.luffy_combine_bwd(lay.layer, lay.d_gathered, lay.d_out, s); m(8)
         L.luffy_expert_ffn_bwd(lay.layer, lay.d_out, lay.recv, w1, w2, w3, lay.pre, lay.act_buf, lay.dpre, lay.d_recv,
                                lay.dw1, lay.dw2, lay.dw3, s); m(9)
@@ -279,7 +304,7 @@ def main():
     # ---- e2e: same step through the public API with the inputs copied from pinned host memory and the
     # output read back every step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not mig:
         hx = torch.empty(x.shape, dtype=tdt, pin_memory=True).copy_(x)
         hdy = torch.empty(dy.shape, dtype=tdt, pin_memory=True).copy_(dy)
         hy = torch.empty(x.shape, dtype=tdt, pin_memory=True)
@@ -334,8 +359,15 @@ def main():
     ffn_ms = breakdown["ffn"] + breakdown["ffn_bwd"]
     achieved = flops / (ffn_ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", 1400.0)) if cfg.dtype == "bf16" else 80.0
+    traffic, tsrc = None, None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemm6.json")
+    if args.config == "C2" and world == 1 and os.path.exists(prof):  # measured on this workload (ncu --set full)
+        with open(prof) as fh:
+            kk = [k for k in json.load(fh) if k["kernel"].startswith("gemm_tc_kernel")]
+        traffic = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in kk)
+        tsrc = "profiles/r01_ncu_gemm6.json: DRAM read+write of the 6 GEMM launches of one step"
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "expert FFN grouped GEMMs (fwd 2 + bwd 4 launches)",
+            "traffic": traffic, "traffic_source": tsrc, "kernel": "expert FFN grouped GEMMs (fwd 2 + bwd 4 launches)",
             "peak_source": f"{src} bf16_tflops_sustained" if cfg.dtype == "bf16" else "fp32 SIMT nominal"}
 
     if rank == 0:
@@ -352,6 +384,7 @@ def main():
                           "l2": "per-step working set (~1 GB activations) exceeds the 126 MB L2; no explicit flush"},
                "condensed_frac_rows": frac_all, "a2a_bytes_condensed_frac": frac_remote,
                "greedy_rounds": rounds, "reps_rank0": R,
+               "migration": ({"q": args.migrate, **mig_stats} if mig else None),
                "breakdown_ms": breakdown, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(out), flush=True)

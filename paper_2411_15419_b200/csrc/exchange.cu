@@ -8,16 +8,6 @@
 namespace luffy {
 namespace {
 
-// Push my representative counts into every rank's inbox row `me`, then publish XP_CNT.
-__global__ void xcnt_push_kernel(const int32_t* __restrict__ nrep, int E, int me, int32_t* const* peer_cnt, int P,
-                                 XSignal sig) {
-  for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
-    const int p = i / E, e = i % E;
-    peer_cnt[p][(size_t)me * E + e] = nrep[e];
-  }
-  xsignal_done(sig);
-}
-
 // Wait until every rank published `seq` for this phase (bounded: traps after ~20 s instead of hanging).
 __global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq) {
   const int p = threadIdx.x;
@@ -25,7 +15,7 @@ __global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (ld_acquire_sys(flags + p) < seq) {
-      __nanosleep(128);
+      __nanosleep(32);
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 20000000000ull) __trap();
@@ -34,12 +24,39 @@ __global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t
   __syncthreads();
 }
 
+// Count exchange and layout plan in ONE single-CTA kernel: push my counts to every rank, publish XP_CNT,
+// wait for every rank's counts, then derive the plan (saves two dependent launches per dispatch).
+__device__ void plan_small_body(const int32_t* __restrict__ c, int P, int E, int me, int32_t* __restrict__ cnt_all,
+                                int32_t* __restrict__ roff, int32_t* __restrict__ dst_base, int32_t* __restrict__ src_soff);
+
+__global__ void xcnt_plan_kernel(const int32_t* __restrict__ nrep, int E, int me, int32_t* const* peer_cnt, int P,
+                                 XSignal sig, const uint32_t* __restrict__ flags, const int32_t* __restrict__ inbox,
+                                 int32_t* __restrict__ cnt_all, int32_t* __restrict__ roff, int32_t* __restrict__ dst_base,
+                                 int32_t* __restrict__ src_soff) {
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
+    const int p = i / E, e = i % E;
+    peer_cnt[p][(size_t)me * E + e] = nrep[e];
+  }
+  xsignal_done(sig);  // (single CTA: publishes XP_CNT to every rank)
+  if (threadIdx.x < P) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys(flags + threadIdx.x) < sig.seq) {
+      __nanosleep(64);
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+  plan_small_body(inbox, P, E, me, cnt_all, roff, dst_base, src_soff);
+}
+
 // Layout plan from the all-to-all counts (one CTA): local copy of the counts, my expert layout (roff),
 // and for each expert e the destination row base of my rows in the owner's layout (dst_base[e]).
-__global__ void xplan_small_kernel(const int32_t* __restrict__ inbox, int P, int E, int me, int32_t* __restrict__ cnt_all,
-                                   int32_t* __restrict__ roff, int32_t* __restrict__ dst_base,
-                                   int32_t* __restrict__ src_soff) {
-  const int32_t* c = inbox;  // [P][E], complete (XP_CNT waited)
+__device__ void plan_small_body(const int32_t* __restrict__ c, int P, int E, int me, int32_t* __restrict__ cnt_all,
+                                int32_t* __restrict__ roff, int32_t* __restrict__ dst_base, int32_t* __restrict__ src_soff) {
+  // c = inbox [P][E], complete (XP_CNT waited)
   const int El = E / P;
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) cnt_all[i] = c[i];
   // src_soff[q][e]: padded send offsets of rank q (expert segments rounded up to kRowAlign)
@@ -180,15 +197,13 @@ XSignal make_signal(const luffy_layer* L, int phase) {
   return sg;
 }
 
-// Dispatch at world > 1: counts -> plan -> fused pack/push -> wait for every rank's rows.
+// Dispatch at world > 1: [counts + wait + plan] -> [row plan | fused pack/push] -> wait for every rank's rows.
 int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int par = L->seq & 1;
-  xcnt_push_kernel<<<1, 256, 0, st>>>(L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT));
-  LUFFY_LAUNCHED();
-  LUFFY_CUDA_TRY(launch_xwait(L, XP_CNT, s));
-  xplan_small_kernel<<<1, 256, 0, st>>>(L->x_cnt_inbox, L->P, L->E, L->rank, L->cnt_all, L->roff, L->x_dst_base,
-                                        L->x_src_soff);
+  xcnt_plan_kernel<<<1, 256, 0, st>>>(L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT),
+                                      L->x_flags + XP_CNT * L->P, L->x_cnt_inbox, L->cnt_all, L->roff, L->x_dst_base,
+                                      L->x_src_soff);
   LUFFY_LAUNCHED();
   xplan_rows_kernel<<<148, 256, 0, st>>>(L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),

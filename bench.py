@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--migrate", type=int, default=0,
                     help="world > 1: sequence migration with Alg. 1 candidate-set size q (0 = off)")
+    ap.add_argument("--kprof", type=int, default=0, help="also write a warm per-kernel table over this many steps")
+    ap.add_argument("--kprof-dir", default=os.path.join(ROOT, "gpurun_out"))
     args = ap.parse_args()
     cfg = workload.CONFIGS[args.config]
     if args.h is not None:
@@ -273,7 +275,6 @@ def main():
     if world > 1:
         dist.barrier()
     n_ev = len(marks) + 1
-    evs = [[ev() for _ in range(n_ev)] for _ in range(args.steps)]
     start, stop = ev(), ev()
     launches0 = L.luffy_launch_count()
     torch.cuda.synchronize()
@@ -282,8 +283,9 @@ def main():
     t_host0 = time.time()
     start.record(stream)
     for i in range(args.steps):
-        step(evs[i])
+        step()  # no events inside the timed steps: a stream event between kernels would block their PDL overlap
     stop.record(stream)
+    host_ms = (time.time() - t_host0) * 1e3 / args.steps  # enqueue time per step (no host sync in the step)
     torch.cuda.synchronize()
     clk.window = (t_host0, time.time())
     time.sleep(0.06)
@@ -298,8 +300,43 @@ def main():
         ms = float(t.item())
     ms_step = ms / args.steps
     value = world * T * args.steps / (ms / 1e3)
-    breakdown = {m: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(args.steps))
+    # per-phase breakdown from a separate pass with events between the API calls (diagnostic only)
+    nb_steps = min(args.steps, 50)
+    evs = [[ev() for _ in range(n_ev)] for _ in range(nb_steps)]
+    for i in range(nb_steps):
+        step(evs[i])
+    torch.cuda.synchronize()
+    breakdown = {m: statistics.mean(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(nb_steps))
                  for j, m in enumerate(marks)}
+
+    # ---- optional per-kernel table (CUPTI activity via torch.profiler, warm, every rank; never under ncu)
+    if args.kprof > 0:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(args.kprof):
+                step()
+            torch.cuda.synchronize()
+        agg, spans = {}, []
+        for e in prof.events():
+            if e.device_type.name == "CUDA":
+                nm = e.name.replace("(anonymous namespace)::", "").replace("void ", "").replace("luffy::", "")
+                nm = nm.split("(")[0][:70]
+                a = agg.setdefault(nm, [0, 0.0, 0.0])
+                a[0] += 1
+                a[1] += e.device_time
+                spans.append((e.time_range.start, e.time_range.end, nm))
+        spans.sort()
+        for (_, b0, _), (a1, _, nm) in zip(spans, spans[1:]):
+            agg[nm][2] += max(0.0, a1 - b0)  # idle gap before this kernel
+        busy = sum(b - a for a, b, _ in spans)
+        wall = spans[-1][1] - spans[0][0] if spans else 0
+        path = os.path.join(args.kprof_dir, f"kprof_{cfg.name}_n{world}_r{rank}.txt")
+        os.makedirs(args.kprof_dir, exist_ok=True)
+        with open(path, "w") as fh:
+            fh.write(f"# {cfg.name} world {world} rank {rank}: per-step us (warm, {args.kprof} steps); "
+                     f"kernels busy {busy / args.kprof:.1f} us of {wall / args.kprof:.1f} us wall per step\n")
+            for k, (c, us, gap) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+                fh.write(f"{us / args.kprof:9.1f} us  {c / args.kprof:5.1f}x  gap-before {gap / args.kprof:6.1f} us  {k}\n")
 
     # ---- e2e: same step through the public API with the inputs copied from pinned host memory and the
     # output read back every step
@@ -386,7 +423,7 @@ def main():
                "greedy_rounds": rounds, "reps_rank0": R,
                "migration": ({"q": args.migrate, **mig_stats} if mig else None),
                "breakdown_ms": breakdown, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(launches), "clocks": clocks}
+               "gpu_launches": int(launches), "host_enqueue_ms_per_step": host_ms, "clocks": clocks}
         print(json.dumps(out), flush=True)
     lay.close()
     if world > 1:

@@ -2,6 +2,7 @@
 // the device-initiated expert-parallel exchange over NVLink (CUDA IPC) between the kernels.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +25,13 @@ luffy_status fail(luffy_status st, const std::string& msg) {
   return st;
 }
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("LUFFY_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 
 int gemm_rows_simt(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0,
                    const int32_t* off, int G, int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd,

@@ -22,6 +22,34 @@ namespace luffy {
 
 typedef __nv_bfloat16 bf16;
 
+// Programmatic dependent launch.  Every kernel is launched with programmatic stream serialization and
+// begins with pdl_enter(): wait until the preceding kernel of the stream has completed and flushed
+// (griddepcontrol.wait), then allow the next kernel's CTAs to be scheduled (launch_dependents), so its
+// launch latency overlaps this kernel instead of following it.  Because every kernel waits before its
+// first global access, completion stays transitive along the stream exactly as without PDL.
+// tests/test_abi_cpu.py checks that every __global__ kernel calls it.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // api.cu: LUFFY_PDL=0 in the environment disables the attribute (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);  // errors surface via LUFFY_LAUNCHED
+}
+
 // 8 consecutive elements <-> 8 floats (one 16-byte load for bf16, two for fp32)
 __device__ __forceinline__ void load8(const bf16* p, float (&v)[8]) {
   uint4 u = *reinterpret_cast<const uint4*>(p);

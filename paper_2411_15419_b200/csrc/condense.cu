@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __rest
                                                            int T, int k, int E, int32_t* __restrict__ gcnt,
                                                            int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
                                                            float* __restrict__ gw, int32_t* __restrict__ gloc) {
+  pdl_enter();
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
   __shared__ int warp_sums[33];
@@ -97,6 +98,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) gather_norm_kernel(const T* __restrict__ x, const int32_t* __restrict__ gtok,
                                                           const int32_t* __restrict__ goff, int E, int d,
                                                           T* __restrict__ xg, double* __restrict__ gnorm) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t rows = goff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
                                                         const int32_t* __restrict__ goff, const int32_t* __restrict__ gcnt,
                                                         const int64_t* __restrict__ adjoff, int E, int d, double c2h,
                                                         uint32_t* __restrict__ adj) {
+  pdl_enter();
   constexpr int TS = 64, BK = 32;
   __shared__ float As[BK][TS + 4];
   __shared__ float Bs[BK][TS + 4];
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
 
 // Word offsets of each group's adjacency: sum over groups of npad^2 / 32.
 __global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff) {
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     int64_t o = 0;
     for (int e = 0; e < E; ++e) {
@@ -295,6 +299,7 @@ struct GreedyArgs {
 };
 
 __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
+  pdl_enter();
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int64_t adjoff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
@@ -448,6 +453,7 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
 // h > 1: no edges -- every copy represents itself.
 __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int32_t* __restrict__ gtok, int E,
                                     int32_t* __restrict__ rep_local, uint32_t* __restrict__ ctrl) {
+  pdl_enter();
   const int rows = goff[E];
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
     rep_local[r] = gtok[r] >= 0 ? (int32_t)r : -1;
@@ -458,15 +464,15 @@ __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int3
 
 int launch_group_build(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  group_build_kernel<<<L->E, 1024, 0, st>>>(L->idx, L->w, L->T, L->k, L->E, L->gcnt, L->goff, L->gtok,
+  launch_pdl(group_build_kernel, L->E, 1024, 0, st, L->idx, L->w, L->T, L->k, L->E, L->gcnt, L->goff, L->gtok,
                                             L->gw, L->gloc);
   LUFFY_LAUNCHED();
   int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);
   if (L->dtype == LUFFY_BF16)
-    gather_norm_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->gtok, L->goff, L->E, L->d,
+    launch_pdl(gather_norm_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->gtok, L->goff, L->E, L->d,
                                                      static_cast<bf16*>(L->xg), L->gnorm);
   else
-    gather_norm_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->gtok, L->goff, L->E, L->d,
+    launch_pdl(gather_norm_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->gtok, L->goff, L->E, L->d,
                                                       static_cast<float*>(L->xg), L->gnorm);
   LUFFY_LAUNCHED();
   return 0;
@@ -474,23 +480,23 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
 
 int launch_identity_rep(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  identity_rep_kernel<<<148, 256, 0, st>>>(L->goff, L->gtok, L->E, L->rep_local, L->ctrl);
+  launch_pdl(identity_rep_kernel, 148, 256, 0, st, L->goff, L->gtok, L->E, L->rep_local, L->ctrl);
   LUFFY_LAUNCHED();
   return 0;
 }
 
 int launch_gram_simt(luffy_layer* L, float h, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  adj_offsets_kernel<<<1, 32, 0, st>>>(L->goff, L->E, L->adjoff);
+  launch_pdl(adj_offsets_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff);
   LUFFY_LAUNCHED();
   const int64_t nt = L->Cpad_max / 64;
   const int64_t tiles = nt * (nt + 1) / 2;  // upper bound over any split of the rows into groups
   const double c2h = 2.0 * (double)h - 1.0;
   if (L->dtype == LUFFY_BF16)
-    gram_simt_kernel<bf16><<<(unsigned)tiles, 256, 0, st>>>(static_cast<const bf16*>(L->xg), L->gnorm, L->goff, L->gcnt,
+    launch_pdl(gram_simt_kernel<bf16>, (unsigned)tiles, 256, 0, st, static_cast<const bf16*>(L->xg), L->gnorm, L->goff, L->gcnt,
                                                             L->adjoff, L->E, L->d, c2h, L->adj);
   else
-    gram_simt_kernel<float><<<(unsigned)tiles, 256, 0, st>>>(static_cast<const float*>(L->xg), L->gnorm, L->goff, L->gcnt,
+    launch_pdl(gram_simt_kernel<float>, (unsigned)tiles, 256, 0, st, static_cast<const float*>(L->xg), L->gnorm, L->goff, L->gcnt,
                                                              L->adjoff, L->E, L->d, c2h, L->adj);
   LUFFY_LAUNCHED();
   return 0;

@@ -10,6 +10,7 @@ namespace {
 
 // Wait until every rank published `seq` for this phase (bounded: traps after ~20 s instead of hanging).
 __global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq) {
+  pdl_enter();
   const int p = threadIdx.x;
   if (p < P) {
     uint64_t t0;
@@ -33,6 +34,7 @@ __global__ void xcnt_plan_kernel(const int32_t* __restrict__ nrep, int E, int me
                                  XSignal sig, const uint32_t* __restrict__ flags, const int32_t* __restrict__ inbox,
                                  int32_t* __restrict__ cnt_all, int32_t* __restrict__ roff, int32_t* __restrict__ dst_base,
                                  int32_t* __restrict__ src_soff) {
+  pdl_enter();
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
     const int p = i / E, e = i % E;
     peer_cnt[p][(size_t)me * E + e] = nrep[e];
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
                                                          int32_t* __restrict__ slot_of, bf16* __restrict__ recv,
                                                          bf16* __restrict__ dexp, int elem_bytes,
                                                          unsigned long long* __restrict__ rowmask) {
+  pdl_enter();
   const int El = E / P;
   const int64_t rows = roff[El];
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(256) xpack_push_kernel(const T* __restrict__ x
                                                          int E, int El, int d, void* const* peer_recv, XSignal sig,
                                                          const unsigned long long* __restrict__ dmask,
                                                          unsigned long long* const* peer_rowmask, int me) {
+  pdl_enter();
   __shared__ int32_t soff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
   for (int i = threadIdx.x; i <= E; i += blockDim.x) {
@@ -183,7 +187,7 @@ inline int grid_warps(int64_t warps) {
 
 int launch_xwait(const luffy_layer* L, int phase, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  xwait_kernel<<<1, 64, 0, st>>>(L->x_flags + phase * L->P, L->P, L->seq);
+  launch_pdl(xwait_kernel, 1, 64, 0, st, L->x_flags + phase * L->P, L->P, L->seq);
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -201,21 +205,21 @@ XSignal make_signal(const luffy_layer* L, int phase) {
 int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int par = L->seq & 1;
-  xcnt_plan_kernel<<<1, 256, 0, st>>>(L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT),
+  launch_pdl(xcnt_plan_kernel, 1, 256, 0, st, L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT),
                                       L->x_flags + XP_CNT * L->P, L->x_cnt_inbox, L->cnt_all, L->roff, L->x_dst_base,
                                       L->x_src_soff);
   LUFFY_LAUNCHED();
-  xplan_rows_kernel<<<148, 256, 0, st>>>(L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
+  launch_pdl(xplan_rows_kernel, 148, 256, 0, st, L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),
                                          static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4, L->x_rowmask);
   LUFFY_LAUNCHED();
   const int blocks = grid_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16)
-    xpack_push_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->perm, L->soff, L->x_dst_base, L->E,
+    launch_pdl(xpack_push_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->perm, L->soff, L->x_dst_base, L->E,
                                                     L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP),
                                                     L->mig ? L->dmask : nullptr, L->x_peer_rowmask, L->rank);
   else
-    xpack_push_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->perm, L->soff, L->x_dst_base, L->E,
+    launch_pdl(xpack_push_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->perm, L->soff, L->x_dst_base, L->E,
                                                      L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP),
                                                      L->mig ? L->dmask : nullptr, L->x_peer_rowmask, L->rank);
   LUFFY_LAUNCHED();

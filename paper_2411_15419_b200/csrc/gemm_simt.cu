@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) gemm_rows_kernel(const T* __restrict__ A,
                                                         const T* __restrict__ B3, T* __restrict__ D, T* __restrict__ aux0,
                                                         const int32_t* __restrict__ off, int G, int N, int K, int bkm,
                                                         XRedirect rd, int has_rd, XSignal sig, int has_sig) {
+  pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int64_t row0 = (int64_t)blockIdx.y * BM;
@@ -139,6 +140,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) gemm_wgrad_kernel(const T* __restrict__ A, const T* __restrict__ B,
                                                          float* __restrict__ D, float* __restrict__ D3, int Msplit,
                                                          const int32_t* __restrict__ off, int M, int N, int lda, int ldb) {
+  pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int g = blockIdx.z;
@@ -191,11 +193,11 @@ int gemm_rows_t(int epi, const void* A, const void* B, const void* B3, void* D, 
   T* d = static_cast<T*>(D);
   T* x = static_cast<T*>(aux0);
   switch (epi) {
-    case EPI_STORE: gemm_rows_kernel<T, EPI_STORE><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
-    case EPI_GELU: gemm_rows_kernel<T, EPI_GELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
-    case EPI_SWIGLU: gemm_rows_kernel<T, EPI_SWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
-    case EPI_DGELU: gemm_rows_kernel<T, EPI_DGELU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
-    default: gemm_rows_kernel<T, EPI_DSWIGLU><<<grid, 256, 0, s>>>(a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_STORE: launch_pdl(gemm_rows_kernel<T, EPI_STORE>, grid, 256, 0, s, a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_GELU: launch_pdl(gemm_rows_kernel<T, EPI_GELU>, grid, 256, 0, s, a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_SWIGLU: launch_pdl(gemm_rows_kernel<T, EPI_SWIGLU>, grid, 256, 0, s, a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    case EPI_DGELU: launch_pdl(gemm_rows_kernel<T, EPI_DGELU>, grid, 256, 0, s, a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
+    default: launch_pdl(gemm_rows_kernel<T, EPI_DSWIGLU>, grid, 256, 0, s, a, b, b3, d, x, off, G, N, K, bkm, rd, has_rd, sg, has_sig); break;
   }
   LUFFY_LAUNCHED();
   return 0;
@@ -216,10 +218,10 @@ int gemm_wgrad_simt(int dtype, const void* A, const void* B, float* D, float* D3
   cudaStream_t st = static_cast<cudaStream_t>(s);
   dim3 grid(N / BN, M / BM, G);
   if (dtype == LUFFY_BF16)
-    gemm_wgrad_kernel<bf16><<<grid, 256, 0, st>>>(static_cast<const bf16*>(A), static_cast<const bf16*>(B), D, D3, Msplit,
+    launch_pdl(gemm_wgrad_kernel<bf16>, grid, 256, 0, st, static_cast<const bf16*>(A), static_cast<const bf16*>(B), D, D3, Msplit,
                                                   off, M, N, lda, ldb);
   else
-    gemm_wgrad_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(A), static_cast<const float*>(B), D, D3,
+    launch_pdl(gemm_wgrad_kernel<float>, grid, 256, 0, st, static_cast<const float*>(A), static_cast<const float*>(B), D, D3,
                                                    Msplit, off, M, N, lda, ldb);
   LUFFY_LAUNCHED();
   return 0;

@@ -197,6 +197,7 @@ template <int EPI, bool A_MN, bool B_MN, bool WG>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                    const __grid_constant__ CUtensorMap tB3, const TcArgs a) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   __shared__ int32_t off_s[LUFFY_MAX_EXPERTS + 1];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -478,7 +479,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3,
     LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
-  kern<<<num_sms(), THREADS, SMEM_BYTES, s>>>(ta, tb, tb3, a);
+  launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, a);
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -48,6 +48,7 @@ __device__ __forceinline__ bool decode_tile(int t, const int32_t* goff_s, int E,
 }
 
 __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_constant__ CUtensorMap tX, const GramArgs a) {
+  pdl_enter();
   extern __shared__ uint8_t smem_raw[];
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
 }
 
 __global__ void adj_offsets_tc_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff) {
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     int64_t o = 0;
     for (int e = 0; e < E; ++e) {
@@ -216,7 +218,7 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
 
 int launch_gram_tc(luffy_layer* L, float h, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  adj_offsets_tc_kernel<<<1, 32, 0, st>>>(L->goff, L->E, L->adjoff);
+  launch_pdl(adj_offsets_tc_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff);
   LUFFY_LAUNCHED();
   CUtensorMap tx;
   LUFFY_CUDA_TRY(make_tmap_bf16(&tx, L->xg, L->d, L->Cpad_max, L->d, TS));
@@ -237,7 +239,7 @@ int launch_gram_tc(luffy_layer* L, float h, void* s) {
   int dev = 0, sms = 0;
   LUFFY_CUDA_TRY(cudaGetDevice(&dev));
   LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  gram_tc_kernel<<<sms, THREADS, SMEM_BYTES, st>>>(tx, a);
+  launch_pdl(gram_tc_kernel, sms, THREADS, SMEM_BYTES, st, tx, a);
   LUFFY_LAUNCHED();
   return 0;
 }

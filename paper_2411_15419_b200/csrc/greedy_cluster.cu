@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       int32_t* __restrict__ rep_local,
                                                                       uint32_t* __restrict__ ctrl, int nmax,
                                                                       int max_rounds, int cache_words) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t gsm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -82,34 +83,49 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     uint32_t left = 0;
     for (int j = 0; j < CS; ++j) left += *cluster.map_shared_rank(cnt + (round & 1), j);
     if (left == 0u) break;
-    // ---- B / C: closed-neighbourhood maxima over alive nodes (local replicas)
-    for (int ph = 0; ph < 2; ++ph) {
-      const unsigned long long* src = ph == 0 ? key : m1;
-      for (int r = r0 + wid; r < r1; r += nwarp) {
-        if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-        const uint32_t* row = ROW(r);
-        unsigned long long m = src[r];
-        for (int w = lane; w < W; w += 32) {
-          const uint32_t bits = row[w] & alive[w];
-          if (bits) {
-#pragma unroll
-            for (int b = 0; b < 32; ++b) {
-              if ((bits >> b) & 1u) {
-                const unsigned long long v = src[w * 32 + b];
-                m = v > m ? v : m;
-              }
-            }
-          }
-        }
-        m = warp_max_u64(m);
-        if (ph == 0) {
-          if (lane < CS) *cluster.map_shared_rank(m1 + r, lane) = m;
-        } else if (m == key[r]) {
-          if (lane < CS) atomicOr(cluster.map_shared_rank(win + (r >> 5), lane), 1u << (r & 31));
+    // ---- B: m1 = max key over the alive closed neighbourhood (local replicas; set bits only)
+    for (int r = r0 + wid; r < r1; r += nwarp) {
+      if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
+      const uint32_t* row = ROW(r);
+      unsigned long long m = key[r];
+      for (int w = lane; w < W; w += 32) {
+        uint32_t bits = row[w] & alive[w];
+        while (bits) {
+          const unsigned long long v = key[w * 32 + __ffs(bits) - 1];
+          bits &= bits - 1u;
+          m = v > m ? v : m;
         }
       }
-      cluster.sync();
+      m = warp_max_u64(m);
+      if (lane < CS) *cluster.map_shared_rank(m1 + r, lane) = m;
     }
+    cluster.sync();
+    // ---- C: winner iff max m1 over the alive closed neighbourhood equals key[r].  Every alive neighbour j
+    // has m1[j] >= key[r] (r is in j's neighbourhood), so r wins iff m1[r] == key[r] and no alive neighbour
+    // has m1[j] != key[r]: most rows lose without a scan and a scan stops at the first violation.
+    for (int r = r0 + wid; r < r1; r += nwarp) {
+      if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
+      const unsigned long long kr = key[r];
+      if (m1[r] != kr) continue;
+      const uint32_t* row = ROW(r);
+      bool lose = false;
+      for (int wb = 0; wb < W; wb += 32) {
+        const int w = wb + lane;
+        if (w < W) {
+          uint32_t bits = row[w] & alive[w];
+          while (bits && !lose) {
+            lose = m1[w * 32 + __ffs(bits) - 1] != kr;
+            bits &= bits - 1u;
+          }
+        }
+        if (__any_sync(0xffffffffu, lose)) {
+          lose = true;
+          break;
+        }
+      }
+      if (!lose && lane < CS) atomicOr(cluster.map_shared_rank(win + (r >> 5), lane), 1u << (r & 31));
+    }
+    cluster.sync();
     // ---- D: claims (a non-winner has at most one winner neighbour: winners are >= 3 hops apart)
     if (threadIdx.x == 0) cnt[(round + 1) & 1] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
@@ -148,13 +164,15 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, cudaS
   cfg.blockDim = dim3(GC_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
                                     kGreedyMaxRounds, cache_words));

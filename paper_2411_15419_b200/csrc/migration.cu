@@ -29,12 +29,14 @@ __device__ __forceinline__ int seq_of(const int32_t* seq_start, int S, int t) {
 }
 
 __global__ void zero_u32_kernel(uint32_t* __restrict__ p, int64_t n) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0u;
 }
 
 // distinct slots per sequence: bit (s, pos[t, j]) for every copy of every token t of sequence s
 __global__ void seq_bits_kernel(const int32_t* __restrict__ pos, const int32_t* __restrict__ seq_start, int S, int T, int k,
                                 int words, uint32_t* __restrict__ bits) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)T * k; i += (int64_t)gridDim.x * blockDim.x) {
     const int t = (int)(i / k);
     const int s = seq_of(seq_start, S, t);
@@ -46,6 +48,7 @@ __global__ void seq_bits_kernel(const int32_t* __restrict__ pos, const int32_t* 
 // rows_at[s][j] = popcount of the bits of sequence s inside rank j's slot range; pushed to every rank.
 __global__ void seq_rows_push_kernel(const uint32_t* __restrict__ bits, const int32_t* __restrict__ soff, int S, int P,
                                      int El, int words, int me, int Smax, int32_t* const* peer_mig, XSignal sig) {
+  pdl_enter();
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < S * P; i += gridDim.x * (blockDim.x >> 5)) {
     const int s = i / P, j = i % P;
     const int w0 = soff[j * El] >> 5, w1 = soff[(j + 1) * El] >> 5;
@@ -59,12 +62,14 @@ __global__ void seq_rows_push_kernel(const uint32_t* __restrict__ bits, const in
 }
 
 __global__ void zero_u64_kernel(unsigned long long* __restrict__ p, int64_t n) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = 0ull;
 }
 
 __global__ void slot_dmask_kernel(const int32_t* __restrict__ pos, const int32_t* __restrict__ seq_start,
                                   const int32_t* __restrict__ seq_dest, int S, int T, int k,
                                   unsigned long long* __restrict__ dmask) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)T * k; i += (int64_t)gridDim.x * blockDim.x) {
     const int s = seq_of(seq_start, S, (int)(i / k));
     atomicOr(dmask + pos[i], 1ull << seq_dest[s]);
@@ -76,6 +81,7 @@ __global__ void mig_meta_push_kernel(const int32_t* __restrict__ pos, const floa
                                      const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_dest,
                                      const int32_t* __restrict__ out_start, int S, int T, int k, int me,
                                      int32_t* const* peer_meta, float* const* peer_meta_w, XSignal sig) {
+  pdl_enter();
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     const int s = seq_of(seq_start, S, t);
     const int g = seq_dest[s];
@@ -97,6 +103,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) uncondense_mig_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ meta,
                                                              const float* __restrict__ meta_w, int64_t n_out, int k, int d,
                                                              int64_t Rpad, T* __restrict__ y) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_out; i += nw) {
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(256) mig_bwd_push_kernel(const T* __restrict__
                                                            const int32_t* __restrict__ meta, int64_t n_out, int k, int d,
                                                            int64_t Rpad, void* const* peer_dy_in, float* const* peer_dw_in,
                                                            XSignal sig) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_out; i += nw) {
@@ -161,12 +169,12 @@ inline int blocks_for(int64_t n, int per) { return (int)std::max<int64_t>(1, std
 int launch_seq_rows(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int words = (int)(L->Rpad_max / 32);
-  zero_u32_kernel<<<blocks_for((int64_t)L->S * words, 256), 256, 0, st>>>(L->seq_bits, (int64_t)L->S * words);
+  launch_pdl(zero_u32_kernel, blocks_for((int64_t)L->S * words, 256), 256, 0, st, L->seq_bits, (int64_t)L->S * words);
   LUFFY_LAUNCHED();
-  seq_bits_kernel<<<blocks_for((int64_t)L->T * L->k, 256), 256, 0, st>>>(L->pos, L->seq_start, L->S, L->T, L->k, words,
+  launch_pdl(seq_bits_kernel, blocks_for((int64_t)L->T * L->k, 256), 256, 0, st, L->pos, L->seq_start, L->S, L->T, L->k, words,
                                                                          L->seq_bits);
   LUFFY_LAUNCHED();
-  seq_rows_push_kernel<<<blocks_for((int64_t)L->S * L->P, 8), 256, 0, st>>>(L->seq_bits, L->soff, L->S, L->P, L->El, words,
+  launch_pdl(seq_rows_push_kernel, blocks_for((int64_t)L->S * L->P, 8), 256, 0, st, L->seq_bits, L->soff, L->S, L->P, L->El, words,
                                                                              L->rank, L->Smax, L->x_peer_mig,
                                                                              make_signal(L, XP_MIG));
   LUFFY_LAUNCHED();
@@ -175,9 +183,9 @@ int launch_seq_rows(luffy_layer* L, void* s) {
 
 int launch_set_migration(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  zero_u64_kernel<<<blocks_for(L->Rpad_max, 256), 256, 0, st>>>(L->dmask, L->Rpad_max);
+  launch_pdl(zero_u64_kernel, blocks_for(L->Rpad_max, 256), 256, 0, st, L->dmask, L->Rpad_max);
   LUFFY_LAUNCHED();
-  slot_dmask_kernel<<<blocks_for((int64_t)L->T * L->k, 256), 256, 0, st>>>(L->pos, L->seq_start, L->seq_dest_l, L->S, L->T,
+  launch_pdl(slot_dmask_kernel, blocks_for((int64_t)L->T * L->k, 256), 256, 0, st, L->pos, L->seq_start, L->seq_dest_l, L->S, L->T,
                                                                            L->k, L->dmask);
   LUFFY_LAUNCHED();
   return 0;
@@ -185,7 +193,7 @@ int launch_set_migration(luffy_layer* L, void* s) {
 
 int launch_mig_meta_push(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  mig_meta_push_kernel<<<blocks_for(L->T, 256), 256, 0, st>>>(L->pos, L->w, L->seq_start, L->seq_dest_l, L->out_start, L->S,
+  launch_pdl(mig_meta_push_kernel, blocks_for(L->T, 256), 256, 0, st, L->pos, L->w, L->seq_start, L->seq_dest_l, L->out_start, L->S,
                                                               L->T, L->k, L->rank, L->x_peer_meta, L->x_peer_meta_w,
                                                               make_signal(L, XP_META));
   LUFFY_LAUNCHED();
@@ -196,10 +204,10 @@ int launch_uncondense_mig(const luffy_layer* L, void* y, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int b = blocks_for(L->n_out, 8);
   if (L->dtype == LUFFY_BF16)
-    uncondense_mig_kernel<bf16><<<b, 256, 0, st>>>(static_cast<const bf16*>(L->x_gathered), L->x_meta, L->x_meta_w,
+    launch_pdl(uncondense_mig_kernel<bf16>, b, 256, 0, st, static_cast<const bf16*>(L->x_gathered), L->x_meta, L->x_meta_w,
                                                    L->n_out, L->k, L->d, L->Rpad_max, static_cast<bf16*>(y));
   else
-    uncondense_mig_kernel<float><<<b, 256, 0, st>>>(static_cast<const float*>(L->x_gathered), L->x_meta, L->x_meta_w,
+    launch_pdl(uncondense_mig_kernel<float>, b, 256, 0, st, static_cast<const float*>(L->x_gathered), L->x_meta, L->x_meta_w,
                                                     L->n_out, L->k, L->d, L->Rpad_max, static_cast<float*>(y));
   LUFFY_LAUNCHED();
   return 0;
@@ -209,11 +217,11 @@ int launch_mig_bwd_push(const luffy_layer* L, const void* dy, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int b = blocks_for(L->n_out, 8);
   if (L->dtype == LUFFY_BF16)
-    mig_bwd_push_kernel<bf16><<<b, 256, 0, st>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(L->x_gathered),
+    launch_pdl(mig_bwd_push_kernel<bf16>, b, 256, 0, st, static_cast<const bf16*>(dy), static_cast<const bf16*>(L->x_gathered),
                                                  L->x_meta, L->n_out, L->k, L->d, L->Rpad_max, L->x_peer_dy_in,
                                                  L->x_peer_dw_in, make_signal(L, XP_MIGB));
   else
-    mig_bwd_push_kernel<float><<<b, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(L->x_gathered),
+    launch_pdl(mig_bwd_push_kernel<float>, b, 256, 0, st, static_cast<const float*>(dy), static_cast<const float*>(L->x_gathered),
                                                   L->x_meta, L->n_out, L->k, L->d, L->Rpad_max, L->x_peer_dy_in,
                                                   L->x_peer_dw_in, make_signal(L, XP_MIGB));
   LUFFY_LAUNCHED();

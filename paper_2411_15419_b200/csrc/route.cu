@@ -15,6 +15,7 @@ __global__ void __launch_bounds__(256) route_kernel(const T* __restrict__ x, con
                                                     float* __restrict__ probs, int32_t* __restrict__ idx,
                                                     float* __restrict__ w, int32_t* __restrict__ idx_out,
                                                     float* __restrict__ w_out) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -114,6 +115,187 @@ __global__ void __launch_bounds__(256) route_kernel(const T* __restrict__ x, con
   }
 }
 
+// Row fragments of 4 consecutive elements: raw load (8 bytes for bf16, 16 for fp32), conversion, store.
+__device__ __forceinline__ uint2 ld4raw(const bf16* p) { return *reinterpret_cast<const uint2*>(p); }
+__device__ __forceinline__ float4 ld4raw(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void cvt4(uint2 u, float (&f)[4]) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+__device__ __forceinline__ void cvt4(float4 u, float (&f)[4]) { f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w; }
+__device__ __forceinline__ void st4(bf16* p, const float (&f)[4]) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]);
+  const __nv_bfloat162 b = __floats2bfloat162_rn(f[2], f[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<const uint32_t*>(&a);
+  u.y = *reinterpret_cast<const uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+__device__ __forceinline__ void st4(float* p, const float (&f)[4]) { *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]); }
+
+// Gate for E <= 8, d % 256 == 0 (the GPT-MoE shapes): a CTA of 8 warps, 4 tokens per warp.  The row loads
+// of up to 1024 columns of the warp's 4 tokens are issued first, W_g (<= 2048 columns per chunk, 64 KiB) is
+// staged in shared memory meanwhile, and each float4 weight read feeds the 4 tokens.  The 32 partial sums
+// (4 tokens x 8 experts) of every lane are then TRANSPOSE-reduced in 31 shuffles so that lane l holds the
+// logit of (token l / 8, expert l % 8), and softmax / top-k / gate weights run lane-parallel in 8-lane
+// groups.  Summation order is fixed (column order within a lane, then the halving tree): reproducible.
+template <typename T>
+__global__ void __launch_bounds__(256, 2) route_e8_kernel(const T* __restrict__ x, const float* __restrict__ wg, int T_,
+                                                          int E, int d, int k, int renorm, float* __restrict__ probs,
+                                                          int32_t* __restrict__ idx, float* __restrict__ w,
+                                                          int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
+  pdl_enter();
+  constexpr int TB = 4, EB = 8, RC = 2048;
+  constexpr int SUB = sizeof(T) == 2 ? 4 : 2;  // 256-column sub-chunks per load batch
+  using R = decltype(ld4raw(static_cast<const T*>(nullptr)));
+  extern __shared__ __align__(16) float wsm[];  // [EB][RC]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t0 = (blockIdx.x * 8 + wid) * TB;
+  float v[TB * EB];
+#pragma unroll
+  for (int i = 0; i < TB * EB; ++i) v[i] = 0.f;
+  for (int c0 = 0; c0 < d; c0 += RC) {
+    const int rc = min(RC, d - c0);
+    for (int s0 = 0; s0 < rc; s0 += 256 * SUB) {
+      R raw[TB][SUB][2];
+#pragma unroll
+      for (int i = 0; i < TB; ++i)
+#pragma unroll
+        for (int u = 0; u < SUB; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = s0 + u * 256 + h * 128 + lane * 4;
+            raw[i][u][h] = (t0 + i < T_ && c < rc) ? ld4raw(x + (size_t)(t0 + i) * d + c0 + c) : R{};
+          }
+      if (s0 == 0) {  // stage this chunk of W_g while the first row loads are in flight
+        __syncthreads();
+        for (int i = threadIdx.x; i < E * (rc / 4); i += blockDim.x) {
+          const int e = i / (rc / 4), c = (i % (rc / 4)) * 4;
+          *reinterpret_cast<float4*>(&wsm[e * RC + c]) = *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < SUB; ++u) {
+        if (s0 + u * 256 >= rc) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = s0 + u * 256 + h * 128 + lane * 4;
+          float xv[TB][4];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) cvt4(raw[i][u][h], xv[i]);
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            if (e < E) {
+              const float4 wv = *reinterpret_cast<const float4*>(&wsm[e * RC + c]);
+#pragma unroll
+              for (int i = 0; i < TB; ++i) {
+                float s = v[i * EB + e];
+                s = fmaf(xv[i][0], wv.x, s);
+                s = fmaf(xv[i][1], wv.y, s);
+                s = fmaf(xv[i][2], wv.z, s);
+                s = fmaf(xv[i][3], wv.w, s);
+                v[i * EB + e] = s;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  // transpose-reduce: after the step with offset o, a lane keeps the half of its values selected by (lane & o)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const bool hi = lane & 16;
+    const float send = hi ? v[j] : v[j + 16];
+    const float keep = hi ? v[j + 16] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool hi = lane & 8;
+    const float send = hi ? v[j] : v[j + 8];
+    const float keep = hi ? v[j + 8] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool hi = lane & 4;
+    const float send = hi ? v[j] : v[j + 4];
+    const float keep = hi ? v[j + 4] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool hi = lane & 2;
+    const float send = hi ? v[j] : v[j + 2];
+    const float keep = hi ? v[j + 2] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  {
+    const bool hi = lane & 1;
+    const float send = hi ? v[0] : v[1];
+    const float keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  // lane l: token t0 + l / 8, expert e = l % 8 (8-lane groups, xor offsets < 8 stay inside a group)
+  const int e = lane & 7;
+  const int t = t0 + (lane >> 3);
+  const float logit = e < E ? v[0] : -INFINITY;
+  float mx = logit;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float ex = e < E ? expf(logit - mx) : 0.f;
+  float se = ex;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (t < T_ && e < E) probs[(size_t)t * E + e] = expf(logit - mx) / se;
+  // top-k by (logit desc, expert id asc)
+  bool taken = e >= E;
+  float selv[8];
+  int seli[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= k) break;
+    float bv = taken ? -INFINITY : logit;
+    int bi = taken ? 0x7fffffff : e;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    taken = taken || bi == e;
+    selv[j] = bv;
+    seli[j] = bi;
+  }
+  float ev[8], sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < k) {
+      ev[j] = renorm ? expf(selv[j] - selv[0]) : expf(selv[j] - mx) / se;
+      sum += ev[j];
+    }
+  float myw = 0.f;
+  int myi = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < k && j == e) {
+      myw = renorm ? ev[j] / sum : ev[j];
+      myi = seli[j];
+    }
+  if (t < T_ && e < k) {
+    w[(size_t)t * k + e] = myw;
+    w_out[(size_t)t * k + e] = myw;
+    idx[(size_t)t * k + e] = myi;
+    idx_out[(size_t)t * k + e] = myi;
+  }
+}
+
 // Fast gate for E <= 32: a CTA of 8 warps owns 32 tokens (4 per warp); W_g is staged through shared
 // memory in chunks of RC columns and every weight read from shared memory feeds 4 tokens.  Lane l owns
 // columns {4l..4l+3} and {128+4l..128+4l+3} of each 256-wide sub-chunk (conflict-free float4 reads).
@@ -123,6 +305,7 @@ __global__ void __launch_bounds__(256) route_fast_kernel(const T* __restrict__ x
                                                          int E, int d, int k, int renorm, float* __restrict__ probs,
                                                          int32_t* __restrict__ idx, float* __restrict__ w,
                                                          int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
+  pdl_enter();
   constexpr int TB = 4, RC = 8192 / EB;  // 32 KiB of staged weights per chunk
   __shared__ __align__(16) float ws[EB][RC];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -244,6 +427,7 @@ __global__ void __launch_bounds__(256) route_bwd_kernel(const float* __restrict_
                                                         const int32_t* __restrict__ idx, const float* __restrict__ w,
                                                         const float* __restrict__ dw, int T_, int E, int d, int k,
                                                         int renorm, float* __restrict__ dl, T* __restrict__ dx) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -291,6 +475,7 @@ __global__ void __launch_bounds__(256) route_bwd_fast_kernel(const float* __rest
                                                              const int32_t* __restrict__ idx, const float* __restrict__ w,
                                                              const float* __restrict__ dw, int T_, int E, int d, int k,
                                                              int renorm, float* __restrict__ dl, T* __restrict__ dx) {
+  pdl_enter();
   constexpr int TB = 4, RC = 8192 / EB;
   __shared__ __align__(16) float ws[EB][RC];
   __shared__ float dls[32][EB];
@@ -386,6 +571,7 @@ __global__ void __launch_bounds__(256) route_bwd_fast_kernel(const float* __rest
 template <typename T, int EB>
 __global__ void __launch_bounds__(256) wg_partial_fast_kernel(const float* __restrict__ dl, const T* __restrict__ x,
                                                               int T_, int E, int d, float* __restrict__ part) {
+  pdl_enter();
   constexpr int TT = 64;
   __shared__ float dls[TT][EB];
   const int col = blockIdx.x * 256 + threadIdx.x;
@@ -415,6 +601,7 @@ __global__ void __launch_bounds__(256) wg_partial_fast_kernel(const float* __res
 template <typename T, int EB>
 __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict__ dl, const T* __restrict__ x,
                                                          int T_, int E, int d, int chunk, float* __restrict__ part) {
+  pdl_enter();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int p = blockIdx.y;
   const int e0 = blockIdx.z * EB;
@@ -435,12 +622,27 @@ __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict
     if (e0 + e < E) part[((size_t)p * E + e0 + e) * d + col] = acc[e];
 }
 
-__global__ void wg_reduce_kernel(const float* __restrict__ part, int parts, int n, float* __restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// dW_g = sum of the partials in a fixed order: CTA = 32 outputs x 8 warps; warp w sums parts w, w+8, ...
+// (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) wg_reduce_kernel(const float* __restrict__ part, int parts, int n,
+                                                        float* __restrict__ out) {
+  pdl_enter();
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int p = 0; p < parts; ++p) s += part[(size_t)p * n + i];
-  out[i] = s;
+  if (i < n) {
+#pragma unroll 4
+    for (int p = wid; p < parts; p += 8) s += part[(size_t)p * n + i];
+  }
+  red[wid][lane] = s;
+  __syncthreads();
+  if (wid == 0 && i < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    out[i] = t;
+  }
 }
 
 template <typename T>
@@ -451,20 +653,25 @@ int route_dispatch(const luffy_layer* L, const void* x, const float* wg, int32_t
   const T* xp = static_cast<const T*>(x);
   if (L->E <= 32 && L->d % 256 == 0) {
     const int fb = (L->T + 31) / 32;
-    if (L->E <= 8)
-      route_fast_kernel<T, 8><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
-                                                  idx_out, w_out);
-    else if (L->E <= 16)
-      route_fast_kernel<T, 16><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+    if (L->E <= 8) {
+      static bool attr = false;
+      if (!attr) {
+        LUFFY_CUDA_TRY(cudaFuncSetAttribute(route_e8_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        attr = true;
+      }
+      launch_pdl(route_e8_kernel<T>, fb, 256, 65536, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+                 idx_out, w_out);
+    } else if (L->E <= 16)
+      launch_pdl(route_fast_kernel<T, 16>, fb, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
                                                    idx_out, w_out);
     else
-      route_fast_kernel<T, 32><<<fb, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
+      launch_pdl(route_fast_kernel<T, 32>, fb, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
                                                    idx_out, w_out);
     LUFFY_LAUNCHED();
     return 0;
   }
 #define LUFFY_ROUTE(EBV)                                                                                 \
-  route_kernel<T, EBV><<<blocks, 256, 0, s>>>(xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, \
+  launch_pdl(route_kernel<T, EBV>, blocks, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, \
                                               L->w, idx_out, w_out)
   if (L->E <= 32) LUFFY_ROUTE(32);
   else if (L->E <= 64) LUFFY_ROUTE(64);
@@ -493,16 +700,16 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
 #define LUFFY_RB(EBV)                                                                                               \
   do {                                                                                                              \
     if (L->dtype == LUFFY_BF16) {                                                                                   \
-      route_bwd_fast_kernel<bf16, EBV><<<fb, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k,  \
+      launch_pdl(route_bwd_fast_kernel<bf16, EBV>, fb, 256, 0, st, wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k,  \
                                                           L->renorm, L->dl, static_cast<bf16*>(dx));                \
       LUFFY_LAUNCHED();                                                                                             \
-      wg_partial_fast_kernel<bf16, EBV><<<pg, 256, 0, st>>>(L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d,    \
+      launch_pdl(wg_partial_fast_kernel<bf16, EBV>, pg, 256, 0, st, L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d,    \
                                                            L->wg_part);                                             \
     } else {                                                                                                        \
-      route_bwd_fast_kernel<float, EBV><<<fb, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, \
+      launch_pdl(route_bwd_fast_kernel<float, EBV>, fb, 256, 0, st, wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, \
                                                            L->renorm, L->dl, static_cast<float*>(dx));              \
       LUFFY_LAUNCHED();                                                                                             \
-      wg_partial_fast_kernel<float, EBV><<<pg, 256, 0, st>>>(L->dl, static_cast<const float*>(x), L->T, L->E, L->d,  \
+      launch_pdl(wg_partial_fast_kernel<float, EBV>, pg, 256, 0, st, L->dl, static_cast<const float*>(x), L->T, L->E, L->d,  \
                                                             L->wg_part);                                            \
     }                                                                                                               \
     LUFFY_LAUNCHED();                                                                                               \
@@ -512,17 +719,17 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
     else LUFFY_RB(32);
 #undef LUFFY_RB
     const int n = L->E * L->d;
-    wg_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(L->wg_part, parts, n, dwg);
+    launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
     LUFFY_LAUNCHED();
     return 0;
   }
   int blocks = (L->T + 7) / 8;
   blocks = blocks > 148 * 16 ? 148 * 16 : blocks;
   if (L->dtype == LUFFY_BF16)
-    route_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, L->renorm,
+    launch_pdl(route_bwd_kernel<bf16>, blocks, 256, 0, st, wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, L->renorm,
                                                    L->dl, static_cast<bf16*>(dx));
   else
-    route_bwd_kernel<float><<<blocks, 256, 0, st>>>(wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, L->renorm,
+    launch_pdl(route_bwd_kernel<float>, blocks, 256, 0, st, wg, L->probs, L->idx, L->w, dw, L->T, L->E, L->d, L->k, L->renorm,
                                                     L->dl, static_cast<float*>(dx));
   LUFFY_LAUNCHED();
   const int parts = wg_parts(L->E, L->d);
@@ -530,12 +737,12 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
   constexpr int EB = 16;
   dim3 grid((L->d + 255) / 256, parts, (L->E + EB - 1) / EB);
   if (L->dtype == LUFFY_BF16)
-    wg_partial_kernel<bf16, EB><<<grid, 256, 0, st>>>(L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d, chunk, L->wg_part);
+    launch_pdl(wg_partial_kernel<bf16, EB>, grid, 256, 0, st, L->dl, static_cast<const bf16*>(x), L->T, L->E, L->d, chunk, L->wg_part);
   else
-    wg_partial_kernel<float, EB><<<grid, 256, 0, st>>>(L->dl, static_cast<const float*>(x), L->T, L->E, L->d, chunk, L->wg_part);
+    launch_pdl(wg_partial_kernel<float, EB>, grid, 256, 0, st, L->dl, static_cast<const float*>(x), L->T, L->E, L->d, chunk, L->wg_part);
   LUFFY_LAUNCHED();
   const int n = L->E * L->d;
-  wg_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(L->wg_part, parts, n, dwg);
+  launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -90,3 +90,22 @@ def test_planner_rejects_bad_arguments(L):
         L.luffy_plan_migration([3], [[1, 1]], 0, 8, 8)          # q < 1
     with pytest.raises(L.LuffyError):
         L.luffy_plan_migration([10, 10], [[1, 1], [1, 1]], 2, 8, 8, capacity_tokens=5)
+
+
+def test_every_kernel_enters_through_pdl():
+    """Kernels are launched with programmatic stream serialization; correctness along the stream needs
+    every kernel to execute griddepcontrol.wait (pdl_enter) before its first global access, and no launch
+    may bypass launch_pdl (a <<<>>> launch would not carry the attribute; harmless, but unmeasured)."""
+    csrc = os.path.join(ROOT, "paper_2411_15419_b200", "csrc")
+    kernels = 0
+    for fn in sorted(os.listdir(csrc)):
+        if not fn.endswith((".cu", ".cuh")):
+            continue
+        src = open(os.path.join(csrc, fn)).read()
+        code = re.sub(r"//[^\n]*", "", src)
+        assert "<<<" not in code, f"{fn}: raw <<<>>> launch"
+        for m in re.finditer(r"__global__[^;{]*?\)\s*\{", code, re.S):
+            body = code[m.end():m.end() + 200].lstrip()
+            assert body.startswith("pdl_enter();"), f"{fn}: kernel at offset {m.start()} does not start with pdl_enter()"
+            kernels += 1
+    assert kernels >= 30

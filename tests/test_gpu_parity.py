@@ -20,6 +20,8 @@ C1 = workload.CONFIGS["C1"]
 C2S = dataclasses.replace(workload.CONFIGS["C2"], seqs_per_rank=2)
 C3S = dataclasses.replace(workload.CONFIGS["C3"], seqs_per_rank=2)
 C5S = dataclasses.replace(workload.CONFIGS["C5"], d_model=1024, d_ffn=2048, seqs_per_rank=1, seq_len=512)
+# C4's 32 experts (the E > 16 gate kernels) at d=512 and 1024 tokens
+C4S = dataclasses.replace(workload.CONFIGS["C4"], d_model=512, d_ffn=1024, seqs_per_rank=1, seq_len=1024)
 
 
 def _inputs(cfg, rank=0, **kw):
@@ -134,7 +136,8 @@ def test_c1_fp32_simulated_ranks(rank):
     _check_numerics(C1, inp, res, C1.h)
 
 
-@pytest.mark.parametrize("cfg,h", [(C2S, 0.9), (C2S, 1.01), (C3S, 0.95), (C3S, 0.8), (C5S, 0.9)])
+@pytest.mark.parametrize("cfg,h", [(C2S, 0.9), (C2S, 1.01), (C3S, 0.95), (C3S, 0.8), (C5S, 0.9),
+                                    (C4S, 0.9)])
 def test_bf16_configs(cfg, h):
     inp = _inputs(cfg)
     res = run_gpu_layer(cfg, inp, h=h)
@@ -180,6 +183,18 @@ def test_ragged_edge_cases():
                 assert res["rep"][a, jj[0]] == res["rep"][3, j]
     z = res["rep"][5]
     assert (z == 5).all()
+
+
+@pytest.mark.parametrize("T", [203, 17])
+def test_ragged_bf16(T):
+    """bf16 C2 dims with a token count that is not a multiple of any kernel's token tile."""
+    inp = _inputs(C2S)
+    inp = dict(inp, X=inp["X"][:T], dY=inp["dY"][:T])
+    res = run_gpu_layer(C2S, inp, h=0.9)
+    _check_route(C2S, inp, res)
+    _check_condense(C2S, inp, res, 0.9)
+    _check_layout(C2S, inp, res)
+    _check_numerics(C2S, inp, res, 0.9)
 
 
 def test_single_token():

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ mcnt, int32_t* __restrict__ mcur,
                                                       int32_t* __restrict__ members, int32_t* __restrict__ mslot,
                                                       int cur_cap) {
+  pdl_enter();
   extern __shared__ int cur_smem[];
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
@@ -194,6 +195,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ x, const int32_t* __restrict__ perm,
                                                         const int32_t* __restrict__ soff, int E, int d,
                                                         T* __restrict__ dst) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t rows = soff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -220,6 +222,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ pos,
                                                          const float* __restrict__ w, int T_, int k, int d,
                                                          T* __restrict__ y) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
@@ -242,6 +245,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) dw_kernel(const T* __restrict__ dy, const T* __restrict__ gathered,
                                                  const int32_t* __restrict__ pos, int T_, int k, int d,
                                                  float* __restrict__ dw) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
@@ -295,6 +299,7 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
     const int32_t* __restrict__ mslot, const int32_t* __restrict__ mstart, const int32_t* __restrict__ mcnt,
     const int32_t* __restrict__ gtok, const float* __restrict__ gw, int d, T* __restrict__ dg, float* __restrict__ part,
     XDest xd) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nwin = goff[E] / WIN;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -395,6 +400,7 @@ __global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int3
                                                                       const int32_t* __restrict__ mcnt, int d,
                                                                       const float* __restrict__ part, T* __restrict__ dg,
                                                                       XDest xd, XSignal sig) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t rows = soff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -427,6 +433,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ dsend, const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ rep, int T_, int k, int d,
                                                          T* __restrict__ dx) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
@@ -459,7 +466,7 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
     LUFFY_CUDA_TRY(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000 * 4));
     attr = true;
   }
-  layout_kernel<<<L->E, 1024, cur_cap * 4, st>>>(L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
+  launch_pdl(layout_kernel, L->E, 1024, cur_cap * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
                                                  L->mcnt, L->mcur, L->members, L->mslot, cur_cap);
   LUFFY_LAUNCHED();
@@ -469,10 +476,10 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
   if (dst_rows) {
     const int blocks = grid_for_warps(L->Rpad_max);
     if (L->dtype == LUFFY_BF16)
-      pack_rows_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->perm, L->soff, L->E, L->d,
+      launch_pdl(pack_rows_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->perm, L->soff, L->E, L->d,
                                                      static_cast<bf16*>(dst_rows));
     else
-      pack_rows_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->perm, L->soff, L->E, L->d,
+      launch_pdl(pack_rows_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->perm, L->soff, L->E, L->d,
                                                       static_cast<float*>(dst_rows));
     LUFFY_LAUNCHED();
   }
@@ -483,10 +490,10 @@ int launch_pack_rows(luffy_layer* L, const void* x, void* dst_rows, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16)
-    pack_rows_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(x), L->perm, L->soff, L->E, L->d,
+    launch_pdl(pack_rows_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->perm, L->soff, L->E, L->d,
                                                    static_cast<bf16*>(dst_rows));
   else
-    pack_rows_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(x), L->perm, L->soff, L->E, L->d,
+    launch_pdl(pack_rows_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->perm, L->soff, L->E, L->d,
                                                     static_cast<float*>(dst_rows));
   LUFFY_LAUNCHED();
   return 0;
@@ -496,10 +503,10 @@ int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void*
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
-    uncondense_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(gathered), L->pos, L->w, L->T, L->k, L->d,
+    launch_pdl(uncondense_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(gathered), L->pos, L->w, L->T, L->k, L->d,
                                                     static_cast<bf16*>(y));
   else
-    uncondense_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(gathered), L->pos, L->w, L->T, L->k, L->d,
+    launch_pdl(uncondense_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(gathered), L->pos, L->w, L->T, L->k, L->d,
                                                      static_cast<float*>(y));
   LUFFY_LAUNCHED();
   return 0;
@@ -523,27 +530,27 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
   const int bs = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16) {
     if (dw) {
-      dw_kernel<bf16><<<bt, 256, 0, st>>>(static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
+      launch_pdl(dw_kernel<bf16>, bt, 256, 0, st, static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
                                           L->k, L->d, dw);
       LUFFY_LAUNCHED();
     }
-    uncondense_bwd_window_kernel<bf16><<<bw, 256, 0, st>>>(static_cast<const bf16*>(dy), L->goff, L->E, L->members,
+    launch_pdl(uncondense_bwd_window_kernel<bf16>, bw, 256, 0, st, static_cast<const bf16*>(dy), L->goff, L->E, L->members,
                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
                                                            static_cast<bf16*>(dg), L->mpart, xd);
     LUFFY_LAUNCHED();
-    uncondense_bwd_finalize_kernel<bf16><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
+    launch_pdl(uncondense_bwd_finalize_kernel<bf16>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
                                                              static_cast<bf16*>(dg), xd, sig);
   } else {
     if (dw) {
-      dw_kernel<float><<<bt, 256, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos,
+      launch_pdl(dw_kernel<float>, bt, 256, 0, st, static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos,
                                            L->T, L->k, L->d, dw);
       LUFFY_LAUNCHED();
     }
-    uncondense_bwd_window_kernel<float><<<bw, 256, 0, st>>>(static_cast<const float*>(dy), L->goff, L->E, L->members,
+    launch_pdl(uncondense_bwd_window_kernel<float>, bw, 256, 0, st, static_cast<const float*>(dy), L->goff, L->E, L->members,
                                                             L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
                                                             static_cast<float*>(dg), L->mpart, xd);
     LUFFY_LAUNCHED();
-    uncondense_bwd_finalize_kernel<float><<<bs, 256, 0, st>>>(L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,
+    launch_pdl(uncondense_bwd_finalize_kernel<float>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,
                                                               L->mpart, static_cast<float*>(dg), xd, sig);
   }
   LUFFY_LAUNCHED();
@@ -554,10 +561,10 @@ int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
-    unpack_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
+    launch_pdl(unpack_bwd_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
                                                     static_cast<bf16*>(dx));
   else
-    unpack_bwd_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
+    launch_pdl(unpack_bwd_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
                                                      static_cast<float*>(dx));
   LUFFY_LAUNCHED();
   return 0;

@@ -1,16 +1,21 @@
 // tcgen05 grouped GEMMs for the expert FFN (bf16 in, fp32 accumulation in TMEM), sm_100a.
 //
-// One persistent CTA per SM, warp-specialized:
-//   warp 0      TMA producer: 4-stage ring of (A 128x64, B 256x64) bf16 tiles, SWIZZLE_128B, mbarrier
-//               transaction counts;
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16)
-//               into a double-buffered TMEM accumulator (2 x 256 columns);
+// One persistent CTA per SM, warp-specialized, as a CTA PAIR (cta_group::2, cluster of 2 on one TPC) or
+// a single CTA (fallback, LUFFY_GEMM_CG=1):
+//   warp 0      TMA producer: ring of (A 128x64, B (256/CG)x64) bf16 tiles, SWIZZLE_128B (6 stages of 32 KiB
+//               per CTA for the pair, 4 of 48 KiB single); in the pair both CTAs load their own halves and
+//               complete the bytes on the leader's barrier;
+//   warp 1      MMA issuer: one thread of the leader issues tcgen05.mma.cta_group::{2,1}.kind::f16 (M=256 or
+//               128, N=256, K=16) into a double-buffered TMEM accumulator (2 x 256 columns per CTA); the
+//               pair halves the B bytes each SM stages and reads per MMA;
 //   warps 2-9   epilogue (two per TMEM lane quarter, one column half each): tcgen05.ld 32x32b.x32 -> fused GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the
 //               fp32 weight gradient) stored straight to global memory.
 // Tiles walk expert segments whose row offsets (multiples of 128) live on the device, so no host sync
 // is needed to size the work.  Operands may be K-major or MN-major (the backward reads W1/W2 and the
 // token-major activations transposed through the descriptor's major bit instead of transposing data).
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "exchange.cuh"
@@ -19,13 +24,18 @@
 namespace luffy {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
-constexpr int B_BYTES = BN * BK * 2;   // 32 KiB
+constexpr int BM = 128, BN = 256, BK = 64;  // BM: accumulator rows per CTA (the pair's tile is 256 x 256)
+constexpr int A_BYTES = BM * BK * 2;   // 16 KiB per CTA
 constexpr int EPI_WARPS = 8;
 constexpr int STG_BYTES = 4096;  // per epilogue warp: output staging (coalesced stores)
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 1024 + 256;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quarter)
+template <int CG>
+struct Pipe {
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int B_ROWS = BN / CG;           // N rows of B staged by one CTA
+  static constexpr int B_BYTES = B_ROWS * BK * 2;  // 32 KiB single, 16 KiB in the pair
+  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 1024 + 256;
+};
 
 struct TcArgs {
   const int32_t* off;  // [G+1] segment offsets (rows), multiples of 128
@@ -46,30 +56,52 @@ struct TcArgs {
 };
 
 struct Tile {
-  int g, m0, n0, nkb, krow0;
+  int g, m0, n0, nkb, krow0, mlim;  // mlim: end of the expert segment (rows mode)
 };
 
-template <bool WG>
+// Pair tiles cover two consecutive 128-row blocks of ONE expert segment (the MMA shares B between the
+// halves); a segment with an odd block count ends in a half-empty pair whose second half is not stored.
+template <bool WG, int CG>
 __device__ __forceinline__ int num_tiles(const TcArgs& a, const int32_t* off_s) {
-  if (WG) return a.G * (a.M / BM) * a.nbc;
-  return (off_s[a.G] / BM) * a.nbc;
+  if (WG) return a.G * (a.M / (BM * CG)) * a.nbc;
+  if (CG == 1) return (off_s[a.G] / BM) * a.nbc;
+  int n = 0;
+  for (int g = 0; g < a.G; ++g) n += ((off_s[g + 1] - off_s[g]) / BM + 1) / 2;
+  return n * a.nbc;
 }
 
-template <int EPI, bool WG>
+template <int EPI, bool WG, int CG>
 __device__ __forceinline__ Tile decode(int t, const TcArgs& a, const int32_t* off_s) {
   Tile x;
   if (WG) {
-    const int tpg = (a.M / BM) * a.nbc;
+    const int tpg = (a.M / (BM * CG)) * a.nbc;
     x.g = t / tpg;
     const int r = t % tpg;
-    x.m0 = (r / a.nbc) * BM;
+    x.m0 = (r / a.nbc) * BM * CG;
     x.n0 = (r % a.nbc) * BN;
     x.krow0 = off_s[x.g];
     x.nkb = (off_s[x.g + 1] - off_s[x.g]) / BK;
+    x.mlim = a.M;
   } else {
     const int mb = t / a.nbc, nb = t % a.nbc;
-    x.m0 = mb * BM;
-    x.g = find_group(off_s, a.G, x.m0);
+    if (CG == 1) {
+      x.m0 = mb * BM;
+      x.g = find_group(off_s, a.G, x.m0);
+    } else {
+      int r = mb;
+      x.g = 0;
+      x.m0 = 0;
+      for (int g = 0; g < a.G; ++g) {
+        const int pb = ((off_s[g + 1] - off_s[g]) / BM + 1) / 2;
+        if (r < pb) {
+          x.g = g;
+          x.m0 = off_s[g] + r * 2 * BM;
+          break;
+        }
+        r -= pb;
+      }
+    }
+    x.mlim = off_s[x.g + 1];
     x.n0 = nb * (EPI == EPI_SWIGLU ? BN / 2 : BN);
     x.nkb = a.K / BK;
     x.krow0 = 0;
@@ -193,13 +225,19 @@ __device__ __forceinline__ void load32_bf16(const bf16* src, float (&v)[32]) {
   }
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool WG>
+template <int EPI, bool A_MN, bool B_MN, bool WG, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                    const __grid_constant__ CUtensorMap tB3, const TcArgs a) {
   pdl_enter();
+  constexpr int STAGES = Pipe<CG>::STAGES;
+  constexpr int B_BYTES = Pipe<CG>::B_BYTES;
+  constexpr int B_ROWS = Pipe<CG>::B_ROWS;
   extern __shared__ uint8_t smem_raw[];
   __shared__ int32_t off_s[LUFFY_MAX_EXPERTS + 1];
+  const uint32_t crank = CG == 2 ? tc::cluster_rank() : 0u;  // 0: leader (issues the MMA)
+  const int hm = (int)crank * BM;       // this CTA's accumulator rows within the pair tile
+  const int hb = (int)crank * B_ROWS;   // this CTA's N rows of B within the tile
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
@@ -219,47 +257,67 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 8);
+      tc::mbar_init(&tempty[s], EPI_WARPS * CG);  // the pair's epilogue warps all release the leader's buffer
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tA);
     tc::tma_prefetch(&tB);
     if (EPI == EPI_SWIGLU || B_MN) tc::tma_prefetch(&tB3);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_holder, 512);
+  if (warp == 1) {
+    if (CG == 2) tc::tmem_alloc_pair(tmem_holder, 512);
+    else tc::tmem_alloc(tmem_holder, 512);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int ntiles = num_tiles<WG>(a, off_s);
+  const int ntiles = num_tiles<WG, CG>(a, off_s);
+  const int tile0 = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstride = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile x = decode<EPI, WG>(t, a, off_s);
+      for (int t = tile0; t < ntiles; t += tstride) {
+        const Tile x = decode<EPI, WG, CG>(t, a, off_s);
         for (int kb = 0; kb < x.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* dA = sA + stage * A_BYTES;
           uint8_t* dB = sB + stage * B_BYTES;
-          tc::mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          uint32_t barc = 0;  // pair: the leader's full barrier (both CTAs' bytes complete on it)
+          if (CG == 2) {
+            if (crank == 0) tc::mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            barc = tc::map_rank(&full[stage], 0);
+          } else {
+            tc::mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          }
+          auto LD = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if (CG == 2) tc::tma_load_2d_pair(dst, m, barc, c0, c1);
+            else tc::tma_load_2d(dst, m, &full[stage], c0, c1);
+          };
           if (!A_MN) {
-            tc::tma_load_2d(dA, &tA, &full[stage], kb * BK, x.m0);
+            LD(dA, &tA, kb * BK, x.m0 + hm);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tc::tma_load_2d(dA + j * 8192, &tA, &full[stage], x.m0 + 64 * j, x.krow0 + kb * BK);
+            for (int j = 0; j < BM / 64; ++j) LD(dA + j * 8192, &tA, x.m0 + hm + 64 * j, x.krow0 + kb * BK);
           }
           if (WG) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tc::tma_load_2d(dB + j * 8192, &tB, &full[stage], x.n0 + 64 * j, x.krow0 + kb * BK);
+            for (int j = 0; j < B_ROWS / 64; ++j) LD(dB + j * 8192, &tB, x.n0 + hb + 64 * j, x.krow0 + kb * BK);
           } else if (!B_MN) {
-            if (EPI == EPI_SWIGLU) {
-              tc::tma_load_2d(dB, &tB, &full[stage], kb * BK, x.g * a.Nb + x.n0);
-              tc::tma_load_2d(dB + B_BYTES / 2, &tB3, &full[stage], kb * BK, x.g * a.Nb + x.n0);
+            if (EPI == EPI_SWIGLU) {  // N = [W1 rows n0.. (128) | W3 rows n0.. (128)]; the pair splits them
+              if (CG == 2) {
+                LD(dB, crank == 0 ? &tB : &tB3, kb * BK, x.g * a.Nb + x.n0);
+              } else {
+                LD(dB, &tB, kb * BK, x.g * a.Nb + x.n0);
+                LD(dB + B_BYTES / 2, &tB3, kb * BK, x.g * a.Nb + x.n0);
+              }
             } else {
-              tc::tma_load_2d(dB, &tB, &full[stage], kb * BK, x.g * a.Nb + x.n0);
+              LD(dB, &tB, kb * BK, x.g * a.Nb + x.n0 + hb);
             }
           } else {
             const int kk = kb * BK;
@@ -267,22 +325,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             const CUtensorMap* mp = hi ? &tB3 : &tB;
             const int kl = hi ? kk - a.Kb : kk;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tc::tma_load_2d(dB + j * 8192, mp, &full[stage], x.n0 + 64 * j, x.g * a.Kb + kl);
+            for (int j = 0; j < B_ROWS / 64; ++j) LD(dB + j * 8192, mp, x.n0 + hb + 64 * j, x.g * a.Kb + kl);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && crank == 0) {
       // ------------------------------------------------------------------ MMA issuer (single thread)
-      constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      constexpr uint32_t IDESC = tc::idesc_bf16(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const Tile x = decode<EPI, WG>(t, a, off_s);
+      for (int t = tile0; t < ntiles; t += tstride) {
+        const Tile x = decode<EPI, WG, CG>(t, a, off_s);
         tc::mbar_wait(&tempty[acc], aphase ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -295,12 +353,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = A_MN ? tc::smem_desc(a0 + kk * 2048, 8192, 1024) : tc::smem_desc(a0 + kk * 32, 16, 1024);
             const uint64_t bd = (B_MN || WG) ? tc::smem_desc(b0 + kk * 2048, 8192, 1024) : tc::smem_desc(b0 + kk * 32, 16, 1024);
-            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            if (CG == 2) tc::mma_bf16_pair(d_tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            else tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb | kk) != 0 ? 1u : 0u);
           }
-          tc::mma_commit(&empty[stage]);
+          if (CG == 2) tc::mma_commit_pair(&empty[stage], 3);
+          else tc::mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit(&tfull[acc]);
+        if (CG == 2) tc::mma_commit_pair(&tfull[acc], 3);
+        else tc::mma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
@@ -324,19 +385,21 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int r = it * 8 + (lane >> 2), c = lane & 3;
-          const bf16* src = static_cast<const bf16*>(a.aux) + (size_t)(x.m0 + 32 * q + r) * ldx + (b ? a.N : 0) +
+          const bf16* src = static_cast<const bf16*>(a.aux) + (size_t)(x.m0 + hm + 32 * q + r) * ldx + (b ? a.N : 0) +
                             x.n0 + c0 + c * 8;
           pf[b][it] = *reinterpret_cast<const uint4*>(src);
         }
     };
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const Tile x = decode<EPI, WG>(t, a, off_s);
-      if (NB) prefetch(x, hc * (BN / 2));
+    for (int t = tile0; t < ntiles; t += tstride) {
+      const Tile x = decode<EPI, WG, CG>(t, a, off_s);
+      const bool live = WG || x.m0 + hm < x.mlim;  // the second half of an expert's last pair may be empty
+      if (NB && live) prefetch(x, hc * (BN / 2));
       tc::mbar_wait(&tfull[acc], aphase);
       tc::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
-      if (WG) {
-        const int m = x.m0 + rt;
+      if (!live) {
+      } else if (WG) {
+        const int m = x.m0 + hm + rt;
         float* dst = m < a.Msplit ? static_cast<float*>(a.D) + ((size_t)x.g * a.Msplit + m) * a.N
                                   : a.D3 + ((size_t)x.g * (a.M - a.Msplit) + (m - a.Msplit)) * a.N;
         dst += x.n0;
@@ -351,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           store_block_f32(stg, v, dst + c0);
         }
       } else {
-        const size_t row = (size_t)(x.m0 + rt);
+        const size_t row = (size_t)(x.m0 + hm + rt);
         bf16* D = static_cast<bf16*>(a.D);
         bf16* X = static_cast<bf16*>(a.aux);
         if (EPI == EPI_SWIGLU) {
@@ -451,13 +514,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) tc::mbar_arrive_cluster(tc::map_rank(&tempty[acc], 0));
+        else tc::mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
   }
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem_base, 512);
+  if (CG == 2) {
+    tc::tc_fence_before();
+    tc::cluster_sync();  // no CTA of the pair leaves while the other can still arrive on its barriers
+    if (warp == 1) tc::tmem_dealloc_pair(tmem_base, 512);
+  } else {
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem_base, 512);
+  }
   if (a.has_sig) xsignal_done(a.sig);
 }
 
@@ -471,17 +543,50 @@ int num_sms() {
   return n;
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool WG>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
-  auto kern = gemm_tc_kernel<EPI, A_MN, B_MN, WG>;
+// CTA pairs unless LUFFY_GEMM_CG=1 (single-CTA fallback, A/B measurements)
+bool use_pairs() {
+  static const bool on = [] {
+    const char* v = std::getenv("LUFFY_GEMM_CG");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool WG, int CG>
+int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
+  auto kern = gemm_tc_kernel<EPI, A_MN, B_MN, WG, CG>;
+  constexpr int SMEM_BYTES = Pipe<CG>::SMEM;
   static bool attr = false;
   if (!attr) {
     LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
-  launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, a);
+  if (CG == 1) {
+    launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, a);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(num_sms() & ~1);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tb3, a);
+  }
   LUFFY_LAUNCHED();
   return 0;
+}
+
+template <int EPI, bool A_MN, bool B_MN, bool WG>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
+  return use_pairs() ? launch_cg<EPI, A_MN, B_MN, WG, 2>(ta, tb, tb3, a, s) : launch_cg<EPI, A_MN, B_MN, WG, 1>(ta, tb, tb3, a, s);
 }
 
 }  // namespace
@@ -535,7 +640,7 @@ int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D,
     const bool sw = epi == EPI_SWIGLU;
     a.Nb = sw ? N / 2 : N;
     a.nbc = sw ? (N / 2) / (BN / 2) : N / BN;
-    LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, K, (uint64_t)G * a.Nb, K, sw ? BN / 2 : BN));
+    LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, K, (uint64_t)G * a.Nb, K, sw ? BN / 2 : (use_pairs() ? BN / 2 : BN)));
     if (sw) LUFFY_CUDA_TRY(make_tmap_bf16(&tb3, B3, K, (uint64_t)G * a.Nb, K, BN / 2));
     else tb3 = tb;
     switch (epi) {

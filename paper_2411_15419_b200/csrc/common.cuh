@@ -122,6 +122,23 @@ __device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& dg) {
   g = x * cdf;
   dg = cdf + x * 0.3989422804014327f * __expf(-0.5f * x * x);
 }
+// The same pair for the bf16 tensor-core epilogue (reading R12b): Phi from one exponential via Abramowitz &
+// Stegun 26.2.17, Q(|x|) = phi(|x|) (b1 t + ... + b5 t^5), t = 1 / (1 + p |x|), |error| < 7.5e-8 -- far below
+// the bf16 resolution of the stored activation -- so GeLU and GeLU' cost ~17 instructions instead of erff's
+// two-range polynomial plus a second exponential.
+__device__ __forceinline__ void gelu_and_grad_as(float x, float& g, float& dg) {
+  const float ax = fabsf(x);
+  const float phi = 0.3989422804014327f * __expf(-0.5f * x * x);
+  const float t = __fdividef(1.f, fmaf(0.2316419f, ax, 1.f));
+  float poly = fmaf(t, 1.330274429f, -1.821255978f);
+  poly = fmaf(t, poly, 1.781477937f);
+  poly = fmaf(t, poly, -0.356563782f);
+  poly = fmaf(t, poly, 0.319381530f);
+  const float q = phi * poly * t;  // upper tail Q(|x|) = 1 - Phi(|x|)
+  const float cdf = x >= 0.f ? 1.f - q : q;
+  g = x * cdf;
+  dg = fmaf(x, phi, cdf);
+}
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + expf(-x)); }
 __device__ __forceinline__ float silu_grad_f(float x) {
   float s = 1.f / (1.f + expf(-x));

@@ -15,6 +15,7 @@
 // token-major activations transposed through the descriptor's major bit instead of transposing data).
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             } else if (EPI == EPI_GELU) {
               float o[32];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) gelu_and_grad_f(v[i], o[i], v[i]);  // v <- GeLU'(pre)
+              for (int i = 0; i < 32; ++i) gelu_and_grad_as(v[i], o[i], v[i]);  // v <- GeLU'(pre)
               store_block_bf16(stg, v, X + row * a.N + n);
               store_block_bf16(stg, o, D + row * a.N + n);
             } else if (EPI == EPI_DGELU) {
@@ -565,7 +566,6 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, a);
   } else {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(num_sms() & ~1);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = SMEM_BYTES;
     cfg.stream = s;
@@ -577,6 +577,18 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
+    // persistent: as many pairs as can be co-resident (a TPC with one usable SM cannot host a pair)
+    static int pairs = 0;
+    if (pairs == 0) {
+      cfg.gridDim = dim3(num_sms() & ~1);
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = num_sms() / 2;
+      cudaGetLastError();
+      pairs = std::min(n, num_sms() / 2);
+      if (std::getenv("LUFFY_VERBOSE")) std::fprintf(stderr, "[luffy] gemm pair grid: %d co-resident pairs\n", pairs);
+    }
+    cfg.gridDim = dim3(2 * pairs);
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, ta, tb, tb3, a);
   }

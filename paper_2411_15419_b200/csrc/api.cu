@@ -106,6 +106,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->goff = cv.take<int32_t>(m.E + 1);
   o->gtok = cv.take<int32_t>(m.Cpad);
   o->gloc = cv.take<int32_t>(m.C);
+  o->gcopy = cv.take<int32_t>(m.Cpad);
   o->gw = cv.take<float>(m.Cpad);
   o->xg = cv.take<char>(m.Cpad * m.d * es);
   o->gnorm = cv.take<double>(m.Cpad);

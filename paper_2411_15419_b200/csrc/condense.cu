@@ -49,7 +49,8 @@ __device__ __forceinline__ int block_scan_flag(bool flag, int* warp_sums, int& t
 __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w,
                                                            int T, int k, int E, int32_t* __restrict__ gcnt,
                                                            int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
-                                                           float* __restrict__ gw, int32_t* __restrict__ gloc) {
+                                                           float* __restrict__ gw, int32_t* __restrict__ gloc,
+                                                           int32_t* __restrict__ gcopy) {
   pdl_enter();
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
@@ -84,12 +85,14 @@ __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __rest
       gtok[g] = t;
       gw[g] = w[(size_t)t * k + jj];
       gloc[(size_t)t * k + jj] = g;
+      gcopy[g] = t * k + jj;
     }
     base += total;
   }
   for (int g = offs[e] + cnt[e] + threadIdx.x; g < offs[e + 1]; g += blockDim.x) {
     gtok[g] = -1;
     gw[g] = 0.f;
+    gcopy[g] = -1;
   }
 }
 
@@ -465,7 +468,7 @@ __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int3
 int launch_group_build(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   launch_pdl(group_build_kernel, L->E, 1024, 0, st, L->idx, L->w, L->T, L->k, L->E, L->gcnt, L->goff, L->gtok,
-                                            L->gw, L->gloc);
+                                            L->gw, L->gloc, L->gcopy);
   LUFFY_LAUNCHED();
   int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);
   if (L->dtype == LUFFY_BF16)

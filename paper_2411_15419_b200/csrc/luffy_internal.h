@@ -42,6 +42,7 @@ struct luffy_layer {
   int32_t* goff;      // [E+1] padded group-row offsets
   int32_t* gtok;      // [Cpad_max] token of each group row (-1 = padding)
   int32_t* gloc;      // [Tmax, k] group row (global, padded space) of copy (t, j)
+  int32_t* gcopy;     // [Cpad_max] copy t * k + j of each group row (-1 = padding)
   float* gw;          // [Cpad_max] gate weight of each group row (0 for padding)
   void* xg;           // [Cpad_max, d] gathered group rows (dtype)
   double* gnorm;      // [Cpad_max] |x| in fp64

@@ -7,9 +7,9 @@
 //  pack_rows:   dst[slot] = x[perm[slot]] with 16-byte vector copies (zero rows for padding).
 //  uncondense:  y_t = sum_j w_tj * gathered[pos_tj] -- a condensed token reuses its representative's
 //               expert output with its own gate weight (R10); fp32 accumulation.
-//  backward:    d_gathered[slot] = sum over the copies it represents (token order) of w * dy; the
-//               members are read from the slot's adjacency row (they are exactly its neighbours whose
-//               rep is the slot, plus itself), so no atomics and a fixed summation order.
+//  backward:    d_gathered[slot] = sum over the copies it represents (token order) of w * dy, from the
+//               slot-sorted member CSR built by layout (no atomics, fixed summation order); the same
+//               pass computes the gate-weight gradient dw[t, j] = <dy_t, gathered[slot of (t, j)]>.
 #include "common.cuh"
 #include "exchange.cuh"
 
@@ -240,31 +240,6 @@ __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ g
   }
 }
 
-// d_topk_w[t, j] = <dy_t, gathered[pos_tj]>
-template <typename T>
-__global__ void __launch_bounds__(256) dw_kernel(const T* __restrict__ dy, const T* __restrict__ gathered,
-                                                 const int32_t* __restrict__ pos, int T_, int k, int d,
-                                                 float* __restrict__ dw) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
-    for (int j = 0; j < k; ++j) {
-      const T* o = gathered + (size_t)pos[(size_t)t * k + j] * d;
-      float s = 0.f;
-      for (int c = lane * 8; c < d; c += 256) {
-        float a[8], b[8];
-        load8(dy + (size_t)t * d + c, a);
-        load8(o + c, b);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s = fmaf(a[i], b[i], s);
-      }
-      s = warp_sum(s);
-      if (lane == 0) dw[(size_t)t * k + j] = s;
-    }
-  }
-}
-
 // d_gathered[slot] = sum_{members m of the slot, token order} gw[m] * dy[gtok[m]]; padding -> 0.
 //
 // Load-balanced and deterministic: the slot-sorted member array (group-row space) is cut into fixed
@@ -273,6 +248,28 @@ __global__ void __launch_bounds__(256) dw_kernel(const T* __restrict__ dy, const
 // boundaries leaves fp32 partials (the head run of a window at part[w][0], the tail run at part[w][1])
 // that uncondense_bwd_finalize sums in window order.
 constexpr int WIN = 16;
+
+// 8 consecutive elements: raw 16-byte (bf16) / 32-byte (fp32) load, then conversion
+struct F8 {
+  float4 a, b;
+};
+__device__ __forceinline__ uint4 ldraw8(const bf16* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ F8 ldraw8(const float* p) {
+  return F8{*reinterpret_cast<const float4*>(p), *reinterpret_cast<const float4*>(p + 4)};
+}
+__device__ __forceinline__ void cvt8(const uint4& u, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void cvt8(const F8& u, float (&v)[8]) {
+  v[0] = u.a.x; v[1] = u.a.y; v[2] = u.a.z; v[3] = u.a.w;
+  v[4] = u.b.x; v[5] = u.b.y; v[6] = u.b.z; v[7] = u.b.w;
+}
 
 // Destination of the backward rows of send slots: local d_gathered, or (fused combine-backward) the
 // owning rank's dexp buffer at row dst_base[e] + (slot - soff[e]).
@@ -297,15 +294,18 @@ template <typename T>
 __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
     const T* __restrict__ dy, const int32_t* __restrict__ goff, int E, const int32_t* __restrict__ members,
     const int32_t* __restrict__ mslot, const int32_t* __restrict__ mstart, const int32_t* __restrict__ mcnt,
-    const int32_t* __restrict__ gtok, const float* __restrict__ gw, int d, T* __restrict__ dg, float* __restrict__ part,
-    XDest xd) {
+    const int32_t* __restrict__ gtok, const float* __restrict__ gw, const int32_t* __restrict__ gcopy, int d,
+    const T* __restrict__ gathered, float* __restrict__ dw, T* __restrict__ dg, float* __restrict__ part, XDest xd) {
   pdl_enter();
+  using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
   const int lane = threadIdx.x & 31;
   const int64_t nwin = goff[E] / WIN;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwin; wi += nw) {
     const int m0 = (int)(wi * WIN);
-    int my_slot = -1, my_tok = 0;
+    // per-member metadata, resolved once per window (lane u = member u): slot, token, gate weight, copy,
+    // whether the member ends its slot's run inside the window, and where that run's sum goes
+    int my_slot = -1, my_tok = 0, my_copy = -1;
     float my_w = 0.f;
     if (lane < WIN) {
       const int g = members[m0 + lane];
@@ -313,86 +313,81 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
         my_slot = mslot[m0 + lane];
         my_tok = gtok[g];
         my_w = gw[g];
+        my_copy = gcopy[g];
       }
     }
     const unsigned live = __ballot_sync(0xffffffffu, my_slot >= 0);
     if (!live) continue;
-    for (int c0 = 0; c0 < d; c0 += 512) {
-      float acc[2][8];
-      int cur = -1;
-      auto flush = [&](int slot) {
-        const int ms = mstart[slot], me = ms + mcnt[slot];
-        const int c = c0 + lane * 8;
-        if (ms >= m0 && me <= m0 + WIN) {
-          T* out = xd.remote ? xd.row<T>(slot, d) : dg + (size_t)slot * d;
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            if (c + q * 256 < d) store8(out + c + q * 256, acc[q]);
-        } else {
-          float* dst = part + ((size_t)wi * 2 + (ms < m0 ? 0 : 1)) * d;
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            if (c + q * 256 < d) store8(dst + c + q * 256, acc[q]);
-        }
-      };
-      // issue all row loads of the window first (at most WIN rows of 2 x 16 bytes per lane)
-      uint4 raw[WIN][2];
-#pragma unroll
-      for (int u = 0; u < WIN; ++u) {
-        const int tok = __shfl_sync(0xffffffffu, my_tok, u);
-        const bool ok = (live >> u) & 1u;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int c = c0 + q * 256 + lane * 8;
-          if (sizeof(T) == 2 && ok && c < d)
-            raw[u][q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(dy) + (size_t)tok * d + c);
-          else
-            raw[u][q] = make_uint4(0, 0, 0, 0);
-        }
+    const int nxt = __shfl_down_sync(0xffffffffu, my_slot, 1);
+    bool my_end = false, my_inside = false;
+    unsigned long long my_dst = 0ull;
+    if (my_slot >= 0) {
+      my_end = lane == WIN - 1 || nxt != my_slot;
+      if (my_end) {
+        const int ms = mstart[my_slot], me = ms + mcnt[my_slot];
+        my_inside = ms >= m0 && me <= m0 + WIN;
+        my_dst = my_inside ? reinterpret_cast<unsigned long long>(xd.remote ? xd.row<T>(my_slot, d) : dg + (size_t)my_slot * d)
+                           : reinterpret_cast<unsigned long long>(part + ((size_t)wi * 2 + (ms < m0 ? 0 : 1)) * d);
       }
+    }
+    const unsigned ends = __ballot_sync(0xffffffffu, my_end);
+    const unsigned inside = __ballot_sync(0xffffffffu, my_inside);
+    float dot[WIN];  // this lane's partial of <dy_t, gathered[slot]> for every member (gate-weight gradient)
+#pragma unroll
+    for (int u = 0; u < WIN; ++u) dot[u] = 0.f;
+    for (int c0 = 0; c0 < d; c0 += 256) {
+      const int c = c0 + lane * 8;
+      // issue the row loads of the whole window first: dy of every member and, for the gate-weight
+      // gradient, the expert output row of its slot (8 elements per lane each)
+      R rdy[WIN], rg[WIN];
 #pragma unroll
       for (int u = 0; u < WIN; ++u) {
-        const int slot = __shfl_sync(0xffffffffu, my_slot, u);
-        const float wm = __shfl_sync(0xffffffffu, my_w, u);
         const int tok = __shfl_sync(0xffffffffu, my_tok, u);
-        if (slot < 0) continue;  // padding rows (warp-uniform)
-        if (slot != cur) {
-          if (cur >= 0) flush(cur);
-          cur = slot;
+        const int slot = __shfl_sync(0xffffffffu, my_slot, u);
+        const bool ok = ((live >> u) & 1u) && c < d;
+        rdy[u] = ok ? ldraw8(dy + (size_t)tok * d + c) : R{};
+        rg[u] = (ok && dw) ? ldraw8(gathered + (size_t)slot * d + c) : R{};
+      }
+      float acc[8];
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+      for (int u = 0; u < WIN; ++u) {
+        const float wm = __shfl_sync(0xffffffffu, my_w, u);
+        const unsigned long long dst = __shfl_sync(0xffffffffu, my_dst, u);
+        if (!((live >> u) & 1u)) continue;  // padding rows (warp-uniform)
+        float v[8], o[8];
+        cvt8(rdy[u], v);
+        cvt8(rg[u], o);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i] = fmaf(wm, v[i], acc[i]);
+          dot[u] = fmaf(v[i], o[i], dot[u]);
         }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int c = c0 + q * 256 + lane * 8;
-          float v[8];
-          if constexpr (sizeof(T) == 2) {
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u][q]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(h[i]);
-              v[2 * i] = f.x;
-              v[2 * i + 1] = f.y;
-            }
-          } else {
-            if (c < d) load8(reinterpret_cast<const float*>(dy) + (size_t)tok * d + c, v);
-            else
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = 0.f;
+        if ((ends >> u) & 1u) {  // the slot's run ends here: write it (whole slot or a partial), restart
+          if (c < d) {
+            if ((inside >> u) & 1u) store8(reinterpret_cast<T*>(dst) + c, acc);
+            else store8(reinterpret_cast<float*>(dst) + c, acc);
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[q][i] = fmaf(wm, v[i], acc[q][i]);
+          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
         }
       }
-      if (cur >= 0) flush(cur);
+    }
+    if (dw) {
+#pragma unroll
+      for (int u = 0; u < WIN; ++u) {
+        const float sdot = warp_sum(dot[u]);
+        const int cp = __shfl_sync(0xffffffffu, my_copy, u);
+        if (lane == 0 && cp >= 0) dw[cp] = sdot;
+      }
     }
   }
   if (xd.remote) __threadfence_system();
 }
 
-// Slots crossing window boundaries: sum the partials in window order.  Padding slots are zeroed.
+// Slots crossing window boundaries: sum the partials in window order (four interleaved accumulators
+// combined in a fixed tree).  One warp per slot; padding slots are zeroed.
 template <typename T>
 __global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int32_t* __restrict__ perm,
                                                                       const int32_t* __restrict__ soff, int E,
@@ -405,24 +400,39 @@ __global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int3
   const int64_t rows = soff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < rows; s += nw) {
-    if (perm[s] < 0) {
+    const int p = perm[s];
+    const int ms = mstart[s], cnt = mcnt[s];
+    if (p < 0) {
       if (!xd.remote)  // (remote: the expert rank zeroes its own padding rows)
         for (int c = lane * 8; c < d; c += 256) zero8(dg + s * d + c);
       continue;
     }
-    T* out = xd.remote ? xd.row<T>((int)s, d) : dg + s * d;
-    const int ms = mstart[s], me = ms + mcnt[s];
-    const int ws = ms / WIN, we = (me - 1) / WIN;
+    const int ws = ms / WIN, we = (ms + cnt - 1) / WIN;
     if (ws == we) continue;  // written by the window kernel
+    T* out = xd.remote ? xd.row<T>((int)s, d) : dg + s * d;
+    const int n = we - ws + 1;  // partial j of the run: window ws + j (the first is a tail, the rest heads)
     for (int c = lane * 8; c < d; c += 256) {
-      float acc[8], v[8];
-      load8(part + ((size_t)ws * 2 + 1) * d + c, acc);
-      for (int w = ws + 1; w <= we; ++w) {
-        load8(part + ((size_t)w * 2) * d + c, v);
+      float a[4][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += v[i];
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[r][i] = 0.f;
+      for (int j0 = 0; j0 < n; j0 += 4) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int j = j0 + r;
+          if (j < n) {
+            float v[8];
+            load8(part + ((size_t)(ws + j) * 2 + (j == 0 ? 1 : 0)) * d + c, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[r][i] += v[i];
+          }
+        }
       }
-      store8(out + c, acc);
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (a[0][i] + a[1][i]) + (a[2][i] + a[3][i]);
+      store8(out + c, o);
     }
   }
   if (xd.remote) xsignal_done(sig);
@@ -525,29 +535,20 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
     xd.El = L->El;
     sig = make_signal(L, XP_CBWD);
   }
-  const int bt = grid_for_warps(L->T);
   const int bw = grid_for_warps(L->Cpad_max / WIN);
   const int bs = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16) {
-    if (dw) {
-      launch_pdl(dw_kernel<bf16>, bt, 256, 0, st, static_cast<const bf16*>(dy), static_cast<const bf16*>(gathered), L->pos, L->T,
-                                          L->k, L->d, dw);
-      LUFFY_LAUNCHED();
-    }
     launch_pdl(uncondense_bwd_window_kernel<bf16>, bw, 256, 0, st, static_cast<const bf16*>(dy), L->goff, L->E, L->members,
-                                                           L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
-                                                           static_cast<bf16*>(dg), L->mpart, xd);
+                                                           L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d,
+                                                           static_cast<const bf16*>(gathered), dw, static_cast<bf16*>(dg),
+                                                           L->mpart, xd);
     LUFFY_LAUNCHED();
     launch_pdl(uncondense_bwd_finalize_kernel<bf16>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
                                                              static_cast<bf16*>(dg), xd, sig);
   } else {
-    if (dw) {
-      launch_pdl(dw_kernel<float>, bt, 256, 0, st, static_cast<const float*>(dy), static_cast<const float*>(gathered), L->pos,
-                                           L->T, L->k, L->d, dw);
-      LUFFY_LAUNCHED();
-    }
     launch_pdl(uncondense_bwd_window_kernel<float>, bw, 256, 0, st, static_cast<const float*>(dy), L->goff, L->E, L->members,
-                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->d,
+                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d,
+                                                            static_cast<const float*>(gathered), dw,
                                                             static_cast<float*>(dg), L->mpart, xd);
     LUFFY_LAUNCHED();
     launch_pdl(uncondense_bwd_finalize_kernel<float>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,

@@ -129,6 +129,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->mstart = cv.take<int32_t>(m.Rpad);
   o->mcnt = cv.take<int32_t>(m.Rpad);
   o->mcur = cv.take<int32_t>(m.Rpad);
+  o->marr = cv.take<int32_t>(m.Rpad);
   o->members = cv.take<int32_t>(m.Cpad);
   o->mslot = cv.take<int32_t>(m.Cpad);
   o->mpart = cv.take<float>((size_t)(m.Cpad / 16) * 2 * m.d);

@@ -66,6 +66,7 @@ struct luffy_layer {
   int32_t* mstart;    // [Rpad_max] first member (group-row space) of each slot's member list
   int32_t* mcnt;      // [Rpad_max] members per slot
   int32_t* mcur;      // [Rpad_max] placement cursor
+  int32_t* marr;      // [Rpad_max] arrivals of the window partials of a slot (uncondense backward)
   int32_t* members;   // [Cpad_max] member group rows, slot-major, token order within a slot
   int32_t* mslot;     // [Cpad_max] slot of each member entry (-1 = padding)
   float* mpart;       // [Cpad_max / 16 * 2, d] fp32 partial sums of slots crossing member windows

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ slot_gl, int32_t* __restrict__ pos,
                                                       int32_t* __restrict__ rep, int32_t* __restrict__ mstart,
                                                       int32_t* __restrict__ mcnt, int32_t* __restrict__ mcur,
+                                                      int32_t* __restrict__ marr,
                                                       int32_t* __restrict__ members, int32_t* __restrict__ mslot,
                                                       int cur_cap) {
   pdl_enter();
@@ -145,7 +146,10 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
   // members[], mslot[] (the slot of each member).  Deterministic: integer-atomic counts, then a stable
   // block-wide placement (in-warp ranks by __match_any_sync, cross-warp order by warp index).
   const int s0 = offs[e], ns = cnt[e];
-  for (int s = s0 + threadIdx.x; s < offs[e + 1]; s += blockDim.x) mcnt[s] = 0;
+  for (int s = s0 + threadIdx.x; s < offs[e + 1]; s += blockDim.x) {
+    mcnt[s] = 0;
+    marr[s] = 0;
+  }
   for (int g = g0 + n + threadIdx.x; g < goff_s[e + 1]; g += blockDim.x) {
     members[g] = -1;
     mslot[g] = -1;
@@ -245,8 +249,8 @@ __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ g
 // Load-balanced and deterministic: the slot-sorted member array (group-row space) is cut into fixed
 // windows of WIN members; one warp per window walks its members in order, accumulating the current
 // slot in fp32.  A slot that lies inside one window is written directly; a slot crossing window
-// boundaries leaves fp32 partials (the head run of a window at part[w][0], the tail run at part[w][1])
-// that uncondense_bwd_finalize sums in window order.
+// boundaries leaves fp32 partials (the head run of a window at part[w][0], the tail run at part[w][1]);
+// the window delivering a slot's last partial sums them in window order (arrival counter per slot).
 constexpr int WIN = 16;
 
 // 8 consecutive elements: raw 16-byte (bf16) / 32-byte (fp32) load, then conversion
@@ -295,13 +299,22 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
     const T* __restrict__ dy, const int32_t* __restrict__ goff, int E, const int32_t* __restrict__ members,
     const int32_t* __restrict__ mslot, const int32_t* __restrict__ mstart, const int32_t* __restrict__ mcnt,
     const int32_t* __restrict__ gtok, const float* __restrict__ gw, const int32_t* __restrict__ gcopy, int d,
-    const T* __restrict__ gathered, float* __restrict__ dw, T* __restrict__ dg, float* __restrict__ part, XDest xd) {
+    const T* __restrict__ gathered, float* __restrict__ dw, T* __restrict__ dg, float* __restrict__ part,
+    int32_t* __restrict__ marr, const int32_t* __restrict__ perm, const int32_t* __restrict__ soff, XDest xd,
+    XSignal sig) {
   pdl_enter();
   using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
   const int lane = threadIdx.x & 31;
   const int64_t nwin = goff[E] / WIN;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nwin; wi += nw) {
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (!xd.remote) {  // padding slots of d_gathered are zero (remote: the expert rank zeroes its own)
+    const int64_t rows = soff[E];
+    for (int64_t s = gwarp; s < rows; s += nw)
+      if (perm[s] < 0)
+        for (int c = lane * 8; c < d; c += 256) zero8(dg + s * d + c);
+  }
+  for (int64_t wi = gwarp; wi < nwin; wi += nw) {
     const int m0 = (int)(wi * WIN);
     // per-member metadata, resolved once per window (lane u = member u): slot, token, gate weight, copy,
     // whether the member ends its slot's run inside the window, and where that run's sum goes
@@ -321,10 +334,13 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
     const int nxt = __shfl_down_sync(0xffffffffu, my_slot, 1);
     bool my_end = false, my_inside = false;
     unsigned long long my_dst = 0ull;
+    int my_ms = 0, my_me = 0;
     if (my_slot >= 0) {
       my_end = lane == WIN - 1 || nxt != my_slot;
       if (my_end) {
         const int ms = mstart[my_slot], me = ms + mcnt[my_slot];
+        my_ms = ms;
+        my_me = me;
         my_inside = ms >= m0 && me <= m0 + WIN;
         my_dst = my_inside ? reinterpret_cast<unsigned long long>(xd.remote ? xd.row<T>(my_slot, d) : dg + (size_t)my_slot * d)
                            : reinterpret_cast<unsigned long long>(part + ((size_t)wi * 2 + (ms < m0 ? 0 : 1)) * d);
@@ -382,60 +398,55 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
         if (lane == 0 && cp >= 0) dw[cp] = sdot;
       }
     }
-  }
-  if (xd.remote) __threadfence_system();
-}
-
-// Slots crossing window boundaries: sum the partials in window order (four interleaved accumulators
-// combined in a fixed tree).  One warp per slot; padding slots are zeroed.
-template <typename T>
-__global__ void __launch_bounds__(256) uncondense_bwd_finalize_kernel(const int32_t* __restrict__ perm,
-                                                                      const int32_t* __restrict__ soff, int E,
-                                                                      const int32_t* __restrict__ mstart,
-                                                                      const int32_t* __restrict__ mcnt, int d,
-                                                                      const float* __restrict__ part, T* __restrict__ dg,
-                                                                      XDest xd, XSignal sig) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int64_t rows = soff[E];
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < rows; s += nw) {
-    const int p = perm[s];
-    const int ms = mstart[s], cnt = mcnt[s];
-    if (p < 0) {
-      if (!xd.remote)  // (remote: the expert rank zeroes its own padding rows)
-        for (int c = lane * 8; c < d; c += 256) zero8(dg + s * d + c);
-      continue;
-    }
-    const int ws = ms / WIN, we = (ms + cnt - 1) / WIN;
-    if (ws == we) continue;  // written by the window kernel
-    T* out = xd.remote ? xd.row<T>((int)s, d) : dg + s * d;
-    const int n = we - ws + 1;  // partial j of the run: window ws + j (the first is a tail, the rest heads)
-    for (int c = lane * 8; c < d; c += 256) {
-      float a[4][8];
+    // runs left as partials (a slot crossing window boundaries): the window that delivers a slot's LAST
+    // partial sums all of them in window order (the tail partial of the first window, then the head
+    // partials) -- a fixed order, so the result does not depend on which window arrives last
+    unsigned pm = ends & ~inside & live;
+    if (pm) {
+      __threadfence();
+      while (pm) {
+        const int u = __ffs(pm) - 1;
+        pm &= pm - 1u;
+        const int slot = __shfl_sync(0xffffffffu, my_slot, u);
+        const int ms = __shfl_sync(0xffffffffu, my_ms, u), me = __shfl_sync(0xffffffffu, my_me, u);
+        const int ws = ms / WIN, we = (me - 1) / WIN, n = we - ws + 1;
+        int last = 0;
+        if (lane == 0) last = atomicAdd(marr + slot, 1) == n - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+        T* out = xd.remote ? xd.row<T>(slot, d) : dg + (size_t)slot * d;
+        for (int c = lane * 8; c < d; c += 256) {
+          float a[4][8];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+          for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[r][i] = 0.f;
-      for (int j0 = 0; j0 < n; j0 += 4) {
+            for (int i = 0; i < 8; ++i) a[r][i] = 0.f;
+          for (int j0 = 0; j0 < n; j0 += 4) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int j = j0 + r;
-          if (j < n) {
-            float v[8];
-            load8(part + ((size_t)(ws + j) * 2 + (j == 0 ? 1 : 0)) * d + c, v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[r][i] += v[i];
+            for (int r = 0; r < 4; ++r) {
+              const int j = j0 + r;
+              if (j < n) {
+                const float4* src = reinterpret_cast<const float4*>(part + ((size_t)(ws + j) * 2 + (j == 0 ? 1 : 0)) * d + c);
+                const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                a[r][0] += x0.x; a[r][1] += x0.y; a[r][2] += x0.z; a[r][3] += x0.w;
+                a[r][4] += x1.x; a[r][5] += x1.y; a[r][6] += x1.z; a[r][7] += x1.w;
+              }
+            }
           }
-        }
-      }
-      float o[8];
+          float o[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = (a[0][i] + a[1][i]) + (a[2][i] + a[3][i]);
-      store8(out + c, o);
+          for (int i = 0; i < 8; ++i) o[i] = (a[0][i] + a[1][i]) + (a[2][i] + a[3][i]);
+          store8(out + c, o);
+        }
+        if (lane == 0) marr[slot] = 0;  // ready for the next backward over the same layout
+      }
     }
   }
-  if (xd.remote) xsignal_done(sig);
+  if (xd.remote) {
+    __threadfence_system();
+    xsignal_done(sig);
+  }
 }
 
 // dx[t] = sum_{j : rep(t, j) == t} d_send[pos_tj]   (condensed copies get no expert-path gradient, R11)
@@ -478,7 +489,7 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
   }
   launch_pdl(layout_kernel, L->E, 1024, cur_cap * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
-                                                 L->mcnt, L->mcur, L->members, L->mslot, cur_cap);
+                                                 L->mcnt, L->mcur, L->marr, L->members, L->mslot, cur_cap);
   LUFFY_LAUNCHED();
   if (rep_out) {
     LUFFY_CUDA_TRY(cudaMemcpyAsync(rep_out, L->rep, sizeof(int32_t) * L->T * L->k, cudaMemcpyDeviceToDevice, st));
@@ -536,23 +547,14 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
     sig = make_signal(L, XP_CBWD);
   }
   const int bw = grid_for_warps(L->Cpad_max / WIN);
-  const int bs = grid_for_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16) {
     launch_pdl(uncondense_bwd_window_kernel<bf16>, bw, 256, 0, st, static_cast<const bf16*>(dy), L->goff, L->E, L->members,
-                                                           L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d,
-                                                           static_cast<const bf16*>(gathered), dw, static_cast<bf16*>(dg),
-                                                           L->mpart, xd);
-    LUFFY_LAUNCHED();
-    launch_pdl(uncondense_bwd_finalize_kernel<bf16>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d, L->mpart,
-                                                             static_cast<bf16*>(dg), xd, sig);
+               L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d, static_cast<const bf16*>(gathered), dw,
+               static_cast<bf16*>(dg), L->mpart, L->marr, L->perm, L->soff, xd, sig);
   } else {
     launch_pdl(uncondense_bwd_window_kernel<float>, bw, 256, 0, st, static_cast<const float*>(dy), L->goff, L->E, L->members,
-                                                            L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d,
-                                                            static_cast<const float*>(gathered), dw,
-                                                            static_cast<float*>(dg), L->mpart, xd);
-    LUFFY_LAUNCHED();
-    launch_pdl(uncondense_bwd_finalize_kernel<float>, bs, 256, 0, st, L->perm, L->soff, L->E, L->mstart, L->mcnt, L->d,
-                                                              L->mpart, static_cast<float*>(dg), xd, sig);
+               L->mslot, L->mstart, L->mcnt, L->gtok, L->gw, L->gcopy, L->d, static_cast<const float*>(gathered), dw,
+               static_cast<float*>(dg), L->mpart, L->marr, L->perm, L->soff, xd, sig);
   }
   LUFFY_LAUNCHED();
   return 0;

@@ -124,15 +124,28 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
       rank_of[r] = -1;
       slot_of[r] = -1;
       rowmask[r] = 0ull;  // padding rows are not combined anywhere
-      // padding row: zero it in the receive buffer and in the backward buffer
-      const size_t rb = (size_t)d * elem_bytes;
+    }
+  }
+  // padding rows (the tail of each local expert segment) are zeroed in the receive buffer and in the
+  // backward buffer: one warp per row, 16-byte coalesced stores
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = nthreads >> 5;
+  int64_t wgl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t rb = (size_t)d * elem_bytes;
+  for (int el = 0; el < El; ++el) {
+    const int e = me * El + el;
+    int64_t used = 0;
+    for (int q = 0; q < P; ++q) used += cnt_all[q * E + e];
+    const int64_t p0 = roff[el] + used, p1 = roff[el + 1];
+    for (int64_t r = p0 + wgl; r < p1; r += nw) {
       uint4* a = reinterpret_cast<uint4*>(reinterpret_cast<char*>(recv) + r * rb);
       uint4* b = reinterpret_cast<uint4*>(reinterpret_cast<char*>(dexp) + r * rb);
-      for (size_t j = 0; j < rb / 16; ++j) {
+      for (size_t j = lane; j < rb / 16; j += 32) {
         a[j] = make_uint4(0, 0, 0, 0);
         b[j] = make_uint4(0, 0, 0, 0);
       }
     }
+    wgl = (wgl + (p1 - p0)) % nw;  // spread the next segment's rows over other warps
   }
 }
 

@@ -310,9 +310,14 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (!xd.remote) {  // padding slots of d_gathered are zero (remote: the expert rank zeroes its own)
     const int64_t rows = soff[E];
-    for (int64_t s = gwarp; s < rows; s += nw)
-      if (perm[s] < 0)
-        for (int c = lane * 8; c < d; c += 256) zero8(dg + s * d + c);
+    for (int64_t b = gwarp * 32; b < rows; b += nw * 32) {  // 32 slots per warp step, one perm load each
+      unsigned pad = __ballot_sync(0xffffffffu, b + lane < rows && perm[b + lane] < 0);
+      while (pad) {
+        const int u = __ffs(pad) - 1;
+        pad &= pad - 1u;
+        for (int c = lane * 8; c < d; c += 256) zero8(dg + (b + u) * d + c);
+      }
+    }
   }
   for (int64_t wi = gwarp; wi < nwin; wi += nw) {
     const int m0 = (int)(wi * WIN);
@@ -416,28 +421,37 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
         if (!last) continue;
         __threadfence();
         T* out = xd.remote ? xd.row<T>(slot, d) : dg + (size_t)slot * d;
-        for (int c = lane * 8; c < d; c += 256) {
+        // partials summed in window order j = 0 .. n-1 for up to 4 column chunks at once (two windows
+        // of loads in flight), chunk groups of 1024 columns
+        for (int cg = 0; cg < d; cg += 1024) {
           float a[4][8];
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
+          for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a[r][i] = 0.f;
-          for (int j0 = 0; j0 < n; j0 += 4) {
+            for (int i = 0; i < 8; ++i) a[q][i] = 0.f;
+#pragma unroll 2
+          for (int j = 0; j < n; ++j) {
+            const float* src = part + ((size_t)(ws + j) * 2 + (j == 0 ? 1 : 0)) * d;
+            float4 x[4][2] = {};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int j = j0 + r;
-              if (j < n) {
-                const float4* src = reinterpret_cast<const float4*>(part + ((size_t)(ws + j) * 2 + (j == 0 ? 1 : 0)) * d + c);
-                const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-                a[r][0] += x0.x; a[r][1] += x0.y; a[r][2] += x0.z; a[r][3] += x0.w;
-                a[r][4] += x1.x; a[r][5] += x1.y; a[r][6] += x1.z; a[r][7] += x1.w;
+            for (int q = 0; q < 4; ++q) {
+              const int c = cg + q * 256 + lane * 8;
+              if (c < d) {
+                x[q][0] = __ldcg(reinterpret_cast<const float4*>(src + c));
+                x[q][1] = __ldcg(reinterpret_cast<const float4*>(src + c) + 1);
               }
             }
-          }
-          float o[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) o[i] = (a[0][i] + a[1][i]) + (a[2][i] + a[3][i]);
-          store8(out + c, o);
+            for (int q = 0; q < 4; ++q) {
+              a[q][0] += x[q][0].x; a[q][1] += x[q][0].y; a[q][2] += x[q][0].z; a[q][3] += x[q][0].w;
+              a[q][4] += x[q][1].x; a[q][5] += x[q][1].y; a[q][6] += x[q][1].z; a[q][7] += x[q][1].w;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = cg + q * 256 + lane * 8;
+            if (c < d) store8(out + c, a[q]);
+          }
         }
         if (lane == 0) marr[slot] = 0;  // ready for the next backward over the same layout
       }

@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) tc::mbar_arrive_cluster(tc::map_rank(&tempty[acc], 0));
+        if (CG == 2) tc::mbar_arrive_cluster_relaxed(tc::map_rank(&tempty[acc], 0));
         else tc::mbar_arrive(&tempty[acc]);
       }
       acc ^= 1;

@@ -2,8 +2,12 @@
 // ... easily parallelized" and P:378 (threshold graph).
 //
 // Per expert group e (rows xg[goff[e] .. goff[e+1]), zero padded to 128), only upper-triangle tiles
-// (I <= J) of G = Xg Xg^T are computed: 128x128 fp32 accumulators in TMEM from a 6-stage TMA ring of
-// 128x64 bf16 tiles (both operands K-major, SWIZZLE_128B).  The epilogue decides each edge in fp64,
+// (I <= J) of G = Xg Xg^T are computed, as 256x256 tiles on a CTA PAIR (cta_group::2, the leader issues
+// M=256 N=256 MMAs): each CTA stages its 128 rows of the I block and its 128-row half of the J block
+// (6-stage TMA ring, both operands K-major, SWIZZLE_128B) and owns a 128x256 fp32 accumulator in TMEM --
+// half the staged bytes per flop of 128x128 single-CTA tiles, the limit of this kernel.  Half blocks past
+// a group's padded end are computed on whatever rows follow and never written.  The epilogue decides
+// each edge in fp64,
 //     edge(i, j)  <=>  G_ij >= (2h - 1) |x_i| |x_j|,  i != j, i, j < n_e, |x_i|, |x_j| > 0,
 // which is s_ij = (1 + G_ij / (|x_i||x_j|)) / 2 >= h without a division, packs 32 decisions per word
 // and writes the word of (i, j) directly and the word of (j, i) through a warp-ballot bit transpose, so
@@ -16,8 +20,8 @@
 namespace luffy {
 namespace {
 
-constexpr int TS = 128, BK = 64, STAGES = 6;
-constexpr int T_BYTES = TS * BK * 2;  // 16 KiB per operand tile
+constexpr int TS = 128, BK = 64, STAGES = 6;  // TS: rows per CTA; the pair tile is 2 TS x 2 TS
+constexpr int T_BYTES = TS * BK * 2;  // 16 KiB per operand half-tile
 constexpr int SMEM_BYTES = STAGES * 2 * T_BYTES + 1024 + 256;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 
@@ -31,9 +35,11 @@ struct GramArgs {
   double c2h;
 };
 
+// pair tiles (I, J), J >= I, over blocks of 2 TS rows of each group
+__device__ __forceinline__ int pair_blocks(int npad) { return (npad / TS + 1) / 2; }
 __device__ __forceinline__ bool decode_tile(int t, const int32_t* goff_s, int E, int& e, int& I, int& J) {
   for (e = 0; e < E; ++e) {
-    const int nt = (goff_s[e + 1] - goff_s[e]) / TS;
+    const int nt = pair_blocks(goff_s[e + 1] - goff_s[e]);
     const int pairs = nt * (nt + 1) / 2;
     if (t < pairs) {
       int i = 0, rem = t;
@@ -53,6 +59,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
   __shared__ int ntiles_s;
+  __shared__ __align__(16) float njs_all[8 * 32];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * T_BYTES;
@@ -62,6 +69,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = tc::cluster_rank();  // 0: leader (issues the MMA)
   const int E = a.E;
   for (int i = threadIdx.x; i <= E; i += blockDim.x) {
     goff_s[i] = a.goff[i];
@@ -71,7 +79,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   if (threadIdx.x == 0) {
     int n = 0;
     for (int e = 0; e < E; ++e) {
-      const int nt = (goff_s[e + 1] - goff_s[e]) / TS;
+      const int nt = pair_blocks(goff_s[e + 1] - goff_s[e]);
       n += nt * (nt + 1) / 2;
     }
     ntiles_s = n;
@@ -81,45 +89,48 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 8);
+      tc::mbar_init(&tempty[s], 16);  // the epilogue warps of both CTAs release the leader's buffer
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tX);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_holder, 256);
+  if (warp == 1) tc::tmem_alloc_pair(tmem_holder, 512);
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int ntiles = ntiles_s;
   const int nkb = a.d / BK;
+  const int tile0 = blockIdx.x >> 1, tstride = gridDim.x >> 1;
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = tile0; t < ntiles; t += tstride) {
         int e, I, J;
         decode_tile(t, goff_s, E, e, I, J);
-        const int rI = goff_s[e] + I * TS, rJ = goff_s[e] + J * TS;
+        const int h = (int)crank * TS;
+        const int rI = goff_s[e] + I * 2 * TS + h, rJ = goff_s[e] + J * 2 * TS + h;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          tc::mbar_expect_tx(&full[stage], 2 * T_BYTES);
-          tc::tma_load_2d(sA + stage * T_BYTES, &tX, &full[stage], kb * BK, rI);
-          tc::tma_load_2d(sB + stage * T_BYTES, &tX, &full[stage], kb * BK, rJ);
+          if (crank == 0) tc::mbar_expect_tx(&full[stage], 4 * T_BYTES);
+          const uint32_t barc = tc::map_rank(&full[stage], 0);
+          tc::tma_load_2d_pair(sA + stage * T_BYTES, &tX, barc, kb * BK, rI);
+          tc::tma_load_2d_pair(sB + stage * T_BYTES, &tX, barc, kb * BK, rJ);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = tc::idesc_bf16(TS, TS, 0, 0);
+    if (lane == 0 && crank == 0) {
+      constexpr uint32_t IDESC = tc::idesc_bf16(2 * TS, 2 * TS, 0, 0);
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = tile0; t < ntiles; t += tstride) {
         tc::mbar_wait(&tempty[acc], aphase ^ 1);
         tc::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * TS;
+        const uint32_t d_tmem = tmem_base + acc * 2 * TS;
         for (int kb = 0; kb < nkb; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::tc_fence_after();
@@ -127,59 +138,101 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
           const uint32_t b0 = tc::smem_u32(sB + stage * T_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            tc::mma_bf16(d_tmem, tc::smem_desc(a0 + kk * 32, 16, 1024), tc::smem_desc(b0 + kk * 32, 16, 1024), IDESC,
-                         (kb | kk) != 0 ? 1u : 0u);
-          tc::mma_commit(&empty[stage]);
+            tc::mma_bf16_pair(d_tmem, tc::smem_desc(a0 + kk * 32, 16, 1024), tc::smem_desc(b0 + kk * 32, 16, 1024),
+                              IDESC, (kb | kk) != 0 ? 1u : 0u);
+          tc::mma_commit_pair(&empty[stage], 3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit(&tfull[acc]);
+        tc::mma_commit_pair(&tfull[acc], 3);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
     }
   } else {
     const int q = warp & 3;
-    const int hc = (warp - 2) >> 2;  // column half of the tile handled by this warp
+    const int hc = (warp - 2) >> 2;  // column half (128 of the 256 columns) handled by this warp
+    float* njs = njs_all + (warp - 2) * 32;  // this warp's column norms (fp32)
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = tile0; t < ntiles; t += tstride) {
       int e, I, J;
       decode_tile(t, goff_s, E, e, I, J);
       const int n = gcnt_s[e];
-      const int W = (goff_s[e + 1] - goff_s[e]) >> 5;
+      const int npad = goff_s[e + 1] - goff_s[e];
+      const int W = npad >> 5;
       uint32_t* base = a.adj + a.adjoff[e];
-      const int i0 = I * TS + 32 * q;          // first row (group-local) of this warp
+      const int i0 = I * 2 * TS + (int)crank * TS + 32 * q;  // first row (group-local) of this warp
       const int li = i0 + lane;
-      const double ni = a.gnorm[goff_s[e] + li];
+      // norms first (row, and the columns of this warp's four 32-column blocks), then the accumulator
+      const double ni = i0 < npad ? a.gnorm[goff_s[e] + li] : 0.0;
+      double njv[4];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int jc = J * 2 * TS + 32 * (4 * hc + k4) + lane;
+        njv[k4] = jc < npad ? a.gnorm[goff_s[e] + jc] : 0.0;
+      }
       const double thr = a.c2h * ni;
+      const float thr_f = (float)thr;
+      const bool rowok = li < n && ni > 0.0;
       tc::mbar_wait(&tfull[acc], aphase);
       tc::tc_fence_after();
-      const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * TS;
-#pragma unroll 1
-      for (int c = 2 * hc; c < 2 * hc + 2; ++c) {
+      const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * 2 * TS;
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int c = 4 * hc + k4;
+        const int j0 = J * 2 * TS + 32 * c;
+        // rows / columns past the group's padded end, and blocks strictly below the diagonal (written as
+        // the transpose of their mirror) are skipped (warp-uniform)
+        if (i0 >= npad || j0 >= npad || j0 < i0) continue;
         uint32_t r[32];
         tc::tmem_ld32(tb + 32 * c, r);
+        // column norms of this 32-column block: validity mask and fp32 copies broadcast from shared memory
+        const double my_nj = njv[k4];
+        const unsigned colok = __ballot_sync(0xffffffffu, j0 + lane < n && my_nj > 0.0);
+        njs[lane] = (float)my_nj;
+        __syncwarp();
         tc::tmem_ld_wait();
-        const int j0 = J * TS + 32 * c;
-        if (J == I && c < q) continue;  // strictly below the diagonal: written as the transpose of (c, q)
-        const double my_nj = a.gnorm[goff_s[e] + j0 + lane];
-        uint32_t word = 0;
+        // edge iff G >= thr * nj (thr = (2h-1)|x_i|, decided as in fp64): the fp32 product is within
+        // 1.8e-7 (relative) of the fp64 one, so outside a 1e-6 margin the fp32 comparison IS the fp64
+        // decision; the rare elements inside the margin are re-decided in fp64
+        uint32_t word = 0, amb = 0;
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
-          const double nj = __shfl_sync(0xffffffffu, my_nj, b);
-          const int lj = j0 + b;
-          const bool on = li < n && lj < n && ni > 0.0 && nj > 0.0 && (double)__uint_as_float(r[b]) >= thr * nj;
-          word |= (uint32_t)on << b;
+        for (int b4 = 0; b4 < 8; ++b4) {
+          const float4 nq = reinterpret_cast<const float4*>(njs)[b4];
+          const float nv[4] = {nq.x, nq.y, nq.z, nq.w};
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const int b = 4 * b4 + k2;
+            const float g = __uint_as_float(r[b]);
+            const float p = thr_f * nv[k2];
+            word |= (uint32_t)(g >= p) << b;
+            amb |= (uint32_t)(fabsf(g - p) <= 1e-6f * fabsf(p)) << b;
+          }
         }
+        if (__any_sync(0xffffffffu, amb != 0u)) {
+#pragma unroll
+          for (int b = 0; b < 32; ++b) {
+            const double nj = __shfl_sync(0xffffffffu, my_nj, b);
+            if ((amb >> b) & 1u) {
+              const bool on = (double)__uint_as_float(r[b]) >= thr * nj;
+              word = on ? (word | (1u << b)) : (word & ~(1u << b));
+            }
+          }
+        }
+        word &= rowok ? colok : 0u;
         const bool diag = (j0 == i0);
         if (diag) word &= (lane == 31) ? 0u : (0xffffffffu << (lane + 1));  // keep j > i only
-        // bit transpose through ballots: column b of the 32x32 block -> word of row j0 + b
-        uint32_t tr = 0;
+        // 32x32 bit transpose across the warp (recursive block swap, 5 shuffles): column b of the block
+        // -> word of row j0 + b, so the adjacency is symmetric by construction
+        uint32_t tr = word;
 #pragma unroll
-        for (int b = 0; b < 32; ++b) {
-          const uint32_t col = __ballot_sync(0xffffffffu, (word >> b) & 1u);
-          if (b == lane) tr = col;
+        for (int sft = 16; sft >= 1; sft >>= 1) {
+          const uint32_t lo = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu : sft == 4 ? 0x0F0F0F0Fu
+                                                          : sft == 2 ? 0x33333333u : 0x55555555u;
+          const uint32_t oth = __shfl_xor_sync(0xffffffffu, tr, sft);
+          tr = (lane & sft) ? ((tr & ~lo) | ((oth & ~lo) >> sft)) : ((tr & lo) | ((oth & lo) << sft));
         }
+        __syncwarp();
         if (diag) {
           base[(size_t)li * W + (j0 >> 5)] = word | tr;
         } else {
@@ -189,13 +242,14 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) tc::mbar_arrive_cluster_relaxed(tc::map_rank(&tempty[acc], 0));
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
   }
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem_base, 256);
+  tc::tc_fence_before();
+  tc::cluster_sync();  // neither CTA of the pair leaves while the other can still arrive on its barriers
+  if (warp == 1) tc::tmem_dealloc_pair(tmem_base, 512);
 }
 
 __global__ void adj_offsets_tc_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff) {
@@ -239,7 +293,21 @@ int launch_gram_tc(luffy_layer* L, float h, void* s) {
   int dev = 0, sms = 0;
   LUFFY_CUDA_TRY(cudaGetDevice(&dev));
   LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  launch_pdl(gram_tc_kernel, sms, THREADS, SMEM_BYTES, st, tx, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sms & ~1);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, gram_tc_kernel, tx, a));
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -2,16 +2,20 @@
 // exact parallel-rounds greedy (condense.cu has the algorithm statement).
 //
 // Groups are independent (only tokens of the same expert are compared), so each group gets its
-// own cluster of CS CTAs and no grid-wide barrier is needed.  Every CTA owns a slice of the group's
-// rows and keeps REPLICAS of the group-wide state in its shared memory: the alive bitset, the winner
-// bitset, the priority keys and the 1-hop maxima.  A value computed for an owned row is broadcast to
-// the replicas of all CTAs through distributed shared memory, so the neighbour maxima are gathered from
-// local shared memory.  Phases are separated by cluster barriers:
+// own cluster of CS CTAs (several groups per cluster, scheduled by cost, when fewer clusters fit than
+// groups) and no grid-wide barrier is needed.  Every CTA owns a slice of the group's rows (whole 32-row
+// words) and keeps REPLICAS of the group-wide state in its shared memory: the alive bitset, the winner
+// bitset, the priority keys and the 1-hop maxima.  A phase writes only the CTA's own slice; after the
+// cluster barrier every CTA copies the other slices through distributed shared memory (coalesced
+// loads), so the neighbour maxima are read from local shared memory.  Phases:
 //   A  residual degree -> key (broadcast); count alive rows
 //   B  m1 = max key over the alive closed neighbourhood (broadcast)
 //   C  m2 = max m1 over the alive closed neighbourhood; winner iff m2 == key (broadcast bit)
 //   D  winners and their alive neighbours leave (rep = winner; alive bit cleared in every replica)
 #include <cooperative_groups.h>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -29,12 +33,47 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       const uint32_t* __restrict__ adj,
                                                                       int32_t* __restrict__ rep_local,
                                                                       uint32_t* __restrict__ ctrl, int nmax,
-                                                                      int max_rounds, int cache_words) {
+                                                                      int max_rounds, int cache_words, int E) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t gsm[];
+  __shared__ int order_s[LUFFY_MAX_EXPERTS];
+  __shared__ int list_s[LUFFY_MAX_EXPERTS];
+  __shared__ int nlist_s, largest_s;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int e = blockIdx.x / CS;
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  // Groups -> clusters (fewer clusters than groups can be co-resident): longest-processing-time
+  // assignment by cost n^2 (a round scans n rows of n/32 words), computed identically in every CTA:
+  // rank by (cost desc, group asc), then each group to the least-loaded cluster (lowest index on ties).
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const long long ci = (long long)gcnt[i] * gcnt[i];
+    int rk = 0;
+    for (int j = 0; j < E; ++j) {
+      const long long cj = (long long)gcnt[j] * gcnt[j];
+      rk += (cj > ci) || (cj == ci && j < i);
+    }
+    order_s[rk] = i;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long load[32];
+    for (int c = 0; c < ncl; ++c) load[c] = 0;
+    int k = 0;
+    for (int r = 0; r < E; ++r) {
+      const int g = order_s[r];
+      int best = 0;
+      for (int c = 1; c < ncl; ++c)
+        if (load[c] < load[best]) best = c;
+      load[best] += (long long)gcnt[g] * gcnt[g] + 1;
+      if (best == cid) list_s[k++] = g;
+    }
+    nlist_s = k;
+    largest_s = order_s[0];
+  }
+  __syncthreads();
+  int round = 0, max_round = 0;
+  for (int gi = 0; gi < nlist_s; ++gi) {
+  const int e = list_s[gi];
   const int g0 = goff[e];
   const int n = gcnt[e];
   const int W = (goff[e + 1] - g0) >> 5;
@@ -49,6 +88,19 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   const int R = ((n + CS - 1) / CS + 31) / 32 * 32;
   const int r0 = min(n, rank * R), r1 = min(n, r0 + R);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  // phase timeline of the largest group (debug export LUFFY_DBG_GREEDY_TIMES): rank 0, thread 0
+  const bool stamp = rank == 0 && threadIdx.x == 0 && e == largest_s;
+  int nst = 0;
+  auto STAMP = [&]() {
+    if (stamp && nst < 28) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ctrl[8 + 2 * nst] = (uint32_t)t;
+      ctrl[9 + 2 * nst] = (uint32_t)(t >> 32);
+      ctrl[3] = (uint32_t)++nst;
+    }
+  };
+  STAMP();
 
   for (int w = threadIdx.x; w < W; w += blockDim.x) {
     const int valid = n - w * 32;
@@ -57,33 +109,56 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   }
   if (threadIdx.x < 2) cnt[threadIdx.x] = 0u;
   const int ncached = W > 0 ? min(r1 - r0, cache_words / W) : 0;
-  for (int64_t i = threadIdx.x; i < (int64_t)ncached * W; i += blockDim.x) rowc[i] = A[(int64_t)r0 * W + i];
+  {  // own rows -> shared memory, 16-byte vectors (row blocks start at multiples of 32 rows x W % 4 == 0 words)
+    const uint4* src = reinterpret_cast<const uint4*>(A + (int64_t)r0 * W);
+    uint4* dst = reinterpret_cast<uint4*>(rowc);
+    const int nv = ncached * W / 4;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
+  }
   auto ROW = [&](int r) -> const uint32_t* { return r - r0 < ncached ? rowc + (r - r0) * W : A + (int64_t)r * W; };
   for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) rep_local[g0 + r] = -1;
   if (rank == CS - 1)  // padding rows of the group's row space: never representatives
     for (int r = n + threadIdx.x; r < W * 32; r += blockDim.x) rep_local[g0 + r] = -1;
-  cluster.sync();
+  STAMP();  // replicas initialised, own rows cached
+  // Replica exchange: in every phase a CTA writes only its OWN slice (rows [r0, r1) of key / m1, words
+  // [r0/32, (r0+R)/32) of win / alive; R is a multiple of 32) in its shared memory; after the cluster
+  // barrier every CTA copies the other slices from their shared memory with coalesced DSMEM loads.
+  auto gather_rows = [&](unsigned long long* arr) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      const int j = r / R;
+      if (j != rank) arr[r] = *cluster.map_shared_rank(arr + r, j);
+    }
+  };
+  auto gather_words = [&](uint32_t* arr) {
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+      const int j = (w * 32) / R;
+      if (j != rank && j < CS) arr[w] = *cluster.map_shared_rank(arr + w, j);
+    }
+  };
+  const int w0 = r0 >> 5, w1 = min(W, (rank * R + R) >> 5);  // owned words
 
-  int round = 0;
-  for (;; ++round) {
+  for (round = 0;; ++round) {
     if (round >= max_rounds) break;
-    // ---- A: degree -> key, broadcast; count alive
-    for (int w = threadIdx.x; w < W; w += blockDim.x) win[w] = 0u;
+    // alive rows left (identical in every replica): every warp counts, so the exit is uniform
+    int left = 0;
+    for (int w = lane; w < W; w += 32) left += __popc(alive[w]);
+    if (__reduce_add_sync(0xffffffffu, left) == 0) break;
+    // ---- A: residual degree -> key (own rows)
+    for (int w = w0 + threadIdx.x; w < w1; w += blockDim.x) win[w] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       const uint32_t* row = ROW(r);
       int deg = 0;
       for (int w = lane; w < W; w += 32) deg += __popc(row[w] & alive[w]);
       deg = __reduce_add_sync(0xffffffffu, deg);
-      const unsigned long long k = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)r);
-      if (lane < CS) *cluster.map_shared_rank(key + r, lane) = k;
-      if (lane == 0) atomicAdd(cnt + (round & 1), 1u);
+      if (lane == 0) key[r] = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)r);
     }
     cluster.sync();
-    uint32_t left = 0;
-    for (int j = 0; j < CS; ++j) left += *cluster.map_shared_rank(cnt + (round & 1), j);
-    if (left == 0u) break;
-    // ---- B: m1 = max key over the alive closed neighbourhood (local replicas; set bits only)
+    gather_rows(key);
+    __syncthreads();
+    STAMP();
+    // ---- B: m1 = max key over the alive closed neighbourhood (own rows; set bits only)
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       const uint32_t* row = ROW(r);
@@ -97,9 +172,12 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         }
       }
       m = warp_max_u64(m);
-      if (lane < CS) *cluster.map_shared_rank(m1 + r, lane) = m;
+      if (lane == 0) m1[r] = m;
     }
     cluster.sync();
+    gather_rows(m1);
+    __syncthreads();
+    STAMP();
     // ---- C: winner iff max m1 over the alive closed neighbourhood equals key[r].  Every alive neighbour j
     // has m1[j] >= key[r] (r is in j's neighbourhood), so r wins iff m1[r] == key[r] and no alive neighbour
     // has m1[j] != key[r]: most rows lose without a scan and a scan stops at the first violation.
@@ -123,11 +201,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
           break;
         }
       }
-      if (!lose && lane < CS) atomicOr(cluster.map_shared_rank(win + (r >> 5), lane), 1u << (r & 31));
+      if (!lose && lane == 0) atomicOr(win + (r >> 5), 1u << (r & 31));
     }
     cluster.sync();
+    gather_words(win);
+    __syncthreads();
+    STAMP();
     // ---- D: claims (a non-winner has at most one winner neighbour: winners are >= 3 hops apart)
-    if (threadIdx.x == 0) cnt[(round + 1) & 1] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       int owner = -1;
@@ -143,24 +223,30 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         found = __reduce_min_sync(0xffffffffu, found);
         if (found != 0x7fffffff) owner = found;
       }
-      if (owner >= 0) {
-        if (lane == 0) rep_local[g0 + r] = g0 + owner;
-        if (lane < CS) atomicAnd(cluster.map_shared_rank(alive + (r >> 5), lane), ~(1u << (r & 31)));
+      if (owner >= 0 && lane == 0) {
+        rep_local[g0 + r] = g0 + owner;
+        atomicAnd(alive + (r >> 5), ~(1u << (r & 31)));
       }
     }
     cluster.sync();
+    gather_words(alive);
+    __syncthreads();
+    STAMP();
   }
-  if (rank == 0 && threadIdx.x == 0) atomicMax(ctrl + 2, (uint32_t)round);
-  cluster.sync();  // no CTA may exit while a peer can still read its shared memory (the counters above)
+  max_round = max(max_round, round);
+  cluster.sync();  // the replicas are reused by the next group, and no CTA may exit while a peer can still
+                   // read its shared memory
+  }
+  if (rank == 0 && threadIdx.x == 0) atomicMax(ctrl + 2, (uint32_t)max_round);
 }
 
 template <int CS>
-int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, cudaStream_t st) {
+int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int nclusters, cudaStream_t st) {
   auto kern = greedy_cluster_kernel<CS>;
   LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (CS > 8) LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(L->E * CS);
+  cfg.gridDim = dim3(std::min(L->E, std::max(1, std::min(nclusters, 32))) * CS);
   cfg.blockDim = dim3(GC_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -175,7 +261,7 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, cudaS
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
-                                    kGreedyMaxRounds, cache_words));
+                                    kGreedyMaxRounds, cache_words, L->E));
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -193,6 +279,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   const int cache_words = (int)(cache_bytes / 4);
   LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * 64, st));
   static int cs = 0;  // cluster size: 16 (non-portable) when the device accepts it, else 8
+  static int ncl = 0;  // co-resident clusters of that size (groups are scheduled onto them)
   if (cs == 0) {
     cs = 16;
     cudaFuncSetAttribute(greedy_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -211,8 +298,28 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, greedy_cluster_kernel<16>, &cfg) != cudaSuccess || nclusters < 1) cs = 8;
     cudaGetLastError();
+    ncl = nclusters;
+    if (cs == 8) {
+      cudaFuncSetAttribute(greedy_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg.gridDim = dim3(8);
+      attr[0].val.clusterDim.x = 8;
+      if (cudaOccupancyMaxActiveClusters(&ncl, greedy_cluster_kernel<8>, &cfg) != cudaSuccess || ncl < 1) ncl = 1;
+      cudaGetLastError();
+      cfg.gridDim = dim3(16);
+      attr[0].val.clusterDim.x = 16;
+    }
+    if (std::getenv("LUFFY_VERBOSE")) {
+      int n8 = 0;
+      cudaFuncSetAttribute(greedy_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg.gridDim = dim3(8);
+      attr[0].val.clusterDim.x = 8;
+      cudaOccupancyMaxActiveClusters(&n8, greedy_cluster_kernel<8>, &cfg);
+      cudaGetLastError();
+      std::fprintf(stderr, "[luffy] greedy clusters co-resident: %d of 16 CTAs, %d of 8 CTAs (smem %zu)\n", nclusters, n8, smem);
+    }
   }
-  return cs == 16 ? launch_cluster<16>(L, nmax, smem, cache_words, st) : launch_cluster<8>(L, nmax, smem, cache_words, st);
+  return cs == 16 ? launch_cluster<16>(L, nmax, smem, cache_words, ncl, st)
+                  : launch_cluster<8>(L, nmax, smem, cache_words, ncl, st);
 }
 
 }  // namespace luffy

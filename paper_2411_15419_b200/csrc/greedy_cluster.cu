@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) rep_local[g0 + r] = -1;
   if (rank == CS - 1)  // padding rows of the group's row space: never representatives
     for (int r = n + threadIdx.x; r < W * 32; r += blockDim.x) rep_local[g0 + r] = -1;
+  __syncthreads();  // replicas and the row cache are read by every warp of the CTA
   STAMP();  // replicas initialised, own rows cached
   // Replica exchange: in every phase a CTA writes only its OWN slice (rows [r0, r1) of key / m1, words
   // [r0/32, (r0+R)/32) of win / alive; R is a multiple of 32) in its shared memory; after the cluster

@@ -89,17 +89,18 @@ class CondensedMoELayer:
         return torch.cuda.current_stream().cuda_stream
 
     def forward(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
-                stats: bool = False, want_rows: bool = False) -> torch.Tensor:
+                stats: bool = False, want_rows: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
         T = x.shape[0]
         s = self._stream()
         self.T = T
+        y = self.y if out is None else out
         L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
         self.stats = L.luffy_condense(self.layer, x, h, self.rep, s, stats=stats)
         self.rows = L.luffy_dispatch(self.layer, x, self.recv, s, want_rows=want_rows)
         L.luffy_expert_ffn(self.layer, self.recv, w1, w2, w3, self.out, self.pre, self.act_buf, s)
         L.luffy_combine(self.layer, self.out, self.gathered, s)
-        L.luffy_uncondense(self.layer, self.gathered, self.y, s)
-        return self.y[:T]
+        L.luffy_uncondense(self.layer, self.gathered, y, s)
+        return y[:T]
 
     def forward_migrated(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
                          seq_len=None, q: int = 1, seq_dest=None, capacity: int = 0, objective: int = 0, group=None):
@@ -143,3 +144,57 @@ class CondensedMoELayer:
         L.luffy_route_bwd(self.layer, x, w_gate, self.dw, self.dx, self.dwg, s)
         T = self.T
         return dict(dx=self.dx[:T], dwg=self.dwg, dw1=self.dw1, dw2=self.dw2, dw3=self.dw3, dw=self.dw[:T])
+
+
+class HostStepper:
+    """Training steps of a layer fed from HOST (pinned) buffers, pipelined over three streams: the inputs
+    of step i+1 (X, dY) are uploaded on a copy stream while step i computes, and the output Y of step i is
+    downloaded on a second copy stream while its backward runs.  Every step copies its own inputs and its
+    result; device buffers are double-buffered and ordered with events (an upload waits for the backward
+    that last read its buffer, a forward waits for the download that last read its output buffer)."""
+
+    def __init__(self, layer: CondensedMoELayer, tokens: int):
+        dev, tdt, d = layer.device, layer.tdt, layer.d
+        self.layer, self.T, self.dev = layer, tokens, dev
+        self.x = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
+        self.dy = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
+        self.y = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        ev = lambda: [torch.cuda.Event() for _ in range(2)]
+        self.ev_in, self.ev_used, self.ev_y, self.ev_out = ev(), ev(), ev(), ev()
+
+    def run(self, batches, w_gate, w1, w2, w3=None, h: float = 0.9):
+        """batches: sequence of (host X, host dY, host Y out).  Returns when the last Y is on the host
+        side of the compute stream's order (callers time it with events on the current stream)."""
+        cs = torch.cuda.current_stream(self.dev)
+        batches = list(batches)
+        n, T = len(batches), self.T
+        start = torch.cuda.Event()
+        start.record(cs)
+
+        def upload(i):
+            b = i % 2
+            self.h2d.wait_event(start if i < 2 else self.ev_used[b])
+            with torch.cuda.stream(self.h2d):
+                self.x[b].copy_(batches[i][0], non_blocking=True)
+                self.dy[b].copy_(batches[i][1], non_blocking=True)
+            self.ev_in[b].record(self.h2d)
+
+        upload(0)
+        for i in range(n):
+            b = i % 2
+            if i + 1 < n:
+                upload(i + 1)
+            cs.wait_event(self.ev_in[b])
+            if i >= 2:
+                cs.wait_event(self.ev_out[b])
+            y = self.layer.forward(self.x[b][:T], w_gate, w1, w2, w3, h=h, out=self.y[b])
+            self.ev_y[b].record(cs)
+            self.d2h.wait_event(self.ev_y[b])
+            with torch.cuda.stream(self.d2h):
+                batches[i][2].copy_(y, non_blocking=True)
+            self.ev_out[b].record(self.d2h)
+            self.layer.backward(self.dy[b][:T], self.x[b][:T], w_gate, w1, w2, w3)
+            self.ev_used[b].record(cs)
+        cs.wait_event(self.ev_out[(n - 1) % 2])

@@ -211,3 +211,34 @@ def test_deterministic_bitwise():
     b = run_gpu_layer(C2S, inp, h=0.9, layer=a["layer"])
     for k in ("Y", "dx", "dwg", "dw1", "dw2", "rep", "idx"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_host_stepper_pipelined_steps():
+    """HostStepper (the e2e driver): three steps with DIFFERENT host inputs, uploads / downloads overlapped
+    with compute on two copy streams; every downloaded Y and the gradients of the last step equal the
+    device-resident path bitwise (the kernels are deterministic)."""
+    import torch
+    from paper_2411_15419_b200 import layer as LY
+    cfg = C2S
+    inps = [_inputs(cfg, rank=r) for r in range(3)]
+    T = inps[0]["X"].shape[0]
+    dev = torch.device("cuda")
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev, torch.bfloat16)
+    W1, W2, W3 = workload.make_expert_weights(cfg)
+    w1, w2 = bf(W1), bf(W2)
+    wg = torch.from_numpy(inps[0]["Wg"]).to(dev)
+    lay = LY.CondensedMoELayer(cfg.num_experts, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T, device=dev)
+    host = []
+    for inp in inps:
+        hx = torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True).copy_(bf(inp["X"]))
+        hdy = torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True).copy_(bf(inp["dY"]))
+        host.append((hx, hdy, torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True)))
+    LY.HostStepper(lay, T).run(host, wg, w1, w2, None, h=0.9)
+    torch.cuda.synchronize()
+    dw1_pipe = lay.dw1.clone()
+    for hx, hdy, hy in host:
+        y = lay.forward(hx.to(dev), wg, w1, w2, None, h=0.9)
+        assert torch.equal(hy.to(dev), y)
+    g = lay.backward(host[-1][1].to(dev), host[-1][0].to(dev), wg, w1, w2, None)
+    assert torch.equal(g["dw1"], dw1_pipe)
+    lay.close()

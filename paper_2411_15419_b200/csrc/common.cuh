@@ -127,17 +127,19 @@ __device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& dg) {
 // the bf16 resolution of the stored activation -- so GeLU and GeLU' cost ~17 instructions instead of erff's
 // two-range polynomial plus a second exponential.
 __device__ __forceinline__ void gelu_and_grad_as(float x, float& g, float& dg) {
-  const float ax = fabsf(x);
-  const float phi = 0.3989422804014327f * __expf(-0.5f * x * x);
-  const float t = __fdividef(1.f, fmaf(0.2316419f, ax, 1.f));
-  float poly = fmaf(t, 1.330274429f, -1.821255978f);
-  poly = fmaf(t, poly, 1.781477937f);
-  poly = fmaf(t, poly, -0.356563782f);
-  poly = fmaf(t, poly, 0.319381530f);
-  const float q = phi * poly * t;  // upper tail Q(|x|) = 1 - Phi(|x|)
+  // e = exp(-x^2/2) = 2^(x * (x * -log2(e)/2)); MUFU ex2 / rcp without range fix-ups (ftz: only values
+  // below 1e-38 are affected); 1/sqrt(2 pi) is folded into the polynomial coefficients
+  float e, t;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * (x * -0.72134752044448170368f)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.2316419f, fabsf(x), 1.f)));
+  float poly = fmaf(t, 0.3989422804014327f * 1.330274429f, 0.3989422804014327f * -1.821255978f);
+  poly = fmaf(t, poly, 0.3989422804014327f * 1.781477937f);
+  poly = fmaf(t, poly, 0.3989422804014327f * -0.356563782f);
+  poly = fmaf(t, poly, 0.3989422804014327f * 0.319381530f);
+  const float q = e * (poly * t);  // upper tail Q(|x|) = 1 - Phi(|x|) = phi(|x|) (b1 t + ... + b5 t^5)
   const float cdf = x >= 0.f ? 1.f - q : q;
   g = x * cdf;
-  dg = fmaf(x, phi, cdf);
+  dg = fmaf(x * 0.3989422804014327f, e, cdf);  // Phi(x) + x phi(x)
 }
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + expf(-x)); }
 __device__ __forceinline__ float silu_grad_f(float x) {

@@ -104,6 +104,24 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _bind_local_cpus(dev: int):
+    """Pin this process to the CPUs NVML reports as local to the GPU (first-touch placement of the pinned
+    host buffers on the GPU's NUMA node); no-op when NVML or the affinity call is unavailable."""
+    if os.environ.get("LUFFY_NO_CPU_BIND"):
+        return
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, wd in enumerate(words) for b in range(64) if (wd >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception:
+        pass
+
+
 def cpu_oracle_step(cfg, inp, ntok: int):
     """The oracle (as it stands) on a bounded sample: fwd+bwd of the first `ntok` tokens."""
     from oracle import luffy_oracle as O
@@ -199,6 +217,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    _bind_local_cpus(local)  # host buffers of the e2e path land on the GPU's NUMA node
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     E, El = cfg.num_experts, cfg.num_experts // world

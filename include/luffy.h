@@ -295,6 +295,12 @@ LUFFY_API luffy_status luffy_plan_migration(const luffy_migration_problem* prob,
 /* Eq. (1): 3*B*L*d^2 + 2*B*L^2*d (P := 1), exact int64. */
 LUFFY_API int64_t luffy_attention_cost(int64_t B, int64_t L, int64_t d);
 
+/* Adaptive condensation threshold, Eq. (2), P:384-387 (the step before the hot path; the layer takes h as
+ * an argument): h_t = c / (1 + exp(l_norm)), l_norm = max(0, (l_ini - l_prev) / l_ini), with c = 1 as
+ * printed (h in (0.269, 0.5]) or, reading R17b, c = 2 (h in [0.538, 1], the range the paper's narrative and
+ * Table IV imply).  scale2 selects c = 2.  Host, pure; LUFFY_E_INVALID for l_ini <= 0 or non-finite inputs. */
+LUFFY_API luffy_status luffy_adaptive_threshold(double l_ini, double l_prev, int32_t scale2, float* h_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,7 @@
 // replaced by a replicated deterministic computation overlapped with the expert GEMMs).
 // Exact int64 arithmetic; P (GPU speed) := 1 because it cancels on a homogeneous B200 box (R16).
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <numeric>
 #include <vector>
@@ -113,5 +114,14 @@ extern "C" luffy_status luffy_plan_migration(const luffy_migration_problem* prob
       for (int r = 0; r < P; ++r)
         if (r != seq_dest[i]) combine_bytes[(size_t)r * P + seq_dest[i]] += prob->rows_at[(size_t)i * P + r] * prob->row_bytes;
   }
+  return LUFFY_OK;
+}
+
+extern "C" luffy_status luffy_adaptive_threshold(double l_ini, double l_prev, int32_t scale2, float* h_out) {
+  if (!h_out) return luffy::fail(LUFFY_E_INVALID, "adaptive_threshold: h_out is NULL");
+  if (!(l_ini > 0.0) || !std::isfinite(l_ini) || !std::isfinite(l_prev))
+    return luffy::fail(LUFFY_E_INVALID, "adaptive_threshold: l_ini must be > 0 and both losses finite");
+  const double l_norm = std::max(0.0, (l_ini - l_prev) / l_ini);
+  *h_out = (float)((scale2 ? 2.0 : 1.0) / (1.0 + std::exp(l_norm)));
   return LUFFY_OK;
 }

@@ -26,7 +26,7 @@ EXPORTED = [
     "luffy_layer_rows", "luffy_route", "luffy_condense", "luffy_dispatch", "luffy_expert_ffn",
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
-    "luffy_attention_cost", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
+    "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -93,6 +93,7 @@ def _load():
         "luffy_route_bwd": (I32, [P, P, P, P, P, P, P]),
         "luffy_plan_migration": (I32, [ctypes.POINTER(MigrationProblem), P, P]),
         "luffy_attention_cost": (I64, [I64, I64, I64]),
+        "luffy_adaptive_threshold": (I32, [ctypes.c_double, ctypes.c_double, I32, P]),
         "luffy_debug_copy": (I32, [P, I32, P, ctypes.POINTER(SZ), P]),
         "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
@@ -259,6 +260,14 @@ def luffy_plan_migration(seq_len, rows_at, q, row_bytes, d_model, capacity_token
 
 def luffy_attention_cost(B, L, d) -> int:
     return LIB.luffy_attention_cost(int(B), int(L), int(d))
+
+
+def luffy_adaptive_threshold(l_ini: float, l_prev: float, scale2: bool = False) -> float:
+    """Eq. (2): the condensation threshold of the next iteration from the first and the previous
+    loss; scale2 selects the factor-2 reading R17b."""
+    h = ctypes.c_float(0.0)
+    _check(LIB.luffy_adaptive_threshold(float(l_ini), float(l_prev), int(bool(scale2)), ctypes.byref(h)))
+    return h.value
 
 
 DBG = dict(gcnt=(0, np.int32), goff=(1, np.int32), gtok=(2, np.int32), adjoff=(3, np.int64), adj=(4, np.uint32),

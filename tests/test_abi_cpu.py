@@ -109,3 +109,29 @@ def test_every_kernel_enters_through_pdl():
             assert body.startswith("pdl_enter();"), f"{fn}: kernel at offset {m.start()} does not start with pdl_enter()"
             kernels += 1
     assert kernels >= 30
+
+
+def test_adaptive_threshold_eq2(L):
+    """Eq. (2) in the library: as printed it equals the oracle and the worked values; the factor-2
+    reading R17b doubles it (range [2/(1+e), 1]); h decreases as the loss falls; invalid inputs raise."""
+    rows = [ln.split() for ln in open(os.path.join(ROOT, "tests", "golden", "eq2_adaptive_threshold.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    for l_ini, l_prev, want in rows:
+        h = L.luffy_adaptive_threshold(float(l_ini), float(l_prev))
+        assert abs(h - float(want)) < 5e-6
+    rng = np.random.default_rng(7)
+    prev_h = None
+    for l_prev in np.linspace(12.0, 0.0, 25):
+        h1 = L.luffy_adaptive_threshold(10.0, l_prev)
+        h2 = L.luffy_adaptive_threshold(10.0, l_prev, scale2=True)
+        assert abs(h1 - O.adaptive_threshold(10.0, l_prev)) < 1e-6
+        assert abs(h2 - 2 * h1) < 1e-6 and 2 / (1 + np.e) - 1e-6 <= h2 <= 1.0
+        if prev_h is not None:
+            assert h1 <= prev_h + 1e-7
+        prev_h = h1
+    for l_ini, l_prev in rng.uniform(0.1, 20.0, size=(50, 2)):
+        assert abs(L.luffy_adaptive_threshold(l_ini, l_prev) - O.adaptive_threshold(l_ini, l_prev)) < 1e-6
+    with pytest.raises(L.LuffyError):
+        L.luffy_adaptive_threshold(0.0, 1.0)
+    with pytest.raises(L.LuffyError):
+        L.luffy_adaptive_threshold(1.0, float("nan"))

@@ -235,8 +235,10 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
 }
 
 // Word offsets of each group's adjacency: sum over groups of npad^2 / 32.
-__global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff) {
+__global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff,
+                                   uint32_t* __restrict__ ctrl) {
   pdl_enter();
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     int64_t o = 0;
     for (int e = 0; e < E; ++e) {
@@ -490,7 +492,7 @@ int launch_identity_rep(luffy_layer* L, void* s) {
 
 int launch_gram_simt(luffy_layer* L, float h, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(adj_offsets_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff);
+  launch_pdl(adj_offsets_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff, L->ctrl);
   LUFFY_LAUNCHED();
   const int64_t nt = L->Cpad_max / 64;
   const int64_t tiles = nt * (nt + 1) / 2;  // upper bound over any split of the rows into groups

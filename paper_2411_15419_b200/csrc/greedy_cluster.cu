@@ -278,7 +278,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   const size_t cache_bytes = std::min<size_t>(224 * 1024 - state, 96 * 1024) / 16 * 16;  // own-row cache
   const size_t smem = state + cache_bytes;
   const int cache_words = (int)(cache_bytes / 4);
-  LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * 64, st));
+  // (the control block is zeroed by the adjacency-offsets kernel that precedes the Gram)
   static int cs = 0;  // cluster size: 16 (non-portable) when the device accepts it, else 8
   static int ncl = 0;  // co-resident clusters of that size (groups are scheduled onto them)
   if (cs == 0) {

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ mcnt, int32_t* __restrict__ mcur,
                                                       int32_t* __restrict__ marr,
                                                       int32_t* __restrict__ members, int32_t* __restrict__ mslot,
-                                                      int cur_cap) {
+                                                      int32_t* __restrict__ rep_out, int cur_cap) {
   pdl_enter();
   extern __shared__ int cur_smem[];
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
       if (idx[(size_t)t * k + j] == e) jj = j;
     pos[(size_t)t * k + jj] = lslot[r];
     rep[(size_t)t * k + jj] = gtok[r];
+    if (rep_out) rep_out[(size_t)t * k + jj] = gtok[r];
   }
   // ---- member CSR of every slot of this expert, members in token (= group row) order, stored in the
   // group-row space [g0, g0 + n) (padding rows of the space hold -1): mstart[slot], mcnt[slot],
@@ -503,11 +504,9 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
   }
   launch_pdl(layout_kernel, L->E, 1024, cur_cap * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
-                                                 L->mcnt, L->mcur, L->marr, L->members, L->mslot, cur_cap);
+                                                 L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out, cur_cap);
   LUFFY_LAUNCHED();
-  if (rep_out) {
-    LUFFY_CUDA_TRY(cudaMemcpyAsync(rep_out, L->rep, sizeof(int32_t) * L->T * L->k, cudaMemcpyDeviceToDevice, st));
-  }
+
   if (dst_rows) {
     const int blocks = grid_for_warps(L->Rpad_max);
     if (L->dtype == LUFFY_BF16)

@@ -39,7 +39,8 @@ int gemm_rows_simt(int dtype, int epi, const void* A, const void* B, const void*
 int gemm_wgrad_simt(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G,
                     int M, int N, int lda, int ldb, void* s);
 int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
-                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s);
+                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s,
+                 const XWaitRows* wr = nullptr);
 int gemm_wgrad_tc(const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M, int N,
                   int lda, int ldb, int64_t max_rows, void* s);
 int launch_pack_rows(luffy_layer* L, const void* x, void* dst_rows, void* s);
@@ -189,8 +190,8 @@ luffy_status validate(const luffy_config* c) {
 // bf16: tcgen05 tensor cores; fp32: exact SIMT FFMA (tf32 would break the fp32 tolerance).
 int gemm_rows(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off,
               int G, int64_t max_rows, int N, int K, int b_kmajor, void* s, const XRedirect* rd = nullptr,
-              const XSignal* sig = nullptr) {
-  if (dtype == LUFFY_BF16) return gemm_rows_tc(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, s);
+              const XSignal* sig = nullptr, const XWaitRows* wr = nullptr) {
+  if (dtype == LUFFY_BF16) return gemm_rows_tc(epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, s, wr);
   return gemm_rows_simt(dtype, epi, A, B, B3, D, aux0, off, G, max_rows, N, K, b_kmajor, rd, sig, s);
 }
 int gemm_wgrad(int dtype, const void* A, const void* B, float* D, float* D3, int Msplit, const int32_t* off, int G, int M,
@@ -631,11 +632,26 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
     rd.stride = L->Rpad_max;
     sig = make_signal(L, XP_COMB);
   }
+  // fused dispatch (bf16): GEMM1 waits per tile for the source ranks of its rows (see launch_xdispatch)
+  XWaitRows wr{};
+  const bool tile_wait = L->P > 1 && L->dtype == LUFFY_BF16;
+  if (tile_wait) {
+    wr.flags = L->x_flags + XP_DISP * L->P;
+    wr.seq = L->seq;
+    wr.P = L->P;
+    wr.E = L->E;
+    wr.El = L->El;
+    wr.me = L->rank;
+    wr.cnt_all = L->cnt_all;
+    wr.roff = L->roff;
+  }
   if (L->act == LUFFY_GELU) {
-    LUFFY_CHECK(gemm_rows(L->dtype, EPI_GELU, recv, w1, nullptr, saved_act, saved_pre, off, L->El, rows, L->f, L->d, 1, stream),
+    LUFFY_CHECK(gemm_rows(L->dtype, EPI_GELU, recv, w1, nullptr, saved_act, saved_pre, off, L->El, rows, L->f, L->d, 1, stream,
+                          nullptr, nullptr, tile_wait ? &wr : nullptr),
                 "expert_ffn/gemm1");
   } else {
-    LUFFY_CHECK(gemm_rows(L->dtype, EPI_SWIGLU, recv, w1, w3, saved_act, saved_pre, off, L->El, rows, 2 * L->f, L->d, 1, stream),
+    LUFFY_CHECK(gemm_rows(L->dtype, EPI_SWIGLU, recv, w1, w3, saved_act, saved_pre, off, L->El, rows, 2 * L->f, L->d, 1, stream,
+                          nullptr, nullptr, tile_wait ? &wr : nullptr),
                 "expert_ffn/gemm1");
   }
   LUFFY_CHECK(gemm_rows(L->dtype, EPI_STORE, saved_act, w2, nullptr, out, nullptr, off, L->El, rows, L->d, L->f, 1, stream,

@@ -236,6 +236,9 @@ int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
                                                      L->El, L->d, L->x_peer_recv + par * L->P, make_signal(L, XP_DISP),
                                                      L->mig ? L->dmask : nullptr, L->x_peer_rowmask, L->rank);
   LUFFY_LAUNCHED();
+  // bf16: the expert FFN's GEMM1 waits per tile for the source ranks of its rows (fused dispatch, exchange.cuh
+  // XWaitRows); the fp32 SIMT path waits here for every rank
+  if (L->dtype == LUFFY_BF16) return 0;
   return launch_xwait(L, XP_DISP, s);
 }
 

@@ -69,4 +69,34 @@ __device__ __forceinline__ void xsignal_done(const XSignal& s) {
 
 XSignal make_signal(const luffy_layer* L, int phase);
 
+// Tile-level wait for dispatched rows (fused dispatch -> GEMM1): a consumer of rows [r0, r1) of local
+// expert el waits only for the source ranks whose rows fall in that range (flags[q] >= seq, published by
+// q's pack-and-push kernel), instead of a stream-wide wait for every rank.
+struct XWaitRows {
+  const uint32_t* flags;   // [P] this rank's XP_DISP flags (one per source rank)
+  uint32_t seq;
+  int P, E, El, me;
+  const int32_t* cnt_all;  // [P][E] rows each source sends to each expert
+  const int32_t* roff;     // [El+1] expert-layout offsets of the local experts
+};
+__device__ __forceinline__ void xwait_rows(const XWaitRows& w, int el, int r0, int r1) {
+  const int e = w.me * w.El + el;
+  int base = w.roff[el];
+  for (int q = 0; q < w.P; ++q) {
+    const int n = w.cnt_all[q * w.E + e];
+    if (n > 0 && base < r1 && base + n > r0) {
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while (ld_acquire_sys(w.flags + q) < w.seq) {
+        __nanosleep(32);
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 20000000000ull) __trap();
+      }
+    }
+    base += n;
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written rows -> TMA (async proxy) reads
+}
+
 }  // namespace luffy

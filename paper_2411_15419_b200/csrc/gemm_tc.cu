@@ -54,6 +54,8 @@ struct TcArgs {
   XRedirect rd;
   int has_sig;         // publish completion to the peers when the kernel ends
   XSignal sig;
+  int has_wr;          // fused dispatch: wait per tile for the source ranks of its A rows
+  XWaitRows wr;
 };
 
 struct Tile {
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       for (int t = tile0; t < ntiles; t += tstride) {
         const Tile x = decode<EPI, WG, CG>(t, a, off_s);
+        if (!WG && a.has_wr) xwait_rows(a.wr, x.g, x.m0 + hm, min(x.m0 + hm + BM, x.mlim));
         for (int kb = 0; kb < x.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* dA = sA + stage * A_BYTES;
@@ -628,9 +631,14 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
 
 // Rows GEMM: D[r, :] over expert segments; see luffy_internal.h (Epi) for the epilogues.
 int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D, void* aux0, const int32_t* off, int G,
-                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s) {
+                 int64_t max_rows, int N, int K, int b_kmajor, const XRedirect* rd, const XSignal* sig, void* s,
+                 const XWaitRows* wr) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   TcArgs a{};
+  if (wr) {
+    a.has_wr = 1;
+    a.wr = *wr;
+  }
   if (rd) {
     a.has_rd = 1;
     a.rd = *rd;

@@ -242,3 +242,17 @@ def test_host_stepper_pipelined_steps():
     g = lay.backward(host[-1][1].to(dev), host[-1][0].to(dev), wg, w1, w2, None)
     assert torch.equal(g["dw1"], dw1_pipe)
     lay.close()
+
+
+def test_grid_greedy_fallback_large_capacity():
+    """A layer sized for 16384 tokens keeps its group state beyond the cluster kernel's shared memory, so
+    representative selection runs on the cooperative grid kernel: same parity bar on a 1024-token batch."""
+    from paper_2411_15419_b200 import layer as LY
+    inp = _inputs(C2S)
+    lay = LY.CondensedMoELayer(C2S.num_experts, C2S.top_k, C2S.d_model, C2S.d_ffn, max_tokens=16384,
+                               dtype=C2S.dtype, act=C2S.act)
+    res = run_gpu_layer(C2S, inp, h=0.9, layer=lay)
+    _check_route(C2S, inp, res)
+    _check_condense(C2S, inp, res, 0.9)
+    _check_layout(C2S, inp, res)
+    _check_numerics(C2S, inp, res, 0.9)

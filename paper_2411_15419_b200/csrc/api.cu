@@ -121,6 +121,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->win = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);
   o->nrep = cv.take<int32_t>(m.E);
+  o->gnrep = cv.take<int32_t>(m.E);
   o->soff = cv.take<int32_t>(m.E + 1);
   o->lslot = cv.take<int32_t>(m.Cpad);
   o->perm = cv.take<int32_t>(m.Rpad);

@@ -33,12 +33,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       const uint32_t* __restrict__ adj,
                                                                       int32_t* __restrict__ rep_local,
                                                                       uint32_t* __restrict__ ctrl, int nmax,
-                                                                      int max_rounds, int cache_words, int E) {
+                                                                      int max_rounds, int cache_words, int E,
+                                                                      int32_t* __restrict__ gnrep) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t gsm[];
   __shared__ int order_s[LUFFY_MAX_EXPERTS];
   __shared__ int list_s[LUFFY_MAX_EXPERTS];
-  __shared__ int nlist_s, largest_s;
+  __shared__ int nlist_s, largest_s, nrep_s;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
@@ -237,6 +238,17 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   max_round = max(max_round, round);
   cluster.sync();  // the replicas are reused by the next group, and no CTA may exit while a peer can still
                    // read its shared memory
+  if (rank == 0) {  // publish the group's representative count (read by the layout for the send offsets)
+    if (threadIdx.x == 0) nrep_s = 0;
+    __syncthreads();
+    int c = 0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) c += rep_local[g0 + r] == g0 + r;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && c) atomicAdd(&nrep_s, c);
+    __syncthreads();
+    if (threadIdx.x == 0) gnrep[e] = nrep_s;
+    __syncthreads();
+  }
   }
   if (rank == 0 && threadIdx.x == 0) atomicMax(ctrl + 2, (uint32_t)max_round);
 }
@@ -262,7 +274,7 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int n
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
-                                    kGreedyMaxRounds, cache_words, L->E));
+                                    kGreedyMaxRounds, cache_words, L->E, L->gnrep));
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -57,6 +57,8 @@ struct luffy_layer {
   uint32_t* ctrl;     // [64 + kGreedyMaxRounds] grid barrier + per-round counters
   // ---- pack / layout
   int32_t* nrep;      // [E] representatives per expert
+  int32_t* gnrep;     // [E] representatives per group, published by representative selection
+  bool gnrep_valid;   // set when the selection kernel of this step published gnrep
   int32_t* soff;      // [E+1] padded send offsets
   int32_t* lslot;     // [Cpad_max] slot of a group row that is a representative (-1 otherwise)
   int32_t* perm;      // [Rpad_max] slot -> token (-1 = padding)

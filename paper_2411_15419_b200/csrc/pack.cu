@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ mcnt, int32_t* __restrict__ mcur,
                                                       int32_t* __restrict__ marr,
                                                       int32_t* __restrict__ members, int32_t* __restrict__ mslot,
-                                                      int32_t* __restrict__ rep_out, int cur_cap) {
+                                                      int32_t* __restrict__ rep_out,
+                                                      const int32_t* __restrict__ gnrep, int cur_cap) {
   pdl_enter();
   extern __shared__ int cur_smem[];
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
@@ -94,9 +95,13 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
     if (i < E) cnt[i] = 0;
   }
   __syncthreads();
-  const int rows = goff_s[E];
-  for (int g = threadIdx.x; g < rows; g += blockDim.x)
-    if (rep_local[g] == g) atomicAdd(&cnt[find_group(goff_s, E, g)], 1);
+  if (gnrep) {  // published by the representative selection of this step
+    for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = gnrep[i];
+  } else {
+    const int rows = goff_s[E];
+    for (int g = threadIdx.x; g < rows; g += blockDim.x)
+      if (rep_local[g] == g) atomicAdd(&cnt[find_group(goff_s, E, g)], 1);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     offs[0] = 0;
@@ -504,7 +509,8 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
   }
   launch_pdl(layout_kernel, L->E, 1024, cur_cap * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
-                                                 L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out, cur_cap);
+                                                 L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out,
+                                                 L->gnrep_valid ? L->gnrep : nullptr, cur_cap);
   LUFFY_LAUNCHED();
 
   if (dst_rows) {

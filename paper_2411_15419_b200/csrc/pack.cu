@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
     int b = 0;
-    for (int w = 0; w < nwb; ++w) {  // warps claim their runs in order: stable across the block
+    const int nwv = min(nwb, (n - c0 + 31) >> 5);  // warps holding rows of this chunk (uniform)
+    for (int w = 0; w < nwv; ++w) {  // warps claim their runs in order: stable across the block
       if (wid == w && valid && lane == leader) {
         b = cur[key];
         cur[key] = b + __popc(peers);

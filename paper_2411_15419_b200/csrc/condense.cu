@@ -100,8 +100,21 @@ __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __rest
 template <typename T>
 __global__ void __launch_bounds__(256) gather_norm_kernel(const T* __restrict__ x, const int32_t* __restrict__ gtok,
                                                           const int32_t* __restrict__ goff, int E, int d,
-                                                          T* __restrict__ xg, double* __restrict__ gnorm) {
+                                                          T* __restrict__ xg, double* __restrict__ gnorm,
+                                                          int64_t* __restrict__ adjoff, uint32_t* __restrict__ ctrl) {
   pdl_enter();
+  if (blockIdx.x == 0) {  // also: word offsets of each group's adjacency (sum of npad^2 / 32) and the greedy
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // control block reset
+    if (threadIdx.x == 0) {
+      int64_t o = 0;
+      for (int e = 0; e < E; ++e) {
+        adjoff[e] = o;
+        const int64_t np = goff[e + 1] - goff[e];
+        o += np * np / 32;
+      }
+      adjoff[E] = o;
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int64_t rows = goff[E];
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -231,22 +244,6 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
       word |= (uint32_t)v << b;
     }
     base[(size_t)(I * TS + r) * W + I * 2 + h] = word;
-  }
-}
-
-// Word offsets of each group's adjacency: sum over groups of npad^2 / 32.
-__global__ void adj_offsets_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff,
-                                   uint32_t* __restrict__ ctrl) {
-  pdl_enter();
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int64_t o = 0;
-    for (int e = 0; e < E; ++e) {
-      adjoff[e] = o;
-      const int64_t np = goff[e + 1] - goff[e];
-      o += np * np / 32;
-    }
-    adjoff[E] = o;
   }
 }
 
@@ -478,10 +475,10 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
   int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);
   if (L->dtype == LUFFY_BF16)
     launch_pdl(gather_norm_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->gtok, L->goff, L->E, L->d,
-                                                     static_cast<bf16*>(L->xg), L->gnorm);
+                                                     static_cast<bf16*>(L->xg), L->gnorm, L->adjoff, L->ctrl);
   else
     launch_pdl(gather_norm_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->gtok, L->goff, L->E, L->d,
-                                                      static_cast<float*>(L->xg), L->gnorm);
+                                                      static_cast<float*>(L->xg), L->gnorm, L->adjoff, L->ctrl);
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -496,8 +493,6 @@ int launch_identity_rep(luffy_layer* L, void* s) {
 
 int launch_gram_simt(luffy_layer* L, float h, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(adj_offsets_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff, L->ctrl);
-  LUFFY_LAUNCHED();
   const int64_t nt = L->Cpad_max / 64;
   const int64_t tiles = nt * (nt + 1) / 2;  // upper bound over any split of the rows into groups
   const double c2h = 2.0 * (double)h - 1.0;

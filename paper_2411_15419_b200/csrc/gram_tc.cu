@@ -252,21 +252,6 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   if (warp == 1) tc::tmem_dealloc_pair(tmem_base, 512);
 }
 
-__global__ void adj_offsets_tc_kernel(const int32_t* __restrict__ goff, int E, int64_t* __restrict__ adjoff,
-                                      uint32_t* __restrict__ ctrl) {
-  pdl_enter();
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block (rounds, stamps)
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int64_t o = 0;
-    for (int e = 0; e < E; ++e) {
-      adjoff[e] = o;
-      const int64_t np = goff[e + 1] - goff[e];
-      o += np * np / 32;
-    }
-    adjoff[E] = o;
-  }
-}
-
 }  // namespace
 
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
@@ -274,8 +259,7 @@ int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t out
 
 int launch_gram_tc(luffy_layer* L, float h, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(adj_offsets_tc_kernel, 1, 32, 0, st, L->goff, L->E, L->adjoff, L->ctrl);
-  LUFFY_LAUNCHED();
+  // (adjoff and the greedy control block are prepared by gather_norm_kernel)
   CUtensorMap tx;
   LUFFY_CUDA_TRY(make_tmap_bf16(&tx, L->xg, L->d, L->Cpad_max, L->d, TS));
   GramArgs a;

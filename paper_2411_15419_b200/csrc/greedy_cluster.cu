@@ -290,49 +290,48 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   const size_t cache_bytes = std::min<size_t>(224 * 1024 - state, 96 * 1024) / 16 * 16;  // own-row cache
   const size_t smem = state + cache_bytes;
   const int cache_words = (int)(cache_bytes / 4);
-  // (the control block is zeroed by the adjacency-offsets kernel that precedes the Gram)
-  static int cs = 0;  // cluster size: 16 (non-portable) when the device accepts it, else 8
-  static int ncl = 0;  // co-resident clusters of that size (groups are scheduled onto them)
+  // (the control block is zeroed by gather_norm_kernel, which precedes the Gram)
+  // Cluster size: 16 CTAs when every group gets its own co-resident cluster, else 8 (twice as many clusters;
+  // the groups are scheduled by cost onto them).  On B200 only 7 clusters of 16 (or of 12) and 15 of 8 fit.
+  static int cs = 0, ncl = 0;
   if (cs == 0) {
-    cs = 16;
-    cudaFuncSetAttribute(greedy_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(greedy_cluster_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(16);
-    cfg.blockDim = dim3(GC_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 16;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, greedy_cluster_kernel<16>, &cfg) != cudaSuccess || nclusters < 1) cs = 8;
-    cudaGetLastError();
-    ncl = nclusters;
-    if (cs == 8) {
-      cudaFuncSetAttribute(greedy_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cfg.gridDim = dim3(8);
-      attr[0].val.clusterDim.x = 8;
-      if (cudaOccupancyMaxActiveClusters(&ncl, greedy_cluster_kernel<8>, &cfg) != cudaSuccess || ncl < 1) ncl = 1;
+    auto coresident = [&](auto kern, int size) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(size);
+      cfg.blockDim = dim3(GC_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = size;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
       cudaGetLastError();
-      cfg.gridDim = dim3(16);
-      attr[0].val.clusterDim.x = 16;
-    }
-    if (std::getenv("LUFFY_VERBOSE")) {
-      int n8 = 0;
-      cudaFuncSetAttribute(greedy_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cfg.gridDim = dim3(8);
-      attr[0].val.clusterDim.x = 8;
-      cudaOccupancyMaxActiveClusters(&n8, greedy_cluster_kernel<8>, &cfg);
-      cudaGetLastError();
-      std::fprintf(stderr, "[luffy] greedy clusters co-resident: %d of 16 CTAs, %d of 8 CTAs (smem %zu)\n", nclusters, n8, smem);
-    }
+      return n;
+    };
+    const int n16 = coresident(greedy_cluster_kernel<16>, 16);
+    const int n12 = coresident(greedy_cluster_kernel<12>, 12);
+    const int n8 = coresident(greedy_cluster_kernel<8>, 8);
+    const char* force = std::getenv("LUFFY_GREEDY_CS");  // experiments: 16 / 12 / 8
+    const int f = force ? std::atoi(force) : 0;
+    if (f == 16 && n16 >= 1) { cs = 16; ncl = n16; }
+    else if (f == 12 && n12 >= 1) { cs = 12; ncl = n12; }
+    else if (f == 8 && n8 >= 1) { cs = 8; ncl = n8; }
+    else if (n16 >= L->E) { cs = 16; ncl = n16; }  // every group on its own 16-CTA cluster
+    else if (n8 >= 1) { cs = 8; ncl = n8; }         // more groups than clusters: twice as many clusters
+    else { cs = 16; ncl = std::max(1, n16); }       // (measured: C2 44 us either way, C4 55 vs 69 us)
+    if (std::getenv("LUFFY_VERBOSE"))
+      std::fprintf(stderr, "[luffy] greedy clusters co-resident: %d x16, %d x12, %d x8 CTAs (smem %zu); using %d x %d\n",
+                   n16, n12, n8, smem, ncl, cs);
   }
-  return cs == 16 ? launch_cluster<16>(L, nmax, smem, cache_words, ncl, st)
-                  : launch_cluster<8>(L, nmax, smem, cache_words, ncl, st);
+  if (cs == 16) return launch_cluster<16>(L, nmax, smem, cache_words, ncl, st);
+  if (cs == 12) return launch_cluster<12>(L, nmax, smem, cache_words, ncl, st);
+  return launch_cluster<8>(L, nmax, smem, cache_words, ncl, st);
 }
 
 }  // namespace luffy

@@ -256,3 +256,17 @@ def test_grid_greedy_fallback_large_capacity():
     _check_condense(C2S, inp, res, 0.9)
     _check_layout(C2S, inp, res)
     _check_numerics(C2S, inp, res, 0.9)
+
+
+@pytest.mark.parametrize("num_experts,top_k,d_model,dtype", [(8, 4, 512, "bf16"), (64, 2, 256, "bf16"),
+                                                             (16, 3, 256, "fp32")])
+def test_wider_routing(num_experts, top_k, d_model, dtype):
+    """Top-k above 2 and E above 32 (the generic gate kernel), on the full parity bar."""
+    cfg = dataclasses.replace(C2S, num_experts=num_experts, top_k=top_k, d_model=d_model, d_ffn=2 * d_model,
+                              dtype=dtype, seqs_per_rank=2, seq_len=512)
+    inp = _inputs(cfg)
+    res = run_gpu_layer(cfg, inp, h=0.9)
+    _check_route(cfg, inp, res)
+    _check_condense(cfg, inp, res, 0.9)
+    _check_layout(cfg, inp, res)
+    _check_numerics(cfg, inp, res, 0.9)

@@ -229,27 +229,16 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ x,
   }
 }
 
-template <typename T>
+// y[t] = sum_j w[t, j] * gathered[pos(t, j)] (j in order, fp32): one warp per token, the token's k slots
+// and weights read once (lanes < k), every row load of a 512-column block issued before the arithmetic.
+template <typename T, int KM>
 __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ pos,
                                                          const float* __restrict__ w, int T_, int k, int d,
-                                                         T* __restrict__ y) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
-    for (int c = lane * 8; c < d; c += 256) {
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < k; ++j) {
-        const float wj = w[(size_t)t * k + j];
-        float v[8];
-        load8(gathered + (size_t)pos[(size_t)t * k + j] * d + c, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(wj, v[i], acc[i]);
-      }
-      store8(y + (size_t)t * d + c, acc);
-    }
-  }
-}
+                                                         T* __restrict__ y);
+template <typename T, int KM>
+__global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ dsend, const int32_t* __restrict__ pos,
+                                                         const int32_t* __restrict__ rep, int T_, int k, int d,
+                                                         T* __restrict__ dx);
 
 // d_gathered[slot] = sum_{members m of the slot, token order} gw[m] * dy[gtok[m]]; padding -> 0.
 //
@@ -471,24 +460,98 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
 }
 
 // dx[t] = sum_{j : rep(t, j) == t} d_send[pos_tj]   (condensed copies get no expert-path gradient, R11)
-template <typename T>
+template <typename T, int KM>
 __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ dsend, const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ rep, int T_, int k, int d,
                                                          T* __restrict__ dx) {
   pdl_enter();
+  using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
+  constexpr int HC = KM <= 2 ? 2 : 1;  // 256-column chunks per load batch
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
-    for (int c = lane * 8; c < d; c += 256) {
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < k; ++j) {
-        if (rep[(size_t)t * k + j] != t) continue;
-        float v[8];
-        load8(dsend + (size_t)pos[(size_t)t * k + j] * d + c, v);
+    int my_pos = -1;
+    if (lane < k && rep[(size_t)t * k + lane] == t) my_pos = pos[(size_t)t * k + lane];
+    int row[KM];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    for (int j = 0; j < KM; ++j) row[j] = __shfl_sync(0xffffffffu, my_pos, j);
+    for (int c0 = 0; c0 < d; c0 += 256 * HC) {
+      R raw[HC][KM];
+#pragma unroll
+      for (int h = 0; h < HC; ++h)
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          const int c = c0 + h * 256 + lane * 8;
+          raw[h][j] = (j < k && row[j] >= 0 && c < d) ? ldraw8(dsend + (size_t)row[j] * d + c) : R{};
+        }
+#pragma unroll
+      for (int h = 0; h < HC; ++h) {
+        const int c = c0 + h * 256 + lane * 8;
+        if (c >= d) break;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          if (j < k && row[j] >= 0) {
+            float v[8];
+            cvt8(raw[h][j], v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += v[i];
+          }
+        }
+        store8(dx + (size_t)t * d + c, acc);
       }
-      store8(dx + (size_t)t * d + c, acc);
+    }
+  }
+}
+
+template <typename T, int KM>
+__global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ pos,
+                                                         const float* __restrict__ w, int T_, int k, int d,
+                                                         T* __restrict__ y) {
+  pdl_enter();
+  using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
+  constexpr int HC = KM <= 2 ? 2 : 1;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += nw) {
+    int my_pos = 0;
+    float my_w = 0.f;
+    if (lane < k) {
+      my_pos = pos[(size_t)t * k + lane];
+      my_w = w[(size_t)t * k + lane];
+    }
+    int row[KM];
+    float wt[KM];
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      row[j] = __shfl_sync(0xffffffffu, my_pos, j);
+      wt[j] = __shfl_sync(0xffffffffu, my_w, j);
+    }
+    for (int c0 = 0; c0 < d; c0 += 256 * HC) {
+      R raw[HC][KM];
+#pragma unroll
+      for (int h = 0; h < HC; ++h)
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          const int c = c0 + h * 256 + lane * 8;
+          raw[h][j] = (j < k && c < d) ? ldraw8(gathered + (size_t)row[j] * d + c) : R{};
+        }
+#pragma unroll
+      for (int h = 0; h < HC; ++h) {
+        const int c = c0 + h * 256 + lane * 8;
+        if (c >= d) break;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          if (j < k) {
+            float v[8];
+            cvt8(raw[h][j], v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = fmaf(wt[j], v[i], acc[i]);
+          }
+        }
+        store8(y + (size_t)t * d + c, acc);
+      }
     }
   }
 }
@@ -544,10 +607,10 @@ int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void*
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
-    launch_pdl(uncondense_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(gathered), L->pos, L->w, L->T, L->k, L->d,
+    launch_pdl(L->k <= 2 ? uncondense_kernel<bf16, 2> : uncondense_kernel<bf16, 8>, blocks, 256, 0, st, static_cast<const bf16*>(gathered), L->pos, L->w, L->T, L->k, L->d,
                                                     static_cast<bf16*>(y));
   else
-    launch_pdl(uncondense_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(gathered), L->pos, L->w, L->T, L->k, L->d,
+    launch_pdl(L->k <= 2 ? uncondense_kernel<float, 2> : uncondense_kernel<float, 8>, blocks, 256, 0, st, static_cast<const float*>(gathered), L->pos, L->w, L->T, L->k, L->d,
                                                      static_cast<float*>(y));
   LUFFY_LAUNCHED();
   return 0;
@@ -584,10 +647,10 @@ int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
-    launch_pdl(unpack_bwd_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
+    launch_pdl(L->k <= 2 ? unpack_bwd_kernel<bf16, 2> : unpack_bwd_kernel<bf16, 8>, blocks, 256, 0, st, static_cast<const bf16*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
                                                     static_cast<bf16*>(dx));
   else
-    launch_pdl(unpack_bwd_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
+    launch_pdl(L->k <= 2 ? unpack_bwd_kernel<float, 2> : unpack_bwd_kernel<float, 8>, blocks, 256, 0, st, static_cast<const float*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
                                                      static_cast<float*>(dx));
   LUFFY_LAUNCHED();
   return 0;

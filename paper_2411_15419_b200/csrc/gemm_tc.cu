@@ -8,8 +8,10 @@
 //   warp 1      MMA issuer: one thread of the leader issues tcgen05.mma.cta_group::{2,1}.kind::f16 (M=256 or
 //               128, N=256, K=16) into a double-buffered TMEM accumulator (2 x 256 columns per CTA); the
 //               pair halves the B bytes each SM stages and reads per MMA;
-//   warps 2-9   epilogue (two per TMEM lane quarter, one column half each): tcgen05.ld 32x32b.x32 -> fused GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the
-//               fp32 weight gradient) stored straight to global memory.
+//   warps 2-9   epilogue (two per TMEM lane quarter, one column half each): tcgen05.ld 32x32b.x32 -> fused
+//               GeLU / SwiGLU / GeLU' / SwiGLU' -> bf16 (or the fp32 weight gradient); each 32 x 32 block is
+//               staged swizzled in shared memory and leaves through one TMA store (bf16 outputs kept on this
+//               GPU) or coalesced per-lane stores (peer rows of the fused exchanges, SwiGLU, weight gradients).
 // Tiles walk expert segments whose row offsets (multiples of 128) live on the device, so no host sync
 // is needed to size the work.  Operands may be K-major or MN-major (the backward reads W1/W2 and the
 // token-major activations transposed through the descriptor's major bit instead of transposing data).
@@ -56,6 +58,7 @@ struct TcArgs {
   XSignal sig;
   int has_wr;          // fused dispatch: wait per tile for the source ranks of its A rows
   XWaitRows wr;
+  int tma_out;         // rows mode: D (and the GeLU' aux) are stored through the tD / tD3 tensor maps
 };
 
 struct Tile {
@@ -231,7 +234,8 @@ __device__ __forceinline__ void load32_bf16(const bf16* src, float (&v)[32]) {
 template <int EPI, bool A_MN, bool B_MN, bool WG, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                   const __grid_constant__ CUtensorMap tB3, const TcArgs a) {
+                   const __grid_constant__ CUtensorMap tB3, const __grid_constant__ CUtensorMap tD,
+                   const __grid_constant__ CUtensorMap tD3, const TcArgs a) {
   pdl_enter();
   constexpr int STAGES = Pipe<CG>::STAGES;
   constexpr int B_BYTES = Pipe<CG>::B_BYTES;
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
       if (!live) {
-      } else if (WG) {
+      } else if (WG && !a.tma_out) {  // per-lane stores through the staging buffer (default)
         const int m = x.m0 + hm + rt;
         float* dst = m < a.Msplit ? static_cast<float*>(a.D) + ((size_t)x.g * a.Msplit + m) * a.N
                                   : a.D3 + ((size_t)x.g * (a.M - a.Msplit) + (m - a.Msplit)) * a.N;
@@ -417,10 +421,37 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 0; i < 32; ++i) v[i] = x.nkb > 0 ? __uint_as_float(r[i]) : 0.f;
           store_block_f32(stg, v, dst + c0);
         }
+      } else if (WG) {
+        // fp32 32x32 blocks leave through TMA stores (tensor maps tD / tD3, box 32 x 32, SWIZZLE_128B): the
+        // staging layout below is the 128-byte swizzle, so one lane issues the whole 4 KiB block
+        const int row0 = x.m0 + hm + 32 * q;  // Msplit is a multiple of 32: a block lies on one side
+        const bool lo = row0 < a.Msplit;
+        const CUtensorMap* md = lo ? &tD : &tD3;
+        const int orow = lo ? x.g * a.Msplit + row0 : x.g * (a.M - a.Msplit) + (row0 - a.Msplit);
+#pragma unroll 1
+        for (int c0 = hc * (BN / 2); c0 < (hc + 1) * (BN / 2); c0 += 32) {
+          uint32_t r[32];
+          tc::tmem_ld32(tb + c0, r);
+          tc::tmem_ld_wait();
+          if (lane == 0) tc::bulk_wait_read();  // the previous block's store has read the buffer
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 u = x.nkb > 0 ? make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) = u;
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) tc::tma_store_2d(md, stg, x.n0 + c0, orow);
+        }
       } else {
         const size_t row = (size_t)(x.m0 + hm + rt);
         bf16* D = static_cast<bf16*>(a.D);
         bf16* X = static_cast<bf16*>(a.aux);
+        // GEMM outputs that stay on this GPU leave through TMA stores (tD = D, tD3 = the GeLU' aux)
+        const bool tma_out = (EPI == EPI_STORE || EPI == EPI_GELU || EPI == EPI_DGELU) && a.tma_out;
         if (EPI == EPI_SWIGLU) {
           const int f = a.f;
 #pragma unroll 1
@@ -475,7 +506,27 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
             const int n = x.n0 + c0;
-            if (EPI == EPI_STORE) {
+            if (tma_out) {  // local output: 32 x 32 blocks leave through TMA stores (box 32 x 32, SWIZZLE_64B)
+              float o[32];
+              if (EPI == EPI_GELU) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) gelu_and_grad_as(v[i], o[i], v[i]);  // v <- GeLU'(pre)
+              } else if (EPI == EPI_DGELU) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] *= pa[0][i];
+              }
+              if (lane == 0) tc::bulk_wait_read();  // the previous chunk's stores have read the buffers
+              __syncwarp();
+              stage_rows_bf16(stg, EPI == EPI_GELU ? o : v);
+              if (EPI == EPI_GELU) stage_rows_bf16(stg + 2048, v);
+              tc::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                const int row0 = x.m0 + hm + 32 * q;
+                tc::tma_store_2d(&tD, stg, n, row0);
+                if (EPI == EPI_GELU) tc::tma_store_2d(&tD3, stg + 2048, n, row0);
+              }
+            } else if (EPI == EPI_STORE) {
               if (a.has_rd) {  // fused exchange: the row goes straight to its rank's buffer over NVLink
                 if (a.rd.mask) {  // combine: every destination rank of the row (sequence migration)
                   const unsigned long long m = a.rd.mask[row];
@@ -525,6 +576,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+    if (lane == 0) tc::bulk_wait_all();  // TMA stores complete before the CTA (and its buffers) retires
   }
   if (CG == 2) {
     tc::tc_fence_before();
@@ -547,6 +599,18 @@ int num_sms() {
   return n;
 }
 
+// TMA stores for the bf16 outputs of the rows GEMMs that stay on this GPU.  LUFFY_TMA_STORE (A/B
+// measurements): 0 = none, 1 = also the fp32 weight gradients, 2 = rows GEMMs only (default: with one
+// 4 KiB staging buffer per warp the wgrad epilogue waits for each block's store to drain the buffer and
+// measured ~0.5% slower per step than its per-lane stores; 0 is ~2% slower than 2)
+int tma_store_mode() {
+  static const int mode = [] {
+    const char* v = std::getenv("LUFFY_TMA_STORE");
+    return v && v[0] >= '0' && v[0] <= '2' ? v[0] - '0' : 2;
+  }();
+  return mode;
+}
+
 // CTA pairs unless LUFFY_GEMM_CG=1 (single-CTA fallback, A/B measurements)
 bool use_pairs() {
   static const bool on = [] {
@@ -557,7 +621,8 @@ bool use_pairs() {
 }
 
 template <int EPI, bool A_MN, bool B_MN, bool WG, int CG>
-int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
+int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const CUtensorMap& td,
+              const CUtensorMap& td3, const TcArgs& a, cudaStream_t s) {
   auto kern = gemm_tc_kernel<EPI, A_MN, B_MN, WG, CG>;
   constexpr int SMEM_BYTES = Pipe<CG>::SMEM;
   static bool attr = false;
@@ -566,7 +631,7 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     attr = true;
   }
   if (CG == 1) {
-    launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, a);
+    launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, td, td3, a);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(THREADS);
@@ -593,32 +658,69 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     }
     cfg.gridDim = dim3(2 * pairs);
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, kern, ta, tb, tb3, a);
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tb3, td, td3, a);
   }
   LUFFY_LAUNCHED();
   return 0;
 }
 
 template <int EPI, bool A_MN, bool B_MN, bool WG>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s) {
-  return use_pairs() ? launch_cg<EPI, A_MN, B_MN, WG, 2>(ta, tb, tb3, a, s) : launch_cg<EPI, A_MN, B_MN, WG, 1>(ta, tb, tb3, a, s);
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tb3, const TcArgs& a, cudaStream_t s,
+           const CUtensorMap* td = nullptr, const CUtensorMap* td3 = nullptr) {
+  const CUtensorMap& d = td ? *td : ta;  // output maps: weight gradient only
+  const CUtensorMap& d3 = td3 ? *td3 : d;
+  return use_pairs() ? launch_cg<EPI, A_MN, B_MN, WG, 2>(ta, tb, tb3, d, d3, a, s)
+                     : launch_cg<EPI, A_MN, B_MN, WG, 1>(ta, tb, tb3, d, d3, a, s);
 }
 
 }  // namespace
 
-int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
-                   uint32_t box_outer) {
-  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                                const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
   static EncodeFn encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
-    LUFFY_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !fn) return (int)cudaErrorNotSupported;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return nullptr;
     encode = reinterpret_cast<EncodeFn>(fn);
   }
+  return encode;
+}
+// fp32 output [outer, inner] (row stride = inner), stored in 32 x 32 boxes with the 128-byte swizzle
+int make_tmap_f32_store(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer) {
+  EncodeFn encode = encode_fn();
+  if (!encode) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+// bf16 output [outer, inner] (row stride = inner), stored in 32 x 32 boxes with the 64-byte swizzle
+int make_tmap_bf16_store(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer) {
+  EncodeFn encode = encode_fn();
+  if (!encode) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+}  // namespace
+
+int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+                   uint32_t box_outer) {
+  EncodeFn encode = encode_fn();
+  if (!encode) return (int)cudaErrorNotSupported;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_stride_elems * 2};
   cuuint32_t box[2] = {64, box_outer};
@@ -654,8 +756,19 @@ int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D,
   a.D = D;
   a.aux = aux0;
   a.f = N / 2;
-  CUtensorMap ta, tb, tb3;
+  CUtensorMap ta, tb, tb3, td, td3;
   LUFFY_CUDA_TRY(make_tmap_bf16(&ta, A, K, max_rows, K, BM));
+  // outputs kept on this GPU (no peer redirect, no completion signal) use TMA stores; D (and aux) hold
+  // max_rows rows like A
+  a.tma_out = tma_store_mode() != 0 && !rd && !sig && (epi == EPI_STORE || epi == EPI_GELU || epi == EPI_DGELU);
+  if (a.tma_out) {
+    LUFFY_CUDA_TRY(make_tmap_bf16_store(&td, D, N, max_rows));
+    if (epi == EPI_GELU) LUFFY_CUDA_TRY(make_tmap_bf16_store(&td3, aux0, N, max_rows));
+    else td3 = td;
+  } else {
+    td = ta;
+    td3 = ta;
+  }
   if (b_kmajor) {
     const bool sw = epi == EPI_SWIGLU;
     a.Nb = sw ? N / 2 : N;
@@ -664,8 +777,8 @@ int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D,
     if (sw) LUFFY_CUDA_TRY(make_tmap_bf16(&tb3, B3, K, (uint64_t)G * a.Nb, K, BN / 2));
     else tb3 = tb;
     switch (epi) {
-      case EPI_STORE: return launch<EPI_STORE, false, false, false>(ta, tb, tb3, a, st);
-      case EPI_GELU: return launch<EPI_GELU, false, false, false>(ta, tb, tb3, a, st);
+      case EPI_STORE: return launch<EPI_STORE, false, false, false>(ta, tb, tb3, a, st, &td, &td3);
+      case EPI_GELU: return launch<EPI_GELU, false, false, false>(ta, tb, tb3, a, st, &td, &td3);
       case EPI_SWIGLU: return launch<EPI_SWIGLU, false, false, false>(ta, tb, tb3, a, st);
       default: return (int)cudaErrorNotSupported;
     }
@@ -677,8 +790,8 @@ int gemm_rows_tc(int epi, const void* A, const void* B, const void* B3, void* D,
   if (a.ksplit) LUFFY_CUDA_TRY(make_tmap_bf16(&tb3, B3, N, (uint64_t)G * a.Kb, N, 64));
   else tb3 = tb;
   switch (epi) {
-    case EPI_STORE: return launch<EPI_STORE, false, true, false>(ta, tb, tb3, a, st);
-    case EPI_DGELU: return launch<EPI_DGELU, false, true, false>(ta, tb, tb3, a, st);
+    case EPI_STORE: return launch<EPI_STORE, false, true, false>(ta, tb, tb3, a, st, &td, &td3);
+    case EPI_DGELU: return launch<EPI_DGELU, false, true, false>(ta, tb, tb3, a, st, &td, &td3);
     case EPI_DSWIGLU: return launch<EPI_DSWIGLU, false, true, false>(ta, tb, tb3, a, st);
     default: return (int)cudaErrorNotSupported;
   }
@@ -697,10 +810,15 @@ int gemm_wgrad_tc(const void* A, const void* B, float* D, float* D3, int Msplit,
   a.D = D;
   a.D3 = D3;
   a.Msplit = Msplit;
-  CUtensorMap ta, tb;
+  if (Msplit % 32 != 0 || (Msplit < M && !D3)) return (int)cudaErrorInvalidValue;
+  a.tma_out = tma_store_mode() == 1;
+  CUtensorMap ta, tb, td, td3;
   LUFFY_CUDA_TRY(make_tmap_bf16(&ta, A, M, max_rows, lda, 64));
   LUFFY_CUDA_TRY(make_tmap_bf16(&tb, B, N, max_rows, ldb, 64));
-  return launch<EPI_STORE, true, true, true>(ta, tb, tb, a, st);
+  LUFFY_CUDA_TRY(make_tmap_f32_store(&td, D, N, (uint64_t)G * Msplit));
+  if (Msplit < M) LUFFY_CUDA_TRY(make_tmap_f32_store(&td3, D3, N, (uint64_t)G * (M - Msplit)));
+  else td3 = td;
+  return launch<EPI_STORE, true, true, true>(ta, tb, tb, a, st, &td, &td3);
 }
 
 }  // namespace luffy

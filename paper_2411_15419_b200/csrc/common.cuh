@@ -141,6 +141,28 @@ __device__ __forceinline__ void gelu_and_grad_as(float x, float& g, float& dg) {
   g = x * cdf;
   dg = fmaf(x * 0.3989422804014327f, e, cdf);  // Phi(x) + x phi(x)
 }
+// The same arithmetic on two values with the packed fp32x2 instructions of sm_100 (FFMA2 / FMUL2: one
+// issue slot for two lanes of work); every step rounds exactly as in gelu_and_grad_as, so the results are
+// bit-identical to it.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ void gelu_and_grad_as2(float2 x, float2& g, float2& dg) {
+  float2 e, t;
+  const float2 a = __fmul2_rn(x, __fmul2_rn(x, f2(-0.72134752044448170368f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a.y));
+  const float2 den = __ffma2_rn(f2(0.2316419f), make_float2(fabsf(x.x), fabsf(x.y)), f2(1.f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(den.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(den.y));
+  float2 poly = __ffma2_rn(t, f2(0.3989422804014327f * 1.330274429f), f2(0.3989422804014327f * -1.821255978f));
+  poly = __ffma2_rn(t, poly, f2(0.3989422804014327f * 1.781477937f));
+  poly = __ffma2_rn(t, poly, f2(0.3989422804014327f * -0.356563782f));
+  poly = __ffma2_rn(t, poly, f2(0.3989422804014327f * 0.319381530f));
+  const float2 q = __fmul2_rn(e, __fmul2_rn(poly, t));
+  const float2 omq = __ffma2_rn(q, f2(-1.f), f2(1.f));  // 1 - q, rounded once as in the scalar form
+  const float2 cdf = make_float2(x.x >= 0.f ? omq.x : q.x, x.y >= 0.f ? omq.y : q.y);
+  g = __fmul2_rn(x, cdf);
+  dg = __ffma2_rn(__fmul2_rn(x, f2(0.3989422804014327f)), e, cdf);
+}
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + expf(-x)); }
 __device__ __forceinline__ float silu_grad_f(float x) {
   float s = 1.f / (1.f + expf(-x));

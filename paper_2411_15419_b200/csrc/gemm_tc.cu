@@ -510,10 +510,21 @@ __global__ void __launch_bounds__(THREADS, 1)
               float o[32];
               if (EPI == EPI_GELU) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) gelu_and_grad_as(v[i], o[i], v[i]);  // v <- GeLU'(pre)
+                for (int i = 0; i < 32; i += 2) {  // v <- GeLU'(pre), o <- GeLU(pre)
+                  float2 gg, dd;
+                  gelu_and_grad_as2(make_float2(v[i], v[i + 1]), gg, dd);
+                  o[i] = gg.x;
+                  o[i + 1] = gg.y;
+                  v[i] = dd.x;
+                  v[i + 1] = dd.y;
+                }
               } else if (EPI == EPI_DGELU) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] *= pa[0][i];
+                for (int i = 0; i < 32; i += 2) {
+                  const float2 p = __fmul2_rn(make_float2(v[i], v[i + 1]), make_float2(pa[0][i], pa[0][i + 1]));
+                  v[i] = p.x;
+                  v[i + 1] = p.y;
+                }
               }
               if (lane == 0) tc::bulk_wait_read();  // the previous chunk's stores have read the buffers
               __syncwarp();

@@ -22,12 +22,18 @@ def main(path, per_step=20):
         if len(r) <= vi:
             continue
         d = launches.setdefault(r[ii], {"kernel": re.sub(r"\(.*", "", r[ki]).replace("void ", "").replace("unnamed>::", "")
-                                        .replace("luffy::", "")})
+                                        .replace("luffy::", "").lstrip("<")})
         v = float(r[vi].replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1,
                  "us": 1, "msecond": 1e3, "ms": 1e3}
         d[r[mi]] = v * scale.get(r[ui], 1)
-    last = list(launches.values())[-per_step:]
+    # one whole step of libluffy kernels: the last window that starts at the routing kernel (torch's own
+    # kernels of the bench harness, e.g. the e2e result check, are not part of the step)
+    mine = [d for d in launches.values() if not d["kernel"].startswith("at::")]
+    starts = [i for i, d in enumerate(mine) if d["kernel"].lstrip("<").startswith("route_") and "bwd" not in d["kernel"]
+              and i + per_step <= len(mine)]
+    s0 = starts[-1] if starts else len(mine) - per_step
+    last = mine[s0:s0 + per_step]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6547.5) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6547.5
     tot = sum(d["gpu__time_duration.sum"] for d in last)

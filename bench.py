@@ -306,6 +306,7 @@ def main():
     stop.record(stream)
     host_ms = (time.time() - t_host0) * 1e3 / args.steps  # enqueue time per step (no host sync in the step)
     torch.cuda.synchronize()
+    launches = (L.luffy_launch_count() - launches0) // args.steps
     clk.window = (t_host0, time.time())
     time.sleep(0.06)
     clk_window = "timed region"
@@ -328,7 +329,6 @@ def main():
     clk.stop()
     if world > 1:
         dist.barrier()
-    launches = (L.luffy_launch_count() - launches0) // args.steps
     ms = start.elapsed_time(stop)
     if world > 1:
         t = torch.tensor([ms], device=dev)

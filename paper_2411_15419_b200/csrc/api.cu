@@ -162,7 +162,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
     o->x_peer_dw_in = cv.take<float*>(m.P);
   }
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
-  o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 63) / 64) * m.E * m.d);
+  o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 31) / 32) * m.E * m.d);
 }
 
 luffy_status validate(const luffy_config* c) {

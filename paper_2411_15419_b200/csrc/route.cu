@@ -566,6 +566,112 @@ __global__ void __launch_bounds__(256) route_bwd_fast_kernel(const float* __rest
   }
 }
 
+// Fused gate backward for E <= 8, d % 1024 == 0: CTA = 32 tokens, thread = 4 columns of every 1024-column
+// pass.  dl of the 32 tokens is formed in shared memory (as in route_bwd_fast_kernel); then each thread
+// streams its columns of x and dx once: dx[t] += dl[t] W_g and part[p][e][c] = sum over the CTA's tokens (in
+// token order) of dl[t][e] x[t][c], so x is read once for both products.  The partials are summed in a
+// fixed order by wg_reduce_kernel (deterministic dW_g).
+template <typename T>
+__global__ void __launch_bounds__(256) route_bwd_fused8_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
+                                                               const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                                               const float* __restrict__ dw, const T* __restrict__ x,
+                                                               int T_, int E, int d, int k, int renorm, float* __restrict__ dl,
+                                                               T* __restrict__ dx, float* __restrict__ part) {
+  pdl_enter();
+  constexpr int EB = 8, TT = 32, U = 4;
+  __shared__ __align__(16) float dls[TT][EB];
+  const int tb0 = blockIdx.x * TT;
+  {
+    const int i = threadIdx.x;  // 256 threads = 32 tokens x 8 experts
+    const int lt = i / EB, e = i % EB;
+    const int t = tb0 + lt;
+    float v = 0.f;
+    if (t < T_ && e < E) {
+      float sacc = 0.f, g = 0.f, wsel = 0.f;
+      bool sel = false;
+      for (int j = 0; j < k; ++j) {
+        const int ej = idx[(size_t)t * k + j];
+        const float dwj = dw[(size_t)t * k + j];
+        sacc += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
+        if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
+      }
+      v = renorm ? (sel ? wsel * (g - sacc) : 0.f) : probs[(size_t)t * E + e] * (g - sacc);
+      dl[(size_t)t * E + e] = v;
+    }
+    dls[lt][e] = v;
+  }
+  __syncthreads();
+  const int nt = min(TT, T_ - tb0);
+  for (int c = threadIdx.x * 4; c < d; c += 1024) {
+    float wr[EB][4], acc[EB][4];
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+      const float4 q = e < E ? *reinterpret_cast<const float4*>(wg + (size_t)e * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      wr[e][0] = q.x; wr[e][1] = q.y; wr[e][2] = q.z; wr[e][3] = q.w;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[e][j] = 0.f;
+    }
+    for (int t0 = 0; t0 < nt; t0 += U) {
+      float xv[U][4], gv[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // all loads of the U tokens first
+        const size_t o = (size_t)(tb0 + t0 + u) * d + c;
+        if (t0 + u < nt) {
+          if constexpr (sizeof(T) == 2) {
+            const uint2 a = *reinterpret_cast<const uint2*>(x + o);
+            const uint2 b = *reinterpret_cast<const uint2*>(dx + o);
+            const float2 a0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.x));
+            const float2 a1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a.y));
+            const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.x));
+            const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b.y));
+            xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
+            gv[u][0] = b0.x; gv[u][1] = b0.y; gv[u][2] = b1.x; gv[u][3] = b1.y;
+          } else {
+            const float4 a = *reinterpret_cast<const float4*>(x + o);
+            const float4 b = *reinterpret_cast<const float4*>(dx + o);
+            xv[u][0] = a.x; xv[u][1] = a.y; xv[u][2] = a.z; xv[u][3] = a.w;
+            gv[u][0] = b.x; gv[u][1] = b.y; gv[u][2] = b.z; gv[u][3] = b.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) xv[u][j] = gv[u][j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 l0 = *reinterpret_cast<const float4*>(&dls[t0 + u][0]);
+        const float4 l1 = *reinterpret_cast<const float4*>(&dls[t0 + u][4]);
+        const float lv[EB] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+        for (int e = 0; e < EB; ++e)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            gv[u][j] = fmaf(lv[e], wr[e][j], gv[u][j]);
+            acc[e][j] = fmaf(lv[e], xv[u][j], acc[e][j]);
+          }
+        if (t0 + u < nt) {
+          const size_t o = (size_t)(tb0 + t0 + u) * d + c;
+          if constexpr (sizeof(T) == 2) {
+            const __nv_bfloat162 a = __floats2bfloat162_rn(gv[u][0], gv[u][1]);
+            const __nv_bfloat162 b = __floats2bfloat162_rn(gv[u][2], gv[u][3]);
+            uint2 q;
+            q.x = *reinterpret_cast<const uint32_t*>(&a);
+            q.y = *reinterpret_cast<const uint32_t*>(&b);
+            *reinterpret_cast<uint2*>(dx + o) = q;
+          } else {
+            *reinterpret_cast<float4*>(dx + o) = make_float4(gv[u][0], gv[u][1], gv[u][2], gv[u][3]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E)
+        *reinterpret_cast<float4*>(part + ((size_t)blockIdx.x * E + e) * d + c) =
+            make_float4(acc[e][0], acc[e][1], acc[e][2], acc[e][3]);
+  }
+}
+
 // dW_g partials, fast path: CTA = (64 tokens, 256 columns); dl of the tile staged in shared memory,
 // x streamed with unrolled loads; part[p][e][col] for token tile p.
 template <typename T, int EB>
@@ -693,6 +799,20 @@ int launch_route(const luffy_layer* L, const void* x, const float* wg, int32_t* 
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const bool fast = L->E <= 32 && L->d % 256 == 0;
+  if (L->E <= 8 && L->d % 1024 == 0) {  // fused: one pass over x for dx and the dW_g partials
+    const int parts = (L->T + 31) / 32;
+    if (L->dtype == LUFFY_BF16)
+      launch_pdl(route_bwd_fused8_kernel<bf16>, parts, 256, 0, st, wg, L->probs, L->idx, L->w, dw,
+                 static_cast<const bf16*>(x), L->T, L->E, L->d, L->k, L->renorm, L->dl, static_cast<bf16*>(dx), L->wg_part);
+    else
+      launch_pdl(route_bwd_fused8_kernel<float>, parts, 256, 0, st, wg, L->probs, L->idx, L->w, dw,
+                 static_cast<const float*>(x), L->T, L->E, L->d, L->k, L->renorm, L->dl, static_cast<float*>(dx), L->wg_part);
+    LUFFY_LAUNCHED();
+    const int n = L->E * L->d;
+    launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
+    LUFFY_LAUNCHED();
+    return 0;
+  }
   if (fast) {
     const int fb = (L->T + 31) / 32;
     const int parts = (L->T + 63) / 64;

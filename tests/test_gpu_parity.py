@@ -151,6 +151,18 @@ def test_bf16_configs(cfg, h):
         assert res["stats"].reps < res["stats"].copies
 
 
+@pytest.mark.parametrize("T", [256, 77])
+def test_fp32_fused_gate_backward(T):
+    """fp32 with E <= 8 and d a multiple of 1024: the fused gate backward (one pass over x for dx and the
+    dW_g partials), including a token count that is not a multiple of its 32-token tile."""
+    cfg = dataclasses.replace(C1, num_experts=8, d_model=1024, d_ffn=1024)
+    inp = _inputs(cfg)
+    inp = dict(inp, X=inp["X"][:T], dY=inp["dY"][:T])
+    res = run_gpu_layer(cfg, inp, h=cfg.h)
+    _check_route(cfg, inp, res)
+    _check_numerics(cfg, inp, res, cfg.h)
+
+
 def test_threshold_above_one_is_plain_moe():
     inp = _inputs(C1)
     res = run_gpu_layer(C1, inp, h=1.01)

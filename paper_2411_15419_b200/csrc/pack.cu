@@ -10,6 +10,8 @@
 //  backward:    d_gathered[slot] = sum over the copies it represents (token order) of w * dy, from the
 //               slot-sorted member CSR built by layout (no atomics, fixed summation order); the same
 //               pass computes the gate-weight gradient dw[t, j] = <dy_t, gathered[slot of (t, j)]>.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "exchange.cuh"
 
@@ -114,6 +116,105 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
       if (i < E) nrep[i] = cnt[i];
     }
   const int g0 = goff_s[e], n = gcnt[e];
+  if (5 * n <= cur_cap) {
+    // The group's rows, their representatives and slots live in shared memory, so the dependent lookups
+    // (slot of a row's representative, its token) cost no global round trips.
+    const int s0 = offs[e], ns = cnt[e];
+    int* s_rep = cur_smem;   // [n] representative of each row (group-local index)
+    int* s_tok = s_rep + n;  // [n] token of each row
+    int* s_ls = s_tok + n;   // [n] slot (relative to s0) of each representative row, -1 otherwise
+    int* s_cnt = s_ls + n;   // [ns] members per slot
+    int* s_cur = s_cnt + ns; // [ns] placement cursors
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      s_rep[c] = rep_local[g0 + c] - g0;
+      s_tok[c] = gtok[g0 + c];
+    }
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) s_cnt[i] = 0;
+    for (int sl = s0 + ns + threadIdx.x; sl < offs[e + 1]; sl += blockDim.x) {
+      perm[sl] = -1;
+      slot_gl[sl] = -1;
+      mcnt[sl] = 0;
+      marr[sl] = 0;
+    }
+    for (int g = g0 + n + threadIdx.x; g < goff_s[e + 1]; g += blockDim.x) {
+      members[g] = -1;
+      mslot[g] = -1;
+    }
+    __syncthreads();
+    int base = 0;
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+      const int c = c0 + threadIdx.x;
+      const bool inr = c < n;
+      const bool isrep = inr && s_rep[c] == c;
+      int total;
+      const int pre = block_scan_flag2(isrep, warp_sums, total);
+      if (isrep) {
+        const int ls = base + pre;
+        s_ls[c] = ls;
+        lslot[g0 + c] = s0 + ls;
+        perm[s0 + ls] = s_tok[c];
+        slot_gl[s0 + ls] = g0 + c;
+      } else if (inr) {
+        s_ls[c] = -1;
+        lslot[g0 + c] = -1;
+      }
+      base += total;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const int t = s_tok[c];
+      const int r = s_rep[c];
+      int jj = 0;
+      for (int j = 0; j < k; ++j)
+        if (idx[(size_t)t * k + j] == e) jj = j;
+      const int ls = s_ls[r];
+      pos[(size_t)t * k + jj] = s0 + ls;
+      rep[(size_t)t * k + jj] = s_tok[r];
+      if (rep_out) rep_out[(size_t)t * k + jj] = s_tok[r];
+      atomicAdd(&s_cnt[ls], 1);
+    }
+    __syncthreads();
+    // member CSR (see below): counts -> exclusive scan -> stable placement in group-row order
+    int run = g0;
+    for (int c0 = 0; c0 < ns; c0 += blockDim.x) {
+      const int i = c0 + threadIdx.x;
+      const int v = i < ns ? s_cnt[i] : 0;
+      int total;
+      const int pre = block_scan_value(v, warp_sums, total);
+      if (i < ns) {
+        mstart[s0 + i] = run + pre;
+        mcnt[s0 + i] = v;
+        marr[s0 + i] = 0;
+        s_cur[i] = run + pre;
+      }
+      run += total;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+      const int c = c0 + threadIdx.x;
+      const bool valid = c < n;
+      const int key = valid ? s_ls[s_rep[c]] : -1 - lane;  // invalid lanes never group
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      int b = 0;
+      const int nwv = min(nwb, (n - c0 + 31) >> 5);
+      for (int w = 0; w < nwv; ++w) {  // warps claim their runs in order: stable across the block
+        if (wid == w && valid && lane == leader) {
+          b = s_cur[key];
+          s_cur[key] = b + __popc(peers);
+        }
+        __syncthreads();
+      }
+      b = __shfl_sync(0xffffffffu, b, leader);
+      if (valid) {
+        const int p = b + __popc(peers & ((1u << lane) - 1u));
+        members[p] = g0 + c;
+        mslot[p] = key + s0;
+      }
+    }
+    return;
+  }
   int base = offs[e];
   for (int c0 = 0; c0 < n; c0 += blockDim.x) {
     const int g = g0 + c0 + threadIdx.x;
@@ -565,13 +666,18 @@ inline int grid_for_warps(int64_t warps) {
 
 int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  const int cur_cap = (int)std::min<int64_t>(L->Rpad_max, 40000);
+  // dynamic shared memory (ints): the staged group state, or the placement cursors of the global-memory
+  // path (LUFFY_LAYOUT_SMEM=0 forces that path, for tests)
+  static const int cur_cap = [] {
+    const char* v = std::getenv("LUFFY_LAYOUT_SMEM");
+    return v && v[0] == '0' ? 0 : 40000;
+  }();
   static bool attr = false;
   if (!attr) {
     LUFFY_CUDA_TRY(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000 * 4));
     attr = true;
   }
-  launch_pdl(layout_kernel, L->E, 1024, cur_cap * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
+  launch_pdl(layout_kernel, L->E, 1024, (size_t)std::max(cur_cap, 1) * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
                                                  L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out,
                                                  L->gnrep_valid ? L->gnrep : nullptr, cur_cap);

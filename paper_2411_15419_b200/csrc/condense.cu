@@ -21,44 +21,44 @@
 namespace luffy {
 namespace {
 
-// Block-wide exclusive scan of one flag per thread (blockDim.x multiple of 32, <= 1024).
-__device__ __forceinline__ int block_scan_flag(bool flag, int* warp_sums, int& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  unsigned b = __ballot_sync(0xffffffffu, flag);
-  int pre = __popc(b & ((1u << lane) - 1u));
-  if (lane == 0) warp_sums[wid] = __popc(b);
-  __syncthreads();
-  if (wid == 0) {
-    int v = lane < nw ? warp_sums[lane] : 0;
-    int inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    if (lane < nw) warp_sums[lane] = inc - v;
-    if (lane == 31) warp_sums[32] = inc;
-  }
-  __syncthreads();
-  pre += warp_sums[wid];
-  total = warp_sums[32];
-  __syncthreads();
-  return pre;
-}
-
+// One CTA per expert (every CTA recounts all experts).  When T*k fits (staged != 0), idx and w are first
+// copied to shared memory with coalesced loads, so the histogram and the in-order scan over the tokens
+// read no global memory inside their loops.
 __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w,
-                                                           int T, int k, int E, int32_t* __restrict__ gcnt,
+                                                           int T, int k, int E, int staged, int32_t* __restrict__ gcnt,
                                                            int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
                                                            float* __restrict__ gw, int32_t* __restrict__ gloc,
                                                            int32_t* __restrict__ gcopy) {
   pdl_enter();
+  extern __shared__ __align__(16) int32_t gb_smem[];  // staged: idx [T*k] then w [T*k]
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
   __shared__ int warp_sums[33];
   const int e = blockIdx.x;
+  const int n = T * k;
+  const int32_t* ix = idx;
+  const float* wx = w;
   for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = 0;
+  if (staged) {
+    int32_t* si = gb_smem;
+    float* sw = reinterpret_cast<float*>(gb_smem + ((n + 3) & ~3));
+    const bool vec = (n & 3) == 0;
+    if (vec) {
+      for (int i = threadIdx.x; i < n / 4; i += blockDim.x) {
+        reinterpret_cast<int4*>(si)[i] = reinterpret_cast<const int4*>(idx)[i];
+        reinterpret_cast<float4*>(sw)[i] = reinterpret_cast<const float4*>(w)[i];
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        si[i] = idx[i];
+        sw[i] = w[i];
+      }
+    }
+    ix = si;
+    wx = sw;
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < T * k; i += blockDim.x) atomicAdd(&cnt[idx[i]], 1);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[ix[i]], 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     offs[0] = 0;
@@ -71,23 +71,47 @@ __global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __rest
       if (i < E) gcnt[i] = cnt[i];
     }
   }
-  int base = offs[e];
-  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
+  // every warp owns a contiguous token range: count its copies of expert e, one block-wide scan of the
+  // 32 counts, then each warp places its copies in token order (ballot ranks) -- one scan instead of one
+  // per 1024 tokens
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int per = (T + nw - 1) / nw;
+  const int ta = min(T, wid * per), tb = min(T, ta + per);
+  auto slot_of = [&](int t) {
     int jj = -1;
-    if (t < T)
+    if (t < tb)
       for (int j = 0; j < k; ++j)
-        if (idx[(size_t)t * k + j] == e) jj = j;
-    int total;
-    int pre = block_scan_flag(jj >= 0, warp_sums, total);
+        if (ix[(size_t)t * k + j] == e) jj = j;
+    return jj;
+  };
+  int mine = 0;
+  for (int t0 = ta; t0 < tb; t0 += 32) mine += __popc(__ballot_sync(0xffffffffu, slot_of(t0 + lane) >= 0));
+  if (lane == 0) warp_sums[wid] = mine;
+  __syncthreads();
+  if (wid == 0) {
+    const int v = lane < nw ? warp_sums[lane] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane < nw) warp_sums[lane] = inc - v;
+  }
+  __syncthreads();
+  int base = offs[e] + warp_sums[wid];
+  for (int t0 = ta; t0 < tb; t0 += 32) {
+    const int t = t0 + lane;
+    const int jj = slot_of(t);
+    const unsigned b = __ballot_sync(0xffffffffu, jj >= 0);
     if (jj >= 0) {
-      const int g = base + pre;
+      const int g = base + __popc(b & ((1u << lane) - 1u));
       gtok[g] = t;
-      gw[g] = w[(size_t)t * k + jj];
+      gw[g] = wx[(size_t)t * k + jj];
       gloc[(size_t)t * k + jj] = g;
       gcopy[g] = t * k + jj;
     }
-    base += total;
+    base += __popc(b);
   }
   for (int g = offs[e] + cnt[e] + threadIdx.x; g < offs[e + 1]; g += blockDim.x) {
     gtok[g] = -1;
@@ -469,7 +493,17 @@ __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int3
 
 int launch_group_build(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(group_build_kernel, L->E, 1024, 0, st, L->idx, L->w, L->T, L->k, L->E, L->gcnt, L->goff, L->gtok,
+  // idx and w staged in shared memory when they fit (T*k <= 25600 copies: 200 KiB)
+  constexpr int kStageMax = 25600;
+  static bool attr = false;
+  if (!attr) {
+    LUFFY_CUDA_TRY(cudaFuncSetAttribute(group_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageMax * 8 + 16));
+    attr = true;
+  }
+  const int n = L->T * L->k;
+  const int staged = n <= kStageMax ? 1 : 0;
+  const size_t smem = staged ? (size_t)((n + 3) & ~3) * 8 : 0;
+  launch_pdl(group_build_kernel, L->E, 1024, smem, st, L->idx, L->w, L->T, L->k, L->E, staged, L->gcnt, L->goff, L->gtok,
                                             L->gw, L->gloc, L->gcopy);
   LUFFY_LAUNCHED();
   int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);

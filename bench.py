@@ -430,12 +430,12 @@ def main():
     achieved = flops / (ffn_ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", 1400.0)) if cfg.dtype == "bf16" else 80.0
     traffic, tsrc = None, None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemm6_cg2.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemm6_v5.json")
     if args.config == "C2" and world == 1 and os.path.exists(prof):  # measured on this workload (ncu --set full)
         with open(prof) as fh:
             kk = [k for k in json.load(fh) if k["kernel"].startswith("gemm_tc_kernel")]
         traffic = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in kk)
-        tsrc = "profiles/r01_ncu_gemm6_cg2.json: DRAM read+write of the 6 GEMM launches of one step"
+        tsrc = "profiles/r01_ncu_gemm6_v5.json: DRAM read+write of the 6 GEMM launches of one step"
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": tsrc, "kernel": "expert FFN grouped GEMMs (fwd 2 + bwd 4 launches)",
             "peak_source": f"{src} bf16_tflops_sustained" if cfg.dtype == "bf16" else "fp32 SIMT nominal"}

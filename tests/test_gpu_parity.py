@@ -282,3 +282,19 @@ def test_wider_routing(num_experts, top_k, d_model, dtype):
     _check_condense(cfg, inp, res, 0.9)
     _check_layout(cfg, inp, res)
     _check_numerics(cfg, inp, res, 0.9)
+
+
+def test_fallback_paths_subprocess():
+    """The alternative kernel paths selected once per process by environment (LUFFY_LAYOUT_SMEM=0: layout
+    through global memory; LUFFY_TMA_STORE=0: per-lane GEMM stores; LUFFY_GEMM_CG=1: single-CTA GEMMs;
+    LUFFY_PDL=0: plain launches) pass the same parity checks, run in a child process."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, LUFFY_LAYOUT_SMEM="0", LUFFY_TMA_STORE="0", LUFFY_GEMM_CG="1", LUFFY_PDL="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "test_ragged_bf16 or test_c1_fp32_simulated_ranks or test_fp32_fused_gate_backward"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

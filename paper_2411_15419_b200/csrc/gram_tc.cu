@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
       }
       const double thr = a.c2h * ni;
       const float thr_f = (float)thr;
+      const float thr_hi = thr_f >= 0.f ? thr_f * (1.f + 1e-6f) : thr_f * (1.f - 1e-6f);  // the larger bound
+      const float thr_lo = thr_f >= 0.f ? thr_f * (1.f - 1e-6f) : thr_f * (1.f + 1e-6f);
       const bool rowok = li < n && ni > 0.0;
       tc::mbar_wait(&tfull[acc], aphase);
       tc::tc_fence_after();
@@ -193,9 +195,10 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
         __syncwarp();
         tc::tmem_ld_wait();
         // edge iff G >= thr * nj (thr = (2h-1)|x_i|, decided as in fp64): the fp32 product is within
-        // 1.8e-7 (relative) of the fp64 one, so outside a 1e-6 margin the fp32 comparison IS the fp64
-        // decision; the rare elements inside the margin are re-decided in fp64
-        uint32_t word = 0, amb = 0;
+        // 1.8e-7 (relative) of the fp64 one, so outside the band [p_lo, p_hi) = thr*nj*(1 -/+ 1e-6) the
+        // fp32 comparison with either bound IS the fp64 decision; the rare elements inside the band are
+        // re-decided in fp64 (two compares per element instead of a compare and an |G - p| test)
+        uint32_t word = 0, lo = 0;
 #pragma unroll
         for (int b4 = 0; b4 < 8; ++b4) {
           const float4 nq = reinterpret_cast<const float4*>(njs)[b4];
@@ -204,11 +207,11 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
           for (int k2 = 0; k2 < 4; ++k2) {
             const int b = 4 * b4 + k2;
             const float g = __uint_as_float(r[b]);
-            const float p = thr_f * nv[k2];
-            word |= (uint32_t)(g >= p) << b;
-            amb |= (uint32_t)(fabsf(g - p) <= 1e-6f * fabsf(p)) << b;
+            word |= (uint32_t)(g >= thr_hi * nv[k2]) << b;
+            lo |= (uint32_t)(g >= thr_lo * nv[k2]) << b;
           }
         }
+        const uint32_t amb = word ^ lo;  // p_lo <= G < p_hi (column norms are >= 0, so the bounds stay ordered)
         if (__any_sync(0xffffffffu, amb != 0u)) {
 #pragma unroll
           for (int b = 0; b < 32; ++b) {

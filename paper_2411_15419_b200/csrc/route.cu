@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(256) route_bwd_fast_kernel(const float* __rest
 // token order) of dl[t][e] x[t][c], so x is read once for both products.  The partials are summed in a
 // fixed order by wg_reduce_kernel (deterministic dW_g).
 template <typename T>
-__global__ void __launch_bounds__(256) route_bwd_fused8_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
+__global__ void __launch_bounds__(256, 2) route_bwd_fused8_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
                                                                const int32_t* __restrict__ idx, const float* __restrict__ w,
                                                                const float* __restrict__ dw, const T* __restrict__ x,
                                                                int T_, int E, int d, int k, int renorm, float* __restrict__ dl,
@@ -642,12 +642,17 @@ __global__ void __launch_bounds__(256) route_bwd_fused8_kernel(const float* __re
         const float4 l0 = *reinterpret_cast<const float4*>(&dls[t0 + u][0]);
         const float4 l1 = *reinterpret_cast<const float4*>(&dls[t0 + u][4]);
         const float lv[EB] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        // packed fp32x2 FMAs over column pairs: every element keeps its own expert-ordered fmaf chain, so
+        // the results are bit-identical to the scalar form at half the issue slots
 #pragma unroll
         for (int e = 0; e < EB; ++e)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            gv[u][j] = fmaf(lv[e], wr[e][j], gv[u][j]);
-            acc[e][j] = fmaf(lv[e], xv[u][j], acc[e][j]);
+          for (int j = 0; j < 4; j += 2) {
+            const float2 l2 = make_float2(lv[e], lv[e]);
+            const float2 g2 = __ffma2_rn(l2, make_float2(wr[e][j], wr[e][j + 1]), make_float2(gv[u][j], gv[u][j + 1]));
+            const float2 a2 = __ffma2_rn(l2, make_float2(xv[u][j], xv[u][j + 1]), make_float2(acc[e][j], acc[e][j + 1]));
+            gv[u][j] = g2.x; gv[u][j + 1] = g2.y;
+            acc[e][j] = a2.x; acc[e][j + 1] = a2.y;
           }
         if (t0 + u < nt) {
           const size_t o = (size_t)(tb0 + t0 + u) * d + c;

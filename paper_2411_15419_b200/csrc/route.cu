@@ -170,9 +170,19 @@ __global__ void __launch_bounds__(256, 2) route_e8_kernel(const T* __restrict__ 
           }
       if (s0 == 0) {  // stage this chunk of W_g while the first row loads are in flight
         __syncthreads();
-        for (int i = threadIdx.x; i < E * (rc / 4); i += blockDim.x) {
+        // expert-pair layout: float4 ((2p + hf) * RC/4 + c/4) holds (w_2p, w_2p+1) at columns c + 2 hf and
+        // c + 2 hf + 1, so one conflict-free float4 read feeds two packed FMAs; the partner of an odd last
+        // expert is zero
+        const int Ep = (E + 1) & ~1;
+        for (int i = threadIdx.x; i < Ep * (rc / 4); i += blockDim.x) {
           const int e = i / (rc / 4), c = (i % (rc / 4)) * 4;
-          *reinterpret_cast<float4*>(&wsm[e * RC + c]) = *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c);
+          const float4 q = e < E ? *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float* b0 = &wsm[((e >> 1) * 2 * (RC / 4) + (c >> 2)) * 4 + (e & 1)];
+          float* b1 = b0 + RC;  // hf = 1: (RC / 4) float4 further
+          b0[0] = q.x;
+          b0[2] = q.y;
+          b1[0] = q.z;
+          b1[2] = q.w;
         }
         __syncthreads();
       }
@@ -185,18 +195,22 @@ __global__ void __launch_bounds__(256, 2) route_e8_kernel(const T* __restrict__ 
           float xv[TB][4];
 #pragma unroll
           for (int i = 0; i < TB; ++i) cvt4(raw[i][u][h], xv[i]);
+          // packed fp32x2 FMAs over expert pairs: each logit keeps its own column-ordered fmaf chain, so the
+          // results are bit-identical to the scalar form at half the issue slots
 #pragma unroll
-          for (int e = 0; e < EB; ++e) {
-            if (e < E) {
-              const float4 wv = *reinterpret_cast<const float4*>(&wsm[e * RC + c]);
+          for (int p = 0; p < EB / 2; ++p) {
+            if (2 * p < E) {
+              const float4 w0 = *reinterpret_cast<const float4*>(&wsm[(p * 2 * (RC / 4) + (c >> 2)) * 4]);
+              const float4 w1 = *reinterpret_cast<const float4*>(&wsm[((p * 2 + 1) * (RC / 4) + (c >> 2)) * 4]);
 #pragma unroll
               for (int i = 0; i < TB; ++i) {
-                float s = v[i * EB + e];
-                s = fmaf(xv[i][0], wv.x, s);
-                s = fmaf(xv[i][1], wv.y, s);
-                s = fmaf(xv[i][2], wv.z, s);
-                s = fmaf(xv[i][3], wv.w, s);
-                v[i * EB + e] = s;
+                float2 s2 = make_float2(v[i * EB + 2 * p], v[i * EB + 2 * p + 1]);
+                s2 = __ffma2_rn(make_float2(xv[i][0], xv[i][0]), make_float2(w0.x, w0.y), s2);
+                s2 = __ffma2_rn(make_float2(xv[i][1], xv[i][1]), make_float2(w0.z, w0.w), s2);
+                s2 = __ffma2_rn(make_float2(xv[i][2], xv[i][2]), make_float2(w1.x, w1.y), s2);
+                s2 = __ffma2_rn(make_float2(xv[i][3], xv[i][3]), make_float2(w1.z, w1.w), s2);
+                v[i * EB + 2 * p] = s2.x;
+                v[i * EB + 2 * p + 1] = s2.y;
               }
             }
           }

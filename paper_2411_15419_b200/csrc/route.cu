@@ -364,14 +364,17 @@ __global__ void __launch_bounds__(256) route_fast_kernel(const T* __restrict__ x
         for (int e = 0; e < EB; ++e) {
           if (e < E) {
             const float4 wv = *reinterpret_cast<const float4*>(&ws[e][cl]);
+            // packed fp32x2 FMAs over token pairs: each logit keeps its own column-ordered fmaf chain
+            // (bit-identical to the scalar form)
 #pragma unroll
-            for (int i = 0; i < TB; ++i) {
-              float s = acc[i][e];
-              s = fmaf(xv[i][0], wv.x, s);
-              s = fmaf(xv[i][1], wv.y, s);
-              s = fmaf(xv[i][2], wv.z, s);
-              s = fmaf(xv[i][3], wv.w, s);
-              acc[i][e] = s;
+            for (int i = 0; i < TB; i += 2) {
+              float2 s2 = make_float2(acc[i][e], acc[i + 1][e]);
+              s2 = __ffma2_rn(make_float2(xv[i][0], xv[i + 1][0]), make_float2(wv.x, wv.x), s2);
+              s2 = __ffma2_rn(make_float2(xv[i][1], xv[i + 1][1]), make_float2(wv.y, wv.y), s2);
+              s2 = __ffma2_rn(make_float2(xv[i][2], xv[i + 1][2]), make_float2(wv.z, wv.z), s2);
+              s2 = __ffma2_rn(make_float2(xv[i][3], xv[i + 1][3]), make_float2(wv.w, wv.w), s2);
+              acc[i][e] = s2.x;
+              acc[i + 1][e] = s2.y;
             }
           }
         }

@@ -33,8 +33,11 @@
  *    All ranks must issue the same sequence of calls.
  *  - Errors: arguments are validated on the host before anything is enqueued; on failure a status is
  *    returned, nothing is launched and luffy_last_error() describes the problem.  CUDA failures map to
- *    LUFFY_E_CUDA.  Calling out of order returns LUFFY_E_STATE.  A rank that stops participating makes the
- *    others trap after a bounded wait (~20 s) instead of hanging.
+ *    LUFFY_E_CUDA.  Calling out of order returns LUFFY_E_STATE.  A rank that stops participating does not
+ *    hang or kill the others: every cross-rank wait is bounded (luffy_layer_set_exchange_timeout, default
+ *    20 s); on expiry the waiting kernel records the phase and step in the layer's error word and
+ *    completes (that step's results are garbage), and every later luffy_* call on the layer returns
+ *    LUFFY_E_STATE naming the phase -- the CUDA context stays usable.
  *  - Determinism: identical inputs give bitwise-identical outputs (no floating-point atomics).
  *  - Thread-compatibility: one thread at a time per luffy_ctx.
  * ------------------------------------------------------------------------------------------------- */
@@ -208,14 +211,26 @@ LUFFY_API luffy_status luffy_dispatch_bwd(luffy_layer* layer, const void* d_recv
 LUFFY_API luffy_status luffy_route_bwd(luffy_layer* layer, const void* x, const float* w_gate, const float* d_topk_w,
                              void* dx, float* dw_gate, void* stream);
 
-/* Host-side exchange plan of the dispatch/combine (used inside luffy_dispatch; exported for tests).
+/* Host export of the dispatch/combine plan (P:143 dispatch, P:144 combine; R14/R15).  The device count
+ * exchange inside luffy_dispatch (world > 1) derives its layout with the SAME code (csrc/xplan.h, one
+ * __host__ __device__ definition), so this call returns exactly the plan the kernels use.
  * counts_all [P][E] (host): representatives each source rank sends to each expert.  Outputs (host):
  * send_off [E+1]  padded send layout of `rank` (expert asc, each segment rounded up to LUFFY_ROW_ALIGN);
  * recv_off [E_l+1] padded expert layout of `rank` (local expert asc; within a segment source rank asc);
+ * dst_base [E] (nullable): first row, in expert e's owner's layout, of the rows `rank` sends to e (the
+ *   dispatch push writes send slot s of expert e to row dst_base[e] + s - send_off[e] there);
+ * rank_of / slot_of [row_capacity] (nullable, together): for every expert-layout row r < recv_off[E_l] of
+ *   `rank`, the source rank and its send slot (the combine returns row r there); -1 for padding rows;
+ *   LUFFY_E_CAPACITY if recv_off[E_l] > row_capacity;
  * send_rows_to [P] / recv_rows_from [P] (nullable): rows exchanged with each peer (self included). */
 LUFFY_API luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts_all,
-                                           int32_t* send_off, int32_t* recv_off, int64_t* send_rows_to,
+                                           int32_t* send_off, int32_t* recv_off, int32_t* dst_base, int32_t* rank_of,
+                                           int32_t* slot_of, int64_t row_capacity, int64_t* send_rows_to,
                                            int64_t* recv_rows_from);
+
+/* world > 1: bound (milliseconds, > 0) of every cross-rank wait of the layer's exchange; default 20000 or
+ * the environment variable LUFFY_EXCHANGE_TIMEOUT_MS read at luffy_layer_create. */
+LUFFY_API luffy_status luffy_layer_set_exchange_timeout(luffy_layer* layer, int64_t ms);
 
 /* ---- debug export (tests) ----------------------------------------------------------------------- */
 

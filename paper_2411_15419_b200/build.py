@@ -50,8 +50,6 @@ def _compile(src: str, digest: str, verbose: bool) -> str:
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == key:
         return obj
     cmd = [NVCC, "-c", path, "-o", obj] + CU_FLAGS
-    if src.endswith(".cpp"):
-        cmd += ["-x", "cu"] if False else []
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -4,7 +4,10 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -25,6 +28,42 @@ luffy_status fail(luffy_status st, const std::string& msg) {
   return st;
 }
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_cache_mu;
+std::map<std::tuple<const void*, int, int64_t>, int> g_cache;
+int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+}  // namespace
+bool dev_cache_get(const void* key, int64_t extra, int* value) {
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  auto it = g_cache.find(std::make_tuple(key, cur_dev(), extra));
+  if (it == g_cache.end()) return false;
+  *value = it->second;
+  return true;
+}
+void dev_cache_put(const void* key, int64_t extra, int value) {
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  g_cache[std::make_tuple(key, cur_dev(), extra)] = value;
+}
+int device_sms() {
+  static const char tag = 0;
+  int n = 0;
+  if (dev_cache_get(&tag, 0, &n)) return n;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, cur_dev());
+  dev_cache_put(&tag, 0, n);
+  return n;
+}
+int smem_optin(const void* kernel, int bytes) {
+  int v = 0;
+  if (dev_cache_get(kernel, bytes, &v)) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) dev_cache_put(kernel, bytes, 1);
+  return (int)e;
+}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("LUFFY_PDL");
@@ -267,6 +306,27 @@ luffy_status need_open(const luffy_layer* L, const char* where) {
     if (_s != LUFFY_OK) return _s;                       \
   } while (0)
 
+// A cross-rank wait of an earlier call timed out (exchange.cuh xwait_flag): the layer is unusable.
+luffy_status exchange_health(const luffy_layer* L, const char* where) {
+  if (L->P > 1 && L->x_err_h) {
+    const uint32_t ph = *reinterpret_cast<volatile const uint32_t*>(L->x_err_h);
+    if (ph != 0u) {
+      static const char* names[] = {"counts", "dispatch", "combine", "combine_bwd", "dispatch_bwd", "migration rows",
+                                    "migration meta", "migration bwd"};
+      const uint32_t sq = reinterpret_cast<volatile const uint32_t*>(L->x_err_h)[1];
+      return fail(LUFFY_E_STATE, std::string(where) + ": an exchange wait timed out (phase " +
+                                     (ph - 1 < XP_NUM ? names[ph - 1] : "?") + ", step " + std::to_string(sq) +
+                                     "): a peer rank stopped participating; the layer must be recreated");
+    }
+  }
+  return LUFFY_OK;
+}
+#define LUFFY_HEALTHY(L, where)                          \
+  do {                                                   \
+    luffy_status _s = exchange_health((L), (where));     \
+    if (_s != LUFFY_OK) return _s;                       \
+  } while (0)
+
 }  // namespace
 }  // namespace luffy
 
@@ -277,25 +337,26 @@ extern "C" {
 const char* luffy_last_error(void) { return g_err.c_str(); }
 
 luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_experts, const int32_t* counts_all,
-                                 int32_t* send_off, int32_t* recv_off, int64_t* send_rows_to, int64_t* recv_rows_from) {
-  if (world < 1 || rank < 0 || rank >= world || num_experts < 1 || num_experts % world)
+                                 int32_t* send_off, int32_t* recv_off, int32_t* dst_base, int32_t* rank_of,
+                                 int32_t* slot_of, int64_t row_capacity, int64_t* send_rows_to, int64_t* recv_rows_from) {
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || num_experts < 1 ||
+      num_experts > LUFFY_MAX_EXPERTS || num_experts % world)
     return fail(LUFFY_E_INVALID, "exchange_plan: bad world/rank/num_experts");
   LUFFY_NEED(counts_all);
   LUFFY_NEED(send_off);
   LUFFY_NEED(recv_off);
   const int P = world, E = num_experts, El = E / world;
-  send_off[0] = 0;
-  for (int e = 0; e < E; ++e) {
-    const int32_t c = counts_all[(size_t)rank * E + e];
-    if (c < 0) return fail(LUFFY_E_INVALID, "exchange_plan: negative count");
-    send_off[e + 1] = send_off[e] + (int32_t)round_up(c, kRowAlign);
-  }
-  recv_off[0] = 0;
-  for (int el = 0; el < El; ++el) {
-    const int e = rank * El + el;
-    int64_t rows = 0;
-    for (int q = 0; q < P; ++q) rows += counts_all[(size_t)q * E + e];
-    recv_off[el + 1] = recv_off[el] + (int32_t)round_up(rows, kRowAlign);
+  for (int i = 0; i < P * E; ++i)
+    if (counts_all[i] < 0) return fail(LUFFY_E_INVALID, "exchange_plan: negative count");
+  // the same code the device count-exchange kernel runs (xplan.h), on one host thread
+  std::vector<int32_t> soff_all((size_t)P * (E + 1)), base(E);
+  xplan_body(counts_all, P, E, rank, nullptr, recv_off, base.data(), soff_all.data(), 0, 1);
+  std::memcpy(send_off, soff_all.data() + (size_t)rank * (E + 1), sizeof(int32_t) * (E + 1));
+  if (dst_base) std::memcpy(dst_base, base.data(), sizeof(int32_t) * E);
+  if (rank_of || slot_of) {
+    if (!rank_of || !slot_of) return fail(LUFFY_E_INVALID, "exchange_plan: rank_of and slot_of go together");
+    if (recv_off[El] > row_capacity) return fail(LUFFY_E_CAPACITY, "exchange_plan: row_capacity < recv_off[E_l]");
+    for (int64_t r = 0; r < recv_off[El]; ++r) xplan_row(r, counts_all, recv_off, soff_all.data(), P, E, rank, rank_of + r, slot_of + r);
   }
   for (int p = 0; p < P; ++p) {
     int64_t so = 0, ri = 0;
@@ -381,6 +442,19 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
       return cuda_fail(e, "exchange region (cudaMalloc / cudaIpcGetMemHandle)");
     }
     std::memcpy(L->x_handle, &h, sizeof(h));
+    // the exchange error word: pinned host memory mapped into the device (read without a sync)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&L->x_err_h), 2 * sizeof(uint32_t), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->x_err_d), L->x_err_h, 0);
+    if (e != cudaSuccess) {
+      luffy_layer_destroy(L);
+      return cuda_fail(e, "exchange error word (cudaHostAlloc mapped)");
+    }
+    L->x_err_h[0] = L->x_err_h[1] = 0u;
+    {
+      const char* v = std::getenv("LUFFY_EXCHANGE_TIMEOUT_MS");
+      const long long ms = v ? std::atoll(v) : 20000;
+      L->x_timeout_ns = (uint64_t)(ms > 0 ? ms : 20000) * 1000000ull;
+    }
     L->x_recv[0] = L->x_region + xl.recv[0];
     L->x_recv[1] = L->x_region + xl.recv[1];
     L->x_gathered = L->x_region + xl.gathered;
@@ -406,7 +480,15 @@ void luffy_layer_destroy(luffy_layer* L) {
     for (int p = 0; p < L->P; ++p)
       if (p != L->rank && L->x_peer_base_h[p]) cudaIpcCloseMemHandle(L->x_peer_base_h[p]);
   if (L->x_region) cudaFree(L->x_region);
+  if (L->x_err_h) cudaFreeHost(L->x_err_h);
   delete L;
+}
+
+luffy_status luffy_layer_set_exchange_timeout(luffy_layer* L, int64_t ms) {
+  LUFFY_NEED(L);
+  if (ms <= 0) return fail(LUFFY_E_INVALID, "luffy_layer_set_exchange_timeout: ms must be > 0");
+  L->x_timeout_ns = (uint64_t)ms * 1000000ull;
+  return LUFFY_OK;
 }
 
 size_t luffy_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
@@ -498,6 +580,7 @@ luffy_status luffy_layer_rows(const luffy_layer* L, int64_t* send_rows, int64_t*
 luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int32_t T, int32_t* topk_idx,
                          float* topk_w, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_route");
   LUFFY_NEED(x);
   LUFFY_NEED(w_gate);
   LUFFY_NEED(topk_idx);
@@ -518,6 +601,7 @@ luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int
 luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep, luffy_condense_stats* stats,
                             void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_condense");
   LUFFY_NEED(x);
   LUFFY_NEED(rep);
   LUFFY_ALIGNED(x);
@@ -583,6 +667,7 @@ luffy_status luffy_layer_exchange_buffers(const luffy_layer* L, void** recv, voi
 
 luffy_status luffy_dispatch(luffy_layer* L, const void* x, void* recv, int64_t* recv_rows, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_dispatch");
   LUFFY_NEED(x);
   LUFFY_ALIGNED(x);
   LUFFY_STAGE(L, 2, "luffy_dispatch");
@@ -610,6 +695,7 @@ luffy_status luffy_dispatch(luffy_layer* L, const void* x, void* recv, int64_t* 
 luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, const void* w2, const void* w3, void* out,
                               void* saved_pre, void* saved_act, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_expert_ffn");
   LUFFY_NEED(w1);
   LUFFY_NEED(w2);
   LUFFY_NEED(saved_pre);
@@ -645,6 +731,7 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
     wr.me = L->rank;
     wr.cnt_all = L->cnt_all;
     wr.roff = L->roff;
+    wr.err = make_xerr(L);
   }
   if (L->act == LUFFY_GELU) {
     LUFFY_CHECK(gemm_rows(L->dtype, EPI_GELU, recv, w1, nullptr, saved_act, saved_pre, off, L->El, rows, L->f, L->d, 1, stream,
@@ -664,6 +751,7 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
 
 luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathered, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_combine");
   LUFFY_STAGE(L, 4, "luffy_combine");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (L->P == 1) {
@@ -687,6 +775,7 @@ luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathere
 
 luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_uncondense");
   LUFFY_NEED(y);
   LUFFY_ALIGNED(y);
   LUFFY_STAGE(L, 5, "luffy_uncondense");
@@ -711,6 +800,7 @@ luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, voi
 luffy_status luffy_uncondense_bwd(luffy_layer* L, const void* dy, const void* gathered, void* d_gathered, float* d_topk_w,
                                   void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_uncondense_bwd");
   LUFFY_NEED(dy);
   LUFFY_NEED(d_topk_w);
   LUFFY_ALIGNED(dy);
@@ -738,6 +828,7 @@ luffy_status luffy_uncondense_bwd(luffy_layer* L, const void* dy, const void* ga
 
 luffy_status luffy_combine_bwd(luffy_layer* L, const void* d_gathered, void* d_expert_out, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_combine_bwd");
   LUFFY_STAGE(L, 6, "luffy_combine_bwd");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (L->P == 1) {
@@ -756,6 +847,7 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
                                   const void* w3, const void* saved_pre, const void* saved_act, void* scratch_dpre,
                                   void* d_recv, float* dw1, float* dw2, float* dw3, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_expert_ffn_bwd");
   LUFFY_NEED(w1);
   LUFFY_NEED(w2);
   LUFFY_NEED(saved_pre);
@@ -807,6 +899,7 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
 
 luffy_status luffy_dispatch_bwd(luffy_layer* L, const void* d_recv, void* dx, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_dispatch_bwd");
   LUFFY_NEED(dx);
   LUFFY_ALIGNED(dx);
   LUFFY_STAGE(L, 6, "luffy_dispatch_bwd");
@@ -825,6 +918,7 @@ luffy_status luffy_dispatch_bwd(luffy_layer* L, const void* d_recv, void* dx, vo
 luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate, const float* d_topk_w, void* dx,
                              float* dw_gate, void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_route_bwd");
   LUFFY_NEED(x);
   LUFFY_NEED(w_gate);
   LUFFY_NEED(d_topk_w);
@@ -840,6 +934,7 @@ luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate,
 luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t num_seqs, int64_t* rows_at_all,
                                  void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_sequence_rows");
   LUFFY_NEED(seq_len);
   LUFFY_NEED(rows_at_all);
   LUFFY_STAGE(L, 2, "luffy_sequence_rows");
@@ -872,6 +967,7 @@ luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t
 luffy_status luffy_set_migration(luffy_layer* L, const int32_t* seq_len_all, const int32_t* seq_dest, int64_t* out_rows,
                                  void* stream) {
   LUFFY_NEED(L);
+  LUFFY_HEALTHY(L, "luffy_set_migration");
   LUFFY_NEED(seq_len_all);
   LUFFY_NEED(seq_dest);
   if (L->S < 1) return fail(LUFFY_E_STATE, "luffy_set_migration: call luffy_sequence_rows first (this step)");

@@ -33,6 +33,15 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Per-device launch caches (api.cu).  Function attributes and occupancy answers belong to a (kernel,
+// device) pair, so they are cached per current device and per `extra` key (e.g. the shared-memory size or
+// the group count they were computed for) -- a process driving several devices or layers of different
+// shapes never reuses another's answer.
+bool dev_cache_get(const void* key, int64_t extra, int* value);
+void dev_cache_put(const void* key, int64_t extra, int value);
+int device_sms();                                      // SM count of the current device
+int smem_optin(const void* kernel, int bytes);         // cudaFuncAttributeMaxDynamicSharedMemorySize, once per device
+
 bool pdl_enabled();  // api.cu: LUFFY_PDL=0 in the environment disables the attribute (A/B measurements)
 
 template <typename... KArgs, typename... Args>

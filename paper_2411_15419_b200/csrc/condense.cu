@@ -495,11 +495,7 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   // idx and w staged in shared memory when they fit (T*k <= 25600 copies: 200 KiB)
   constexpr int kStageMax = 25600;
-  static bool attr = false;
-  if (!attr) {
-    LUFFY_CUDA_TRY(cudaFuncSetAttribute(group_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageMax * 8 + 16));
-    attr = true;
-  }
+  LUFFY_CUDA_TRY(smem_optin((const void*)group_build_kernel, kStageMax * 8 + 16));
   const int n = L->T * L->k;
   const int staged = n <= kStageMax ? 1 : 0;
   const size_t smem = staged ? (size_t)((n + 3) & ~3) * 8 : 0;
@@ -549,13 +545,12 @@ int launch_greedy(luffy_layer* L, void* s) {
   if (rc >= 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(s);
   LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * (64 + kGreedyMaxRounds), st));
-  static int blocks = 0;
-  if (blocks == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  int blocks = 0;
+  if (!dev_cache_get((const void*)greedy_kernel, 0, &blocks)) {
+    int per_sm = 0;
     LUFFY_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, greedy_kernel, 256, 0));
-    LUFFY_CUDA_TRY(cudaGetDevice(&dev));
-    LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    blocks = std::max(1, std::min(per_sm, 8)) * sms;
+    blocks = std::max(1, std::min(per_sm, 8)) * device_sms();
+    dev_cache_put((const void*)greedy_kernel, 0, blocks);
   }
   GreedyArgs a;
   a.E = L->E;

@@ -8,91 +8,29 @@
 namespace luffy {
 namespace {
 
-// Wait until every rank published `seq` for this phase (bounded: traps after ~20 s instead of hanging).
-__global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq) {
+// Wait until every rank published `seq` for this phase (bounded: see xwait_flag).
+__global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq, XErr err, int phase) {
   pdl_enter();
   const int p = threadIdx.x;
-  if (p < P) {
-    uint64_t t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire_sys(flags + p) < seq) {
-      __nanosleep(32);
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 20000000000ull) __trap();
-    }
-  }
+  if (p < P) xwait_flag(flags + p, seq, err, phase);
   __syncthreads();
 }
 
 // Count exchange and layout plan in ONE single-CTA kernel: push my counts to every rank, publish XP_CNT,
-// wait for every rank's counts, then derive the plan (saves two dependent launches per dispatch).
-__device__ void plan_small_body(const int32_t* __restrict__ c, int P, int E, int me, int32_t* __restrict__ cnt_all,
-                                int32_t* __restrict__ roff, int32_t* __restrict__ dst_base, int32_t* __restrict__ src_soff);
-
+// wait for every rank's counts, then derive the plan with the shared host/device xplan_body (xplan.h).
 __global__ void xcnt_plan_kernel(const int32_t* __restrict__ nrep, int E, int me, int32_t* const* peer_cnt, int P,
                                  XSignal sig, const uint32_t* __restrict__ flags, const int32_t* __restrict__ inbox,
                                  int32_t* __restrict__ cnt_all, int32_t* __restrict__ roff, int32_t* __restrict__ dst_base,
-                                 int32_t* __restrict__ src_soff) {
+                                 int32_t* __restrict__ src_soff, XErr err) {
   pdl_enter();
   for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
     const int p = i / E, e = i % E;
     peer_cnt[p][(size_t)me * E + e] = nrep[e];
   }
   xsignal_done(sig);  // (single CTA: publishes XP_CNT to every rank)
-  if (threadIdx.x < P) {
-    uint64_t t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire_sys(flags + threadIdx.x) < sig.seq) {
-      __nanosleep(64);
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 20000000000ull) __trap();
-    }
-  }
+  if (threadIdx.x < P) xwait_flag(flags + threadIdx.x, sig.seq, err, XP_CNT);
   __syncthreads();
-  plan_small_body(inbox, P, E, me, cnt_all, roff, dst_base, src_soff);
-}
-
-// Layout plan from the all-to-all counts (one CTA): local copy of the counts, my expert layout (roff),
-// and for each expert e the destination row base of my rows in the owner's layout (dst_base[e]).
-__device__ void plan_small_body(const int32_t* __restrict__ c, int P, int E, int me, int32_t* __restrict__ cnt_all,
-                                int32_t* __restrict__ roff, int32_t* __restrict__ dst_base, int32_t* __restrict__ src_soff) {
-  // c = inbox [P][E], complete (XP_CNT waited)
-  const int El = E / P;
-  for (int i = threadIdx.x; i < P * E; i += blockDim.x) cnt_all[i] = c[i];
-  // src_soff[q][e]: padded send offsets of rank q (expert segments rounded up to kRowAlign)
-  for (int q = threadIdx.x; q < P; q += blockDim.x) {
-    int o = 0;
-    for (int e = 0; e < E; ++e) {
-      src_soff[q * (E + 1) + e] = o;
-      o += (c[q * E + e] + kRowAlign - 1) / kRowAlign * kRowAlign;
-    }
-    src_soff[q * (E + 1) + E] = o;
-  }
-  if (threadIdx.x == 0) {
-    // my expert layout
-    int o = 0;
-    for (int el = 0; el < El; ++el) {
-      roff[el] = o;
-      int rows = 0;
-      for (int q = 0; q < P; ++q) rows += c[q * E + me * El + el];
-      o += (rows + kRowAlign - 1) / kRowAlign * kRowAlign;
-    }
-    roff[El] = o;
-  }
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    // owner p = e / El lays out expert e after all experts el' < e % El of p, each padded
-    const int p = e / El, el = e % El;
-    int base = 0;
-    for (int j = 0; j < el; ++j) {
-      int rows = 0;
-      for (int q = 0; q < P; ++q) rows += c[q * E + p * El + j];
-      base += (rows + kRowAlign - 1) / kRowAlign * kRowAlign;
-    }
-    for (int q = 0; q < me; ++q) base += c[q * E + e];
-    dst_base[e] = base;
-  }
+  xplan_body(inbox, P, E, me, cnt_all, roff, dst_base, src_soff, threadIdx.x, blockDim.x);
 }
 
 // Per expert-layout row: the source rank and its send slot (for the combine and dispatch-backward
@@ -107,25 +45,9 @@ __global__ void __launch_bounds__(256) xplan_rows_kernel(const int32_t* __restri
   const int El = E / P;
   const int64_t rows = roff[El];
   const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += nthreads) {
-    int el = 0;
-    while (el + 1 <= El && roff[el + 1] <= r) ++el;
-    const int e = me * El + el;
-    int64_t i = r - roff[el];
-    int q = 0;
-    while (q < P && i >= cnt_all[q * E + e]) {
-      i -= cnt_all[q * E + e];
-      ++q;
-    }
-    if (q < P) {
-      rank_of[r] = q;
-      slot_of[r] = src_soff[q * (E + 1) + e] + (int32_t)i;
-    } else {
-      rank_of[r] = -1;
-      slot_of[r] = -1;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += nthreads)
+    if (!xplan_row(r, cnt_all, roff, src_soff, P, E, me, rank_of + r, slot_of + r))
       rowmask[r] = 0ull;  // padding rows are not combined anywhere
-    }
-  }
   // padding rows (the tail of each local expert segment) are zeroed in the receive buffer and in the
   // backward buffer: one warp per row, 16-byte coalesced stores
   const int lane = threadIdx.x & 31;
@@ -200,9 +122,16 @@ inline int grid_warps(int64_t warps) {
 
 int launch_xwait(const luffy_layer* L, int phase, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(xwait_kernel, 1, 64, 0, st, L->x_flags + phase * L->P, L->P, L->seq);
+  launch_pdl(xwait_kernel, 1, 64, 0, st, L->x_flags + phase * L->P, L->P, L->seq, make_xerr(L), phase);
   LUFFY_LAUNCHED();
   return 0;
+}
+
+XErr make_xerr(const luffy_layer* L) {
+  XErr e;
+  e.word = L->x_err_d;
+  e.timeout_ns = L->x_timeout_ns;
+  return e;
 }
 
 XSignal make_signal(const luffy_layer* L, int phase) {
@@ -220,7 +149,7 @@ int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
   const int par = L->seq & 1;
   launch_pdl(xcnt_plan_kernel, 1, 256, 0, st, L->nrep, L->E, L->rank, L->x_peer_cnt, L->P, make_signal(L, XP_CNT),
                                       L->x_flags + XP_CNT * L->P, L->x_cnt_inbox, L->cnt_all, L->roff, L->x_dst_base,
-                                      L->x_src_soff);
+                                      L->x_src_soff, make_xerr(L));
   LUFFY_LAUNCHED();
   launch_pdl(xplan_rows_kernel, 148, 256, 0, st, L->cnt_all, L->roff, L->x_src_soff, L->P, L->E, L->rank, L->d, L->recv_max,
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "luffy_internal.h"
+#include "xplan.h"
 
 namespace luffy {
 
@@ -69,6 +70,44 @@ __device__ __forceinline__ void xsignal_done(const XSignal& s) {
 
 XSignal make_signal(const luffy_layer* L, int phase);
 
+// Bounded cross-rank wait.  A peer that stops publishing must not hang or kill this rank's context: after
+// `timeout_ns` the waiter records (phase + 1, seq) in the layer's error word -- pinned host memory mapped
+// into the device, so the host reads it without a synchronisation -- and proceeds as if the flag had
+// arrived (the data of that step is garbage; flags are left unchanged).  Every later wait of the layer
+// sees the error word and returns at once, and the next luffy_* call on the layer returns LUFFY_E_STATE.
+struct XErr {
+  uint32_t* word;        // [2] mapped host memory: (phase + 1, seq) of the first timed-out wait, 0 = none
+  uint64_t timeout_ns;
+};
+
+XErr make_xerr(const luffy_layer* L);
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// true when the flag reached seq, false on timeout or an earlier failure of the layer.
+__device__ __forceinline__ bool xwait_flag(const uint32_t* flag, uint32_t seq, const XErr& e, int phase) {
+  if (ld_acquire_sys(flag) >= seq) return true;
+  if (ld_volatile_u32(e.word) != 0u) return false;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t it = 1;; ++it) {
+    __nanosleep(32);
+    if (ld_acquire_sys(flag) >= seq) return true;
+    if ((it & 255u) == 0u) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (ld_volatile_u32(e.word) != 0u) return false;
+      if (t - t0 > e.timeout_ns) {
+        if (atomicCAS_system(e.word, 0u, (uint32_t)phase + 1u) == 0u) atomicExch_system(e.word + 1, seq);
+        __threadfence_system();
+        return false;
+      }
+    }
+  }
+}
+
 // Tile-level wait for dispatched rows (fused dispatch -> GEMM1): a consumer of rows [r0, r1) of local
 // expert el waits only for the source ranks whose rows fall in that range (flags[q] >= seq, published by
 // q's pack-and-push kernel), instead of a stream-wide wait for every rank.
@@ -78,22 +117,14 @@ struct XWaitRows {
   int P, E, El, me;
   const int32_t* cnt_all;  // [P][E] rows each source sends to each expert
   const int32_t* roff;     // [El+1] expert-layout offsets of the local experts
+  XErr err;
 };
 __device__ __forceinline__ void xwait_rows(const XWaitRows& w, int el, int r0, int r1) {
   const int e = w.me * w.El + el;
   int base = w.roff[el];
   for (int q = 0; q < w.P; ++q) {
     const int n = w.cnt_all[q * w.E + e];
-    if (n > 0 && base < r1 && base + n > r0) {
-      uint64_t t0;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-      while (ld_acquire_sys(w.flags + q) < w.seq) {
-        __nanosleep(32);
-        uint64_t t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 20000000000ull) __trap();
-      }
-    }
+    if (n > 0 && base < r1 && base + n > r0) xwait_flag(w.flags + q, w.seq, w.err, XP_DISP);
     base += n;
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written rows -> TMA (async proxy) reads

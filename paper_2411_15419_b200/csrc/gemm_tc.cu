@@ -600,15 +600,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (a.has_sig) xsignal_done(a.sig);
 }
 
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int num_sms() { return device_sms(); }
 
 // TMA stores for the bf16 outputs of the rows GEMMs that stay on this GPU.  LUFFY_TMA_STORE (A/B
 // measurements): 0 = none, 1 = also the fp32 weight gradients, 2 = rows GEMMs only (default: with one
@@ -636,11 +628,7 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
               const CUtensorMap& td3, const TcArgs& a, cudaStream_t s) {
   auto kern = gemm_tc_kernel<EPI, A_MN, B_MN, WG, CG>;
   constexpr int SMEM_BYTES = Pipe<CG>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
-  }
+  LUFFY_CUDA_TRY(smem_optin((const void*)kern, SMEM_BYTES));
   if (CG == 1) {
     launch_pdl(kern, num_sms(), THREADS, SMEM_BYTES, s, ta, tb, tb3, td, td3, a);
   } else {
@@ -657,14 +645,15 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     // persistent: as many pairs as can be co-resident (a TPC with one usable SM cannot host a pair)
-    static int pairs = 0;
-    if (pairs == 0) {
+    int pairs = 0;
+    if (!dev_cache_get((const void*)kern, -1, &pairs)) {
       cfg.gridDim = dim3(num_sms() & ~1);
       cfg.numAttrs = 1;
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = num_sms() / 2;
       cudaGetLastError();
       pairs = std::min(n, num_sms() / 2);
+      dev_cache_put((const void*)kern, -1, pairs);
       if (std::getenv("LUFFY_VERBOSE")) std::fprintf(stderr, "[luffy] gemm pair grid: %d co-resident pairs\n", pairs);
     }
     cfg.gridDim = dim3(2 * pairs);

@@ -274,14 +274,8 @@ int launch_gram_tc(luffy_layer* L, float h, void* s) {
   a.E = L->E;
   a.d = L->d;
   a.c2h = 2.0 * (double)h - 1.0;
-  static bool attr = false;
-  if (!attr) {
-    LUFFY_CUDA_TRY(cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
-  }
-  int dev = 0, sms = 0;
-  LUFFY_CUDA_TRY(cudaGetDevice(&dev));
-  LUFFY_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  LUFFY_CUDA_TRY(smem_optin((const void*)gram_tc_kernel, SMEM_BYTES));
+  const int sms = device_sms();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sms & ~1);
   cfg.blockDim = dim3(THREADS);

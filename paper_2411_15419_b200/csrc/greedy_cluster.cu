@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
 template <int CS>
 int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int nclusters, cudaStream_t st) {
   auto kern = greedy_cluster_kernel<CS>;
-  LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LUFFY_CUDA_TRY(smem_optin((const void*)kern, (int)smem));
   if (CS > 8) LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(L->E, std::max(1, std::min(nclusters, 32))) * CS);
@@ -293,8 +293,14 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   // (the control block is zeroed by gather_norm_kernel, which precedes the Gram)
   // Cluster size: 16 CTAs when every group gets its own co-resident cluster, else 8 (twice as many clusters;
   // the groups are scheduled by cost onto them).  On B200 only 7 clusters of 16 (or of 12) and 15 of 8 fit.
-  static int cs = 0, ncl = 0;
-  if (cs == 0) {
+  // the choice depends on (device, shared-memory size, E): cached per device under that key
+  static const char tag = 0;
+  int cs = 0, ncl = 0, packed = 0;
+  const int64_t ckey = ((int64_t)smem << 16) | L->E;
+  if (dev_cache_get(&tag, ckey, &packed)) {
+    cs = packed >> 16;
+    ncl = packed & 0xffff;
+  } else {
     auto coresident = [&](auto kern, int size) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -328,6 +334,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
     if (std::getenv("LUFFY_VERBOSE"))
       std::fprintf(stderr, "[luffy] greedy clusters co-resident: %d x16, %d x12, %d x8 CTAs (smem %zu); using %d x %d\n",
                    n16, n12, n8, smem, ncl, cs);
+    dev_cache_put(&tag, ckey, (cs << 16) | (ncl & 0xffff));
   }
   if (cs == 16) return launch_cluster<16>(L, nmax, smem, cache_words, ncl, st);
   if (cs == 12) return launch_cluster<12>(L, nmax, smem, cache_words, ncl, st);

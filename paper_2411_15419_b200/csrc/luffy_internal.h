@@ -91,6 +91,9 @@ struct luffy_layer {
   uint8_t x_handle[64];
   void* x_peer_base_h[64];  // host: mapped base of every rank's region (own at [rank])
   bool x_open;
+  uint32_t* x_err_h;     // [2] mapped pinned host memory: first timed-out exchange wait (phase + 1, seq)
+  uint32_t* x_err_d;     // its device alias
+  uint64_t x_timeout_ns; // bound of every cross-rank wait (LUFFY_EXCHANGE_TIMEOUT_MS, luffy_layer_set_exchange_timeout)
   void* x_recv[2];     // own buffers inside the region
   void* x_gathered;
   void* x_dexp;

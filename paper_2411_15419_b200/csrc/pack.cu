@@ -672,11 +672,7 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
     const char* v = std::getenv("LUFFY_LAYOUT_SMEM");
     return v && v[0] == '0' ? 0 : 40000;
   }();
-  static bool attr = false;
-  if (!attr) {
-    LUFFY_CUDA_TRY(cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000 * 4));
-    attr = true;
-  }
+  LUFFY_CUDA_TRY(smem_optin((const void*)layout_kernel, 40000 * 4));
   launch_pdl(layout_kernel, L->E, 1024, (size_t)std::max(cur_cap, 1) * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
                                                  L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out,

@@ -782,11 +782,7 @@ int route_dispatch(const luffy_layer* L, const void* x, const float* wg, int32_t
   if (L->E <= 32 && L->d % 256 == 0) {
     const int fb = (L->T + 31) / 32;
     if (L->E <= 8) {
-      static bool attr = false;
-      if (!attr) {
-        LUFFY_CUDA_TRY(cudaFuncSetAttribute(route_e8_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-        attr = true;
-      }
+      LUFFY_CUDA_TRY(smem_optin((const void*)route_e8_kernel<T>, 65536));
       launch_pdl(route_e8_kernel<T>, fb, 256, 65536, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
                  idx_out, w_out);
     } else if (L->E <= 16)

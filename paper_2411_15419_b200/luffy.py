@@ -26,7 +26,7 @@ EXPORTED = [
     "luffy_layer_rows", "luffy_route", "luffy_condense", "luffy_dispatch", "luffy_expert_ffn",
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
-    "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan",
+    "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan", "luffy_layer_set_exchange_timeout",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -95,7 +95,8 @@ def _load():
         "luffy_attention_cost": (I64, [I64, I64, I64]),
         "luffy_adaptive_threshold": (I32, [ctypes.c_double, ctypes.c_double, I32, P]),
         "luffy_debug_copy": (I32, [P, I32, P, ctypes.POINTER(SZ), P]),
-        "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P]),
+        "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P, P, I64, P, P]),
+        "luffy_layer_set_exchange_timeout": (I32, [P, I64]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -291,16 +292,28 @@ def luffy_debug_gemm(kind, dtype, epi, A, B, B3, D, aux, D3, Msplit, off, G, max
 
 
 def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
-    """Host-side dispatch/combine plan: (send_off [E+1], recv_off [E_l+1], send_rows_to [P], recv_rows_from [P])."""
+    """Dispatch/combine plan (the same code the device count exchange runs, csrc/xplan.h): dict with
+    send_off [E+1], recv_off [E_l+1], dst_base [E], rank_of / slot_of [recv_off[-1]], send_rows_to [P],
+    recv_rows_from [P]."""
     counts_all = np.ascontiguousarray(counts_all, dtype=np.int32)
     El = num_experts // world
     so = np.empty(num_experts + 1, np.int32)
     ro = np.empty(El + 1, np.int32)
+    db = np.empty(num_experts, np.int32)
+    cap = int(counts_all.astype(np.int64).sum()) + El * ROW_ALIGN
+    rk = np.empty(max(cap, 1), np.int32)
+    sl = np.empty(max(cap, 1), np.int32)
     st = np.empty(world, np.int64)
     rf = np.empty(world, np.int64)
     _check(LIB.luffy_exchange_plan(world, rank, num_experts, counts_all.ctypes.data, so.ctypes.data, ro.ctypes.data,
-                                   st.ctypes.data, rf.ctypes.data))
-    return so, ro, st, rf
+                                   db.ctypes.data, rk.ctypes.data, sl.ctypes.data, cap, st.ctypes.data, rf.ctypes.data))
+    n = int(ro[-1])
+    return dict(send_off=so, recv_off=ro, dst_base=db, rank_of=rk[:n], slot_of=sl[:n], send_rows_to=st,
+                recv_rows_from=rf)
+
+
+def luffy_layer_set_exchange_timeout(layer, ms: int):
+    _check(LIB.luffy_layer_set_exchange_timeout(layer, int(ms)))
 
 
 def luffy_sequence_rows(layer, seq_len, world, stream):

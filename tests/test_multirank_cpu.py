@@ -1,5 +1,8 @@
 """World-size-2 gloo test (CPU) of the N>1 host logic: the exchange plan exported by the C ABI
-(luffy_exchange_plan) drives a simulated dispatch and combine over torch.distributed (gloo); the rows each
+(luffy_exchange_plan -- the same __host__ __device__ code, csrc/xplan.h, the device count exchange runs)
+drives a simulated dispatch (rows pushed to dst_base[e] + slot offset, as the pack-and-push kernel does)
+and combine (row r back to (rank_of[r], slot_of[r]), as the GEMM2 epilogue does) over torch.distributed
+(gloo); the rows each
 rank receives must be exactly the oracle's receive layout (expert-major, source rank ascending, then the
 source's send order; reading R15), padding rows zero, and the combine must return every row to its slot."""
 import os
@@ -50,7 +53,9 @@ def _worker(rank, world, port, q):
         gathered = [torch.empty_like(cnt) for _ in range(world)]
         dist.all_gather(gathered, cnt)
         counts_all = torch.stack(gathered).numpy()
-        send_off, recv_off, send_to, recv_from = L.luffy_exchange_plan(world, rank, E, counts_all)
+        plan = L.luffy_exchange_plan(world, rank, E, counts_all)
+        send_off, recv_off, dst_base = plan["send_off"], plan["recv_off"], plan["dst_base"]
+        send_to, recv_from = plan["send_rows_to"], plan["recv_rows_from"]
         # send layout: padded expert segments of this rank's representatives
         send = np.zeros((send_off[-1], d), np.float32)
         dense = 0
@@ -58,32 +63,42 @@ def _worker(rank, world, port, q):
             n = int(pk.counts[e])
             send[send_off[e]:send_off[e] + n] = X[pk.perm[dense:dense + n]]
             dense += n
-        # dispatch over gloo following the plan
+        # dispatch as the device push does it: send slot s of expert e -> row dst_base[e] + s - send_off[e]
+        # of the owner's expert layout (rows and their destination row indices travel over gloo)
+        def exchange(out_rows, out_idx):
+            """out_rows[p] / out_idx[p]: rows and destination row indices for peer p -> what peers sent me."""
+            cnt_out = torch.tensor([len(out_idx[p]) for p in range(world)], dtype=torch.int64)
+            cnt_in = [torch.empty(world, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(cnt_in, cnt_out)
+            reqs, got = [], {}
+            for p in range(world):
+                n_in = int(cnt_in[p][rank])
+                if p == rank:
+                    got[p] = (np.asarray(out_idx[p], np.int64), np.asarray(out_rows[p], np.float32).reshape(-1, d))
+                    continue
+                if len(out_idx[p]):
+                    reqs.append(dist.isend(torch.tensor(np.asarray(out_idx[p], np.int64)), p))
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(out_rows[p], np.float32).reshape(-1, d)), p))
+                ib, rb = torch.empty(n_in, dtype=torch.int64), torch.empty(n_in, d)
+                if n_in:
+                    reqs.append(dist.irecv(ib, p))
+                    reqs.append(dist.irecv(rb, p))
+                got[p] = (ib, rb)
+            for rq in reqs:
+                rq.wait()
+            return {p: (np.asarray(v[0]), np.asarray(v[1])) for p, v in got.items()}
+
+        rows_to = {p: [] for p in range(world)}
+        idx_to = {p: [] for p in range(world)}
+        for e in range(E):
+            p = e // El
+            for s_ in range(int(send_off[e]), int(send_off[e]) + int(pk.counts[e])):
+                rows_to[p].append(send[s_])
+                idx_to[p].append(int(dst_base[e]) + s_ - int(send_off[e]))
         recv = np.zeros((recv_off[-1], d), np.float32)
-        reqs, bufs = [], []
-        for p in range(world):
-            chunks = [send[send_off[p * El + el]:send_off[p * El + el] + counts_all[rank, p * El + el]] for el in range(El)]
-            out = torch.from_numpy(np.ascontiguousarray(np.concatenate(chunks))) if chunks else torch.zeros(0, d)
-            assert out.shape[0] == send_to[p]
-            inb = torch.empty(int(recv_from[p]), d)
-            if p == rank:
-                inb.copy_(out)
-            else:
-                if out.shape[0]:
-                    reqs.append(dist.isend(out, p))
-                if inb.shape[0]:
-                    reqs.append(dist.irecv(inb, p))
-            bufs.append(inb)
-        for rq in reqs:
-            rq.wait()
-        for p in range(world):
-            o = 0
-            for el in range(El):
-                e = rank * El + el
-                n = int(counts_all[p, e])
-                row = recv_off[el] + int(counts_all[:p, e].sum())
-                recv[row:row + n] = bufs[p][o:o + n].numpy()
-                o += n
+        for p, (ri, rr) in exchange(rows_to, idx_to).items():
+            assert len(ri) == recv_from[p]
+            recv[ri] = rr
         # expected: the oracle's receive layout built from every rank's pack
         blocks, off = O.recv_layout(counts_all.astype(np.int64), rank, E, world)
         exp_rows = []
@@ -96,36 +111,20 @@ def _worker(rank, world, port, q):
         ok = np.array_equal(got, expected.astype(np.float32))
         pad_zero = all(not recv[recv_off[el] + int(counts_all[:, rank * El + el].sum()):recv_off[el + 1]].any()
                        for el in range(El))
-        # combine: expert side returns (2 * row) to the source's slots
-        ret_send = {p: [] for p in range(world)}
-        for el in range(El):
-            e = rank * El + el
-            for p in range(world):
-                row = recv_off[el] + int(counts_all[:p, e].sum())
-                ret_send[p].append(2.0 * recv[row:row + int(counts_all[p, e])])
+        # combine as the GEMM2 epilogue does it: expert-layout row r -> (rank_of[r], slot_of[r]); returns 2*row
+        rank_of, slot_of = plan["rank_of"], plan["slot_of"]
+        pad_rows = rank_of < 0
+        pad_ok = bool(np.all(slot_of[pad_rows] == -1))
+        rows_to = {p: [] for p in range(world)}
+        idx_to = {p: [] for p in range(world)}
+        for r in np.nonzero(~pad_rows)[0]:
+            rows_to[int(rank_of[r])].append(2.0 * recv[r])
+            idx_to[int(rank_of[r])].append(int(slot_of[r]))
         gathered_rows = np.zeros_like(send)
-        reqs, bufs = [], {}
-        for p in range(world):
-            out = torch.from_numpy(np.ascontiguousarray(np.concatenate(ret_send[p])))
-            inb = torch.empty(int(send_to[p]), d)
-            if p == rank:
-                inb.copy_(out)
-            else:
-                if out.shape[0]:
-                    reqs.append(dist.isend(out, p))
-                if inb.shape[0]:
-                    reqs.append(dist.irecv(inb, p))
-            bufs[p] = inb
-        for rq in reqs:
-            rq.wait()
-        for p in range(world):
-            o = 0
-            for el in range(El):
-                e = p * El + el
-                n = int(counts_all[rank, e])
-                gathered_rows[send_off[e]:send_off[e] + n] = bufs[p][o:o + n].numpy()
-                o += n
-        comb_ok = np.array_equal(gathered_rows, 2.0 * send)
+        for p, (ri, rr) in exchange(rows_to, idx_to).items():
+            assert len(ri) == send_to[p]
+            gathered_rows[ri] = rr
+        comb_ok = np.array_equal(gathered_rows, 2.0 * send) and pad_ok
         conserve = int(counts_all.sum())
         q.put((rank, bool(ok), bool(pad_zero), bool(comb_ok), int(recv_from.sum()), conserve))
     finally:

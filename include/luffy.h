@@ -95,6 +95,8 @@ typedef struct luffy_layer luffy_layer; /* per MoE layer call chain: saved routi
 typedef struct {
   int64_t copies;                 /* T * k token copies */
   int64_t reps;                   /* representatives R (rows that are dispatched and run by experts) */
+  int64_t ambiguous_pairs;        /* pairs i < j of a group with |s_ij - h| <= 1e-5 (R18), from the fp32 Gram */
+  int64_t near_tie_tokens;        /* tokens whose k+1 largest logits have an adjacent gap <= 1e-5 max(1,|l_1|) (R2) */
   int32_t rounds;                 /* parallel selection rounds used */
   int32_t reps_per_expert[LUFFY_MAX_EXPERTS];
   int32_t copies_per_expert[LUFFY_MAX_EXPERTS];
@@ -152,7 +154,9 @@ LUFFY_API luffy_status luffy_route(luffy_layer* layer, const void* x, const floa
  * zero vectors have no edges (R7); greedy on the dynamic residual degree with ties to the lowest token
  * (R8), computed exactly by parallel 2-hop rounds.  h > 1 disables condensation (identity map).
  * Output rep [T, k] int32: the token whose copy represents copy (t, j) in expert topk_idx[t, j]
- * (rep[rep] == rep).  `stats` (host, nullable) is filled synchronously when non-NULL ([sync] then). */
+ * (rep[rep] == rep).  `stats` (host, nullable) is filled synchronously when non-NULL ([sync] then); the
+ * near-tie report recomputes candidate logits from x and the w_gate passed to this step's luffy_route,
+ * which must still be valid. */
 LUFFY_API luffy_status luffy_condense(luffy_layer* layer, const void* x, float h, int32_t* rep,
                             luffy_condense_stats* stats, void* stream);
 
@@ -252,6 +256,13 @@ typedef enum {
 /* Synchronously copies an internal array of the layer's current forward to host memory `dst` (host).
  * *bytes (in: capacity of dst, out: bytes of the item).  [sync] */
 LUFFY_API luffy_status luffy_debug_copy(luffy_layer* layer, int32_t item, void* dst, size_t* bytes, void* stream);
+
+/* Registers a device buffer (16-byte aligned, capacity in floats; NULL unregisters) that every following
+ * luffy_condense fills with the fp32 similarity Gram the threshold is applied to (tests: A18's
+ * max |s_gpu - s_ref| check): group e occupies floats [adjoff[e] * 32, + npad_e^2) as a dense row-major
+ * [npad_e][npad_e] matrix (npad_e = goff[e+1] - goff[e]); only 32x32 blocks with column block >= row
+ * block are written (the matrix is symmetric); blocks beyond the capacity are skipped. */
+LUFFY_API luffy_status luffy_debug_gram_dump(luffy_layer* layer, float* dst, size_t capacity_floats);
 
 /* Grouped GEMM used by the expert FFN, exposed for unit tests.  kind 0 ("rows"): D[r, :N] over the
  * row segments off[0..G] (device, multiples of LUFFY_ROW_ALIGN) = A[r, :K] B_g^T with the epilogue `epi`

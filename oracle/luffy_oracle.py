@@ -22,6 +22,8 @@ Parity status per function (what pins it, tests/test_oracle_*.py):
                         graphs; soundness / idempotence / coverage invariants.  The CHOICE of the
                         dynamic-degree reading (R8) is not discriminated by the paper: "parity
                         unpinned" for that reading only (R8).
+  band_components       pinned: hand-built graphs (paths, triangles, singletons) and 200 random graphs vs
+                        a transitive-closure reference (tests/test_oracle_pins.py::test_band_components_pins)
   pack / recv_layout    pinned: conservation, stable order == sorted() brute force
   expert_ffn            pinned: dense torch fp64 matmul + torch GeLU(erf) / SiLU
   layer_forward/backward pinned: h>1 equals a looped dense top-k MoE under torch fp64 autograd;

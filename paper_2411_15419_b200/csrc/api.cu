@@ -159,6 +159,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->alive = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->win = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);
+  o->stat64 = cv.take<uint64_t>(4);
   o->nrep = cv.take<int32_t>(m.E);
   o->gnrep = cv.take<int32_t>(m.E);
   o->soff = cv.take<int32_t>(m.E + 1);
@@ -589,6 +590,7 @@ luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int
   LUFFY_ALIGNED(w_gate);
   if (T < 1 || T > L->Tmax) return fail(LUFFY_E_INVALID, "need 0 < T <= max_tokens");
   L->T = T;
+  L->wg_route = w_gate;
   L->stage = 0;
   L->seq += 1;  // a new forward step (every rank calls in lockstep)
   L->S = 0;
@@ -608,6 +610,13 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
   LUFFY_STAGE(L, 1, "luffy_condense");
   if (!(h == h)) return fail(LUFFY_E_INVALID, "h is NaN");
   L->h = h;
+  unsigned long long* band = nullptr;  // stats: near-threshold pair count from the Gram epilogue
+  if (stats) {
+    LUFFY_CHECK(cudaMemsetAsync(L->stat64, 0, 4 * sizeof(uint64_t), static_cast<cudaStream_t>(stream)), "stats");
+    band = reinterpret_cast<unsigned long long*>(L->stat64);
+    LUFFY_CHECK(launch_near_tie(L, x, L->wg_route, reinterpret_cast<unsigned long long*>(L->stat64) + 1, stream),
+                "luffy_condense/near_tie");
+  }
   LUFFY_CHECK(launch_group_build(L, x, stream), "luffy_condense/group_build");
   if (h > 1.0f) {
     L->has_adj = false;
@@ -615,8 +624,8 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
   } else {
     L->has_adj = true;
     // bf16: tcgen05 Gram; fp32: exact SIMT FFMA Gram
-    if (L->dtype == LUFFY_BF16) LUFFY_CHECK(launch_gram_tc(L, h, stream), "luffy_condense/gram");
-    else LUFFY_CHECK(launch_gram_simt(L, h, stream), "luffy_condense/gram");
+    if (L->dtype == LUFFY_BF16) LUFFY_CHECK(launch_gram_tc(L, h, band, stream), "luffy_condense/gram");
+    else LUFFY_CHECK(launch_gram_simt(L, h, band, stream), "luffy_condense/gram");
     LUFFY_CHECK(launch_greedy(L, stream), "luffy_condense/greedy");
   }
   LUFFY_CHECK(launch_pack(L, x, nullptr, rep, stream), "luffy_condense/layout");
@@ -625,6 +634,8 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     std::vector<int32_t> gc(L->E), nr(L->E);
     uint32_t rounds = 0;
+    uint64_t s64[4] = {0, 0, 0, 0};
+    LUFFY_CHECK(cudaMemcpyAsync(s64, L->stat64, sizeof(s64), cudaMemcpyDeviceToHost, st), "stats");
     LUFFY_CHECK(cudaMemcpyAsync(gc.data(), L->gcnt, sizeof(int32_t) * L->E, cudaMemcpyDeviceToHost, st), "stats");
     LUFFY_CHECK(cudaMemcpyAsync(nr.data(), L->nrep, sizeof(int32_t) * L->E, cudaMemcpyDeviceToHost, st), "stats");
     LUFFY_CHECK(cudaMemcpyAsync(&rounds, L->ctrl + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, st), "stats");
@@ -637,6 +648,8 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
       stats->reps_per_expert[e] = nr[e];
     }
     stats->rounds = (int32_t)rounds;
+    stats->ambiguous_pairs = (int64_t)s64[0];
+    stats->near_tie_tokens = (int64_t)s64[1];
   }
   return LUFFY_OK;
 }
@@ -1010,6 +1023,14 @@ luffy_status luffy_migration_out_tokens(const luffy_layer* L, int32_t* home_rank
     if (home_rank) home_rank[i] = m[i * (2 + L->k)];
     if (home_token) home_token[i] = m[i * (2 + L->k) + 1];
   }
+  return LUFFY_OK;
+}
+
+luffy_status luffy_debug_gram_dump(luffy_layer* L, float* dst, size_t capacity_floats) {
+  LUFFY_NEED(L);
+  if (dst && reinterpret_cast<uintptr_t>(dst) % 16) return fail(LUFFY_E_INVALID, "luffy_debug_gram_dump: dst must be 16-byte aligned");
+  L->dbg_gram = dst;
+  L->dbg_gram_cap = dst ? capacity_floats : 0;
   return LUFFY_OK;
 }
 

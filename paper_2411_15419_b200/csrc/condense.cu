@@ -194,7 +194,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg, const double* __restrict__ gnorm,
                                                         const int32_t* __restrict__ goff, const int32_t* __restrict__ gcnt,
                                                         const int64_t* __restrict__ adjoff, int E, int d, double c2h,
-                                                        uint32_t* __restrict__ adj) {
+                                                        uint32_t* __restrict__ adj, float* __restrict__ gdump,
+                                                        int64_t gdump_cap, unsigned long long* __restrict__ band) {
   pdl_enter();
   constexpr int TS = 64, BK = 32;
   __shared__ float As[BK][TS + 4];
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
     }
     __syncthreads();
   }
+  int nband = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int li = I * TS + ty * 4 + i;
@@ -240,10 +242,17 @@ __global__ void __launch_bounds__(256) gram_simt_kernel(const T* __restrict__ xg
     for (int j = 0; j < 4; ++j) {
       const int lj = J * TS + tx * 4 + j;
       const double nj = gnorm[goff_s[e] + lj];
-      bool on = li < n && lj < n && li != lj && ni > 0.0 && nj > 0.0 && (double)acc[i][j] >= c2h * ni * nj;
+      const bool pair = li < n && lj < n && li != lj && ni > 0.0 && nj > 0.0;
+      bool on = pair && (double)acc[i][j] >= c2h * ni * nj;
       edge[ty * 4 + i][tx * 4 + j] = on;
+      if (band && pair && li < lj && fabs((double)acc[i][j] - c2h * ni * nj) <= 2e-5 * ni * nj) ++nband;
+      if (gdump) {  // debug export of the accumulator (same layout as the tcgen05 Gram's)
+        const int64_t o = adjoff[e] * 32 + (int64_t)li * npad + lj;
+        if (o < gdump_cap) gdump[o] = acc[i][j];
+      }
     }
   }
+  if (band && nband) atomicAdd(band, (unsigned long long)nband);
   __syncthreads();
   uint32_t* base = adj + adjoff[e];
   const int t = threadIdx.x;
@@ -521,17 +530,19 @@ int launch_identity_rep(luffy_layer* L, void* s) {
   return 0;
 }
 
-int launch_gram_simt(luffy_layer* L, float h, void* s) {
+int launch_gram_simt(luffy_layer* L, float h, unsigned long long* band, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int64_t nt = L->Cpad_max / 64;
   const int64_t tiles = nt * (nt + 1) / 2;  // upper bound over any split of the rows into groups
   const double c2h = 2.0 * (double)h - 1.0;
   if (L->dtype == LUFFY_BF16)
     launch_pdl(gram_simt_kernel<bf16>, (unsigned)tiles, 256, 0, st, static_cast<const bf16*>(L->xg), L->gnorm, L->goff, L->gcnt,
-                                                            L->adjoff, L->E, L->d, c2h, L->adj);
+                                                            L->adjoff, L->E, L->d, c2h, L->adj, L->dbg_gram,
+                                                            (int64_t)L->dbg_gram_cap, band);
   else
     launch_pdl(gram_simt_kernel<float>, (unsigned)tiles, 256, 0, st, static_cast<const float*>(L->xg), L->gnorm, L->goff, L->gcnt,
-                                                             L->adjoff, L->E, L->d, c2h, L->adj);
+                                                             L->adjoff, L->E, L->d, c2h, L->adj, L->dbg_gram,
+                                                            (int64_t)L->dbg_gram_cap, band);
   LUFFY_LAUNCHED();
   return 0;
 }

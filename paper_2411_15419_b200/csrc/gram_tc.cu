@@ -33,6 +33,9 @@ struct GramArgs {
   uint32_t* adj;
   int E, d;
   double c2h;
+  float* gdump;                   // debug (nullable): fp32 G of every computed block, group e at float
+  int64_t gdump_cap;              //   offset adjoff[e] * 32, dense [npad_e][npad_e] row-major (j-block >= i-block)
+  unsigned long long* band;       // stats (nullable): pairs i < j with |s_ij - h| <= 1e-5 (reading R18)
 };
 
 // pair tiles (I, J), J >= I, over blocks of 2 TS rows of each group
@@ -198,6 +201,29 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
         // 1.8e-7 (relative) of the fp64 one, so outside the band [p_lo, p_hi) = thr*nj*(1 -/+ 1e-6) the
         // fp32 comparison with either bound IS the fp64 decision; the rare elements inside the band are
         // re-decided in fp64 (two compares per element instead of a compare and an |G - p| test)
+        if (a.gdump != nullptr) {  // debug export of the accumulator (tests: max |s_gpu - s_ref|, A18)
+          const int64_t o = a.adjoff[e] * 32 + (int64_t)li * npad + j0;
+          if (o + 32 <= a.gdump_cap) {
+            float4* dst = reinterpret_cast<float4*>(a.gdump + o);
+#pragma unroll
+            for (int b4 = 0; b4 < 8; ++b4)
+              dst[b4] = make_float4(__uint_as_float(r[4 * b4]), __uint_as_float(r[4 * b4 + 1]),
+                                    __uint_as_float(r[4 * b4 + 2]), __uint_as_float(r[4 * b4 + 3]));
+          }
+        }
+        if (a.band != nullptr) {  // near-threshold pairs: |G - (2h-1) n_i n_j| <= 2e-5 n_i n_j  <=>  |s - h| <= 1e-5
+          const float blo = (float)((a.c2h - 2e-5) * ni), bhi = (float)((a.c2h + 2e-5) * ni);
+          uint32_t bw = 0;
+#pragma unroll
+          for (int b = 0; b < 32; ++b) {
+            const float g = __uint_as_float(r[b]), nv = njs[b];
+            bw |= (uint32_t)(g >= blo * nv && g <= bhi * nv) << b;
+          }
+          bw &= rowok ? colok : 0u;
+          if (j0 == i0) bw &= (lane == 31) ? 0u : (0xffffffffu << (lane + 1));
+          const int c = __reduce_add_sync(0xffffffffu, __popc(bw));
+          if (lane == 0 && c) atomicAdd(a.band, (unsigned long long)c);
+        }
         uint32_t word = 0, lo = 0;
 #pragma unroll
         for (int b4 = 0; b4 < 8; ++b4) {
@@ -260,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
 int make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
                    uint32_t box_outer);
 
-int launch_gram_tc(luffy_layer* L, float h, void* s) {
+int launch_gram_tc(luffy_layer* L, float h, unsigned long long* band, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   // (adjoff and the greedy control block are prepared by gather_norm_kernel)
   CUtensorMap tx;
@@ -274,6 +300,9 @@ int launch_gram_tc(luffy_layer* L, float h, void* s) {
   a.E = L->E;
   a.d = L->d;
   a.c2h = 2.0 * (double)h - 1.0;
+  a.gdump = L->dbg_gram;
+  a.gdump_cap = (int64_t)L->dbg_gram_cap;
+  a.band = band;
   LUFFY_CUDA_TRY(smem_optin((const void*)gram_tc_kernel, SMEM_BYTES));
   const int sms = device_sms();
   cudaLaunchConfig_t cfg{};

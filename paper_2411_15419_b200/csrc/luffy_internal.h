@@ -78,6 +78,11 @@ struct luffy_layer {
   // ---- backward scratch
   float* dl;          // [Tmax, E] gate logit gradients
   float* wg_part;     // [kWgParts, E, d]
+  const float* wg_route;  // w_gate of this step's luffy_route (the stats' near-tie report reads it)
+  uint64_t* stat64;   // [4] device stats of the last condense: [0] near-threshold pairs, [1] near-tie tokens
+  // ---- debug export
+  float* dbg_gram;    // caller's device buffer for the fp32 Gram (luffy_debug_gram_dump), nullable
+  size_t dbg_gram_cap;  // its capacity in floats
   // ---- host-side state
   int T;
   float h;
@@ -143,8 +148,9 @@ struct Ctx;
 int launch_route(const luffy_layer* L, const void* x, const float* wg, int32_t* idx_out, float* w_out, void* s);
 int launch_group_build(luffy_layer* L, const void* x, void* s);
 int launch_identity_rep(luffy_layer* L, void* s);
-int launch_gram_simt(luffy_layer* L, float h, void* s);
-int launch_gram_tc(luffy_layer* L, float h, void* s);
+int launch_gram_simt(luffy_layer* L, float h, unsigned long long* band, void* s);
+int launch_gram_tc(luffy_layer* L, float h, unsigned long long* band, void* s);
+int launch_near_tie(const luffy_layer* L, const void* x, const float* wg, unsigned long long* out, void* s);
 int launch_greedy(luffy_layer* L, void* s);
 int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out, void* s);
 int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void* s);

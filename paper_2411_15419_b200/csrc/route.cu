@@ -4,6 +4,8 @@
 // partial dot products with the fp32 gate weights in a fixed order (chunk order, then a butterfly
 // reduction), so the result is bitwise reproducible.  Top-k by (logit desc, expert id asc) via a warp
 // argmax; softmax over all experts is saved for the backward.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace luffy {
@@ -807,6 +809,73 @@ int route_dispatch(const luffy_layer* L, const void* x, const float* wg, int32_t
 }
 
 }  // namespace
+
+// Near-tie report (reading R2, stats only): a token whose k+1 largest logits, in the gate's order (logit
+// desc, expert asc), have an adjacent gap <= 1e-5 * max(1, |l_1|).  One warp per token: the order and a
+// loose screen come from the saved softmax probabilities (log p_a - log p_b = l_a - l_b); only screened
+// tokens recompute their k+1 logits from x and W_g (fp32) for the exact tolerance test.
+template <typename T>
+__global__ void __launch_bounds__(256) near_tie_kernel(const float* __restrict__ probs, const T* __restrict__ x,
+                                                       const float* __restrict__ wg, int T_, int E, int d, int k,
+                                                       unsigned long long* __restrict__ out) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int nk = min(k + 1, E);
+  int cnt = 0;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += (gridDim.x * blockDim.x) >> 5) {
+    int sel[9];
+    float ps[9];
+    float pv[8];  // experts 0..E-1 in chunks of 32 lanes: E <= 256 -> up to 8 values per lane
+    for (int c = 0; c < 8; ++c) pv[c] = (c * 32 + lane < E) ? probs[(size_t)t * E + c * 32 + lane] : -1.f;
+    for (int i = 0; i < nk; ++i) {  // arg-max by (p desc, expert asc), k+1 times
+      float best = -2.f;
+      int be = 0x7fffffff;
+      for (int c = 0; c < 8; ++c) {
+        const int e = c * 32 + lane;
+        if (e < E && pv[c] > best) { best = pv[c]; be = e; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        if (ob > best || (ob == best && oe < be)) { best = ob; be = oe; }
+      }
+      sel[i] = be;
+      ps[i] = best;
+      if ((be & 31) == lane) pv[be >> 5] = -1.f;  // remove
+    }
+    bool screen = false;
+    for (int i = 0; i + 1 < nk; ++i) {
+      const float a = ps[i], b = ps[i + 1];
+      if (b <= 0.f) continue;                       // underflowed runner-up: far from a tie
+      screen |= (logf(a) - logf(b)) <= 1e-3f;
+    }
+    if (!screen) continue;
+    float l[9];
+    for (int i = 0; i < nk; ++i) {
+      float acc = 0.f;
+      for (int c = lane; c < d; c += 32) acc = fmaf(to_f(x[(size_t)t * d + c]), wg[(size_t)sel[i] * d + c], acc);
+      l[i] = warp_sum(acc);
+    }
+    const float tol = 1e-5f * fmaxf(1.f, fabsf(l[0]));
+    bool tie = false;
+    for (int i = 0; i + 1 < nk; ++i) tie |= fabsf(l[i] - l[i + 1]) <= tol;
+    cnt += tie ? 1 : 0;
+  }
+  if (lane == 0 && cnt) atomicAdd(out, (unsigned long long)cnt);
+}
+
+int launch_near_tie(const luffy_layer* L, const void* x, const float* wg, unsigned long long* out, void* s) {
+  cudaStream_t st = static_cast<cudaStream_t>(s);
+  const int blocks = std::max(1, std::min((L->T + 7) / 8, 148 * 8));
+  if (L->dtype == LUFFY_BF16)
+    launch_pdl(near_tie_kernel<bf16>, blocks, 256, 0, st, L->probs, static_cast<const bf16*>(x), wg, L->T, L->E, L->d,
+               L->k, out);
+  else
+    launch_pdl(near_tie_kernel<float>, blocks, 256, 0, st, L->probs, static_cast<const float*>(x), wg, L->T, L->E, L->d,
+               L->k, out);
+  LUFFY_LAUNCHED();
+  return 0;
+}
 
 int launch_route(const luffy_layer* L, const void* x, const float* wg, int32_t* idx_out, float* w_out, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);

@@ -27,6 +27,7 @@ EXPORTED = [
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan", "luffy_layer_set_exchange_timeout",
+    "luffy_debug_gram_dump",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -45,7 +46,8 @@ class Config(ctypes.Structure):
 
 
 class CondenseStats(ctypes.Structure):
-    _fields_ = [("copies", ctypes.c_int64), ("reps", ctypes.c_int64), ("rounds", ctypes.c_int32),
+    _fields_ = [("copies", ctypes.c_int64), ("reps", ctypes.c_int64), ("ambiguous_pairs", ctypes.c_int64),
+                ("near_tie_tokens", ctypes.c_int64), ("rounds", ctypes.c_int32),
                 ("reps_per_expert", ctypes.c_int32 * MAX_EXPERTS),
                 ("copies_per_expert", ctypes.c_int32 * MAX_EXPERTS)]
 
@@ -97,6 +99,7 @@ def _load():
         "luffy_debug_copy": (I32, [P, I32, P, ctypes.POINTER(SZ), P]),
         "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P, P, I64, P, P]),
         "luffy_layer_set_exchange_timeout": (I32, [P, I64]),
+        "luffy_debug_gram_dump": (I32, [P, P, ctypes.c_size_t]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -310,6 +313,14 @@ def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
     n = int(ro[-1])
     return dict(send_off=so, recv_off=ro, dst_base=db, rank_of=rk[:n], slot_of=sl[:n], send_rows_to=st,
                 recv_rows_from=rf)
+
+
+def luffy_debug_gram_dump(layer, buf):
+    """Register a device fp32 tensor (or None) that the following luffy_condense calls fill with the Gram."""
+    if buf is None:
+        _check(LIB.luffy_debug_gram_dump(layer, None, 0))
+    else:
+        _check(LIB.luffy_debug_gram_dump(layer, ctypes.c_void_p(buf.data_ptr()), buf.numel()))
 
 
 def luffy_layer_set_exchange_timeout(layer, ms: int):

@@ -28,8 +28,9 @@ def to_dev(a: np.ndarray, dtype: str):
 
 
 def run_gpu_layer(cfg: workload.LayerConfig, inp: dict, h: float, T: int | None = None, backward: bool = True,
-                  layer=None):
-    """One fwd(+bwd) of the CUDA path at world == 1; returns host arrays and debug exports."""
+                  layer=None, gram_dump: bool = False):
+    """One fwd(+bwd) of the CUDA path at world == 1; returns host arrays and debug exports (with
+    gram_dump: the fp32 Gram the threshold was applied to, per group, via luffy_debug_gram_dump)."""
     from paper_2411_15419_b200 import layer as LY
     from paper_2411_15419_b200 import luffy as L
     X = inp["X"] if T is None else inp["X"][:T]
@@ -42,6 +43,11 @@ def run_gpu_layer(cfg: workload.LayerConfig, inp: dict, h: float, T: int | None 
     w1 = to_dev(inp["W1"], cfg.dtype)
     w2 = to_dev(inp["W2"], cfg.dtype)
     w3 = to_dev(inp["W3"], cfg.dtype) if inp["W3"] is not None else None
+    gbuf = None
+    if gram_dump:
+        C = T * cfg.top_k + cfg.num_experts * ROW_ALIGN
+        gbuf = torch.full((C * C,), float("nan"), dtype=torch.float32, device="cuda")
+        L.luffy_debug_gram_dump(layer.layer, gbuf)
     y = layer.forward(x, wg, w1, w2, w3, h=h, stats=True)
     s = torch.cuda.current_stream().cuda_stream
     res = dict(layer=layer, T=T, idx=layer.idx[:T].cpu().numpy().astype(np.int64),
@@ -53,6 +59,12 @@ def run_gpu_layer(cfg: workload.LayerConfig, inp: dict, h: float, T: int | None 
         res["adjoff"] = L.luffy_debug_copy(layer.layer, "adjoff", s)
         res["adj"] = L.luffy_debug_copy(layer.layer, "adj", s)
     res["recv"] = layer.recv.float().cpu().numpy()
+    if gbuf is not None:
+        L.luffy_debug_gram_dump(layer.layer, None)
+        torch.cuda.synchronize()
+        nfl = int(res["adjoff"][-1]) * 32
+        res["gram"] = gbuf[:nfl].cpu().numpy()
+        del gbuf
     if backward:
         dY = inp["dY"][:T]
         g = layer.backward(to_dev(dY, cfg.dtype), x, wg, w1, w2, w3)
@@ -74,6 +86,19 @@ def group_adjacency(res, e: int) -> np.ndarray:
     words = res["adj"][int(res["adjoff"][e]):int(res["adjoff"][e]) + npad * W].reshape(npad, W)
     bits = np.unpackbits(words.view(np.uint8).reshape(npad, W, 4), axis=2, bitorder="little")
     return bits.reshape(npad, npad)[:n, :n].astype(bool)
+
+
+def group_gram(res, e: int) -> np.ndarray:
+    """fp32 Gram [n_e, n_e] of group e from the debug dump (upper 32x32 blocks written; mirrored here)."""
+    goff, gcnt = res["goff"], res["gcnt"]
+    npad = int(goff[e + 1] - goff[e])
+    n = int(gcnt[e])
+    o = int(res["adjoff"][e]) * 32
+    G = res["gram"][o:o + npad * npad].reshape(npad, npad).astype(np.float64)
+    blk = np.arange(npad) // 32
+    upper = blk[None, :] >= blk[:, None]
+    G = np.where(upper, G, G.T)
+    return G[:n, :n]
 
 
 def dense_perm(res, E: int):

@@ -240,6 +240,46 @@ def test_greedy_invariants():
     assert (O.greedy_condense(clique) == 0).all()                 # one representative per clique
 
 
+def _closure_components(adj: np.ndarray, nodes) -> np.ndarray:
+    """Independent reference for band_components: nodes reachable from `nodes` by transitive closure of
+    the boolean adjacency (repeated squaring of I + A), no graph walk."""
+    n = adj.shape[0]
+    R = np.eye(n, dtype=bool) | adj | adj.T
+    for _ in range(max(1, int(np.ceil(np.log2(max(n, 2)))) + 1)):
+        R = (R.astype(np.int64) @ R.astype(np.int64)) > 0
+    bad = np.zeros(n, bool)
+    for v in nodes:
+        bad |= R[v]
+    return bad
+
+
+def test_band_components_pins():
+    """Reading R18's exclusion set on hand-built graphs (G+ = edges with s >= h - band): exactly the nodes
+    of the connected components that contain a band pair -- no more (other components keep their
+    bit-exact check), no less (a component is independent under the greedy only as a whole)."""
+    A = np.zeros((8, 8), bool)
+    for a, b in [(0, 1), (1, 2), (4, 5), (5, 6), (6, 4)]:   # path 0-1-2, isolated 3, triangle 4-5-6, isolated 7
+        A[a, b] = A[b, a] = True
+    assert not O.band_components(A, []).any()
+    assert np.array_equal(np.nonzero(O.band_components(A, [(1, 2)]))[0], [0, 1, 2])
+    assert np.array_equal(np.nonzero(O.band_components(A, [(0, 1)]))[0], [0, 1, 2])   # an end pair: whole path
+    assert np.array_equal(np.nonzero(O.band_components(A, [(4, 6)]))[0], [4, 5, 6])
+    assert np.array_equal(np.nonzero(O.band_components(A, [(1, 2), (5, 6)]))[0], [0, 1, 2, 4, 5, 6])
+    assert np.array_equal(np.nonzero(O.band_components(A, [(3, 7)]))[0], [3, 7])       # band pair below h: singletons
+    # random graphs vs the transitive-closure reference
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        n = int(rng.integers(1, 40))
+        M = rng.random((n, n)) < rng.uniform(0.0, 0.15)
+        M = np.triu(M, 1)
+        M = M | M.T
+        pairs = [tuple(p) for p in zip(*np.nonzero(np.triu(M, 1)))]
+        pick = [pairs[i] for i in rng.choice(len(pairs), size=min(len(pairs), int(rng.integers(0, 3))), replace=False)] \
+            if pairs else []
+        ref = _closure_components(M, [v for p in pick for v in p])
+        assert np.array_equal(O.band_components(M, pick), ref)
+
+
 def test_condense_duplicates_and_threshold_above_one():
     rng = np.random.default_rng(8)
     X = rng.standard_normal((40, 32))

@@ -44,6 +44,95 @@ def _peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+def _kname(raw: str) -> str:
+    nm = raw.replace("(anonymous namespace)::", "").replace("void ", "").replace("luffy::", "")
+    return nm.split("(")[0].split("<")[0].strip()
+
+
+def kernel_table(step, steps: int = 10):
+    """Warm per-kernel device durations (CUPTI via torch.profiler), PDL off so a kernel's duration excludes
+    its dependency wait (luffy_debug_set_pdl; results are bitwise the same).  {kernel: (launches/step,
+    us/step)} -- measured live in this process, never under ncu."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2411_15419_b200 import luffy as L
+    L.luffy_debug_set_pdl(False)
+    try:
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(steps):
+                step()
+            torch.cuda.synchronize()
+    finally:
+        L.luffy_debug_set_pdl(True)
+    agg = {}
+    for e in prof.events():
+        if e.device_type.name == "CUDA" and "Memcpy" not in e.name and "Memset" not in e.name:
+            a = agg.setdefault(_kname(e.name), [0, 0.0])
+            a[0] += 1
+            a[1] += e.device_time
+    return {k: (c / steps, us / steps) for k, (c, us) in agg.items()}
+
+
+def ffn_work(cfg, R: int, El: int):
+    """Algorithmic work of the six expert-FFN GEMMs of one fwd+bwd: flops 12 R d f (GeLU) /
+    18 R d f (SwiGLU); compulsory HBM bytes: activation rows (bf16) written and read by the GEMMs that
+    need them (recv, act, GeLU'/pre, out, dO, dPre, d_recv), expert weights read twice (fwd, dgrad) and
+    the fp32 weight gradients written once."""
+    d, f, B = cfg.d_model, cfg.d_ffn, 2 if cfg.dtype == "bf16" else 4
+    if cfg.act == "swiglu":
+        flops = 18 * R * d * f
+        rows = R * B * (6 * d + 13 * f)   # pre [2f] 2x, act [f] 3x, dpre [2f] 3x
+        wts = El * d * f * (3 * 2 * B + 3 * 4)
+    else:
+        flops = 12 * R * d * f
+        rows = R * B * (6 * d + 8 * f)
+        wts = El * d * f * (2 * 2 * B + 2 * 4)
+    return flops, rows + wts
+
+
+def mem_kernel_bytes(name: str, cfg, T: int, R: int, Rpad: int, parts: int) -> float | None:
+    """Compulsory HBM bytes of one launch of each memory-side kernel (None: not a memory-side kernel).
+    B = element bytes; C = T k copies; R = representatives (expert rows), Rpad = padded slots."""
+    d, E, k = cfg.d_model, cfg.num_experts, cfg.top_k
+    B = 2 if cfg.dtype == "bf16" else 4
+    C = T * k
+    table = {
+        "route_e8_kernel": T * d * B + E * d * 4 + T * E * 4 + C * 8,
+        "route_fast_kernel": T * d * B + E * d * 4 + T * E * 4 + C * 8,
+        "route_kernel": T * d * B + E * d * 4 + T * E * 4 + C * 8,
+        "gather_norm_kernel": T * d * B + C * d * B + C * 8,             # x once, group rows + norms written
+        "pack_rows_kernel": R * d * B + Rpad * d * B,
+        "uncondense_kernel": R * d * B + T * d * B + C * 8,              # each slot's row once, y written
+        "uncondense_bwd_window_kernel": T * d * B + R * d * B + Rpad * d * B + C * 4,
+        "unpack_bwd_kernel": R * d * B + T * d * B,
+        "route_bwd_fused8_kernel": 3 * T * d * B + T * E * 4 + parts * E * d * 4,
+        "route_bwd_fast_kernel": 2 * T * d * B + T * E * 4,
+        "wg_partial_fast_kernel": T * d * B + parts * E * d * 4,
+        "wg_reduce_kernel": parts * E * d * 4 + E * d * 4,
+    }
+    return table.get(name)
+
+
+def ncu_traffic(config: str, world: int):
+    """DRAM read+write bytes per step of the FFN GEMMs and of the Gram from the per-config ncu --set full
+    capture committed under profiles/ (tools/ncu_capture.sh), or None."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_{config}_n{world}.json")))
+    if not paths:
+        return None, None, None
+    with open(paths[-1]) as fh:
+        ks = json.load(fh)
+    dram = lambda k: k.get("dram_read", 0) + k.get("dram_write", 0)
+    gem = [k for k in ks if k["kernel"].startswith("gemm_tc_kernel")][:6]   # the first step's six GEMMs
+    gr = [k for k in ks if k["kernel"].startswith("gram_tc_kernel")][-1:]
+    return (sum(dram(k) for k in gem) if len(gem) == 6 else None, dram(gr[0]) if gr else None,
+            os.path.relpath(paths[-1], ROOT))
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
 
@@ -138,14 +227,35 @@ def _threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(cfg, inp, ntok: int, reps: int = 1):
+def _host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in out.splitlines() if ln.startswith("Model name")), None)
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "lscpu_model": model, "blas_threads": _threads()}
+
+
+def cpu_baseline(cfg, inp, ntok: int = 0, budget_s: float = 30.0):
+    """The oracle as it stands (numpy fp64, all host cores through BLAS) on the full rank-0 batch when it
+    fits the budget (C1-C3), else on the largest whole-sequence prefix that does (estimated from a
+    256-token probe)."""
+    T = inp["X"].shape[0]
+    if ntok <= 0:
+        probe = min(T, 256)
+        t0 = time.perf_counter()
+        cpu_oracle_step(cfg, inp, probe)
+        per_tok = (time.perf_counter() - t0) / probe
+        ntok = T if per_tok * T <= 2 * budget_s else max(cfg.seq_len, int(budget_s / per_tok) // cfg.seq_len * cfg.seq_len)
+        ntok = min(ntok, T)
     t0 = time.perf_counter()
-    for _ in range(reps):
-        cpu_oracle_step(cfg, inp, ntok)
-    dt = (time.perf_counter() - t0) / reps
+    cpu_oracle_step(cfg, inp, ntok)
+    dt = time.perf_counter() - t0
+    what = "the full" if ntok == T else f"the first {ntok} tokens (whole sequences) of the"
     return {"value": ntok / dt, "unit": UNIT, "cores": _threads(), "kind": "oracle",
-            "sample": f"fwd+bwd of the first {ntok} tokens (of {inp['X'].shape[0]}) of the {cfg.name} rank-0 batch, "
-                      f"numpy fp64, {reps} rep(s), {dt:.2f} s each"}
+            "sample": f"fwd+bwd of {what} {cfg.name} rank-0 batch ({T} tokens), numpy fp64, {dt:.1f} s",
+            "host": _host_info()}
 
 
 def run_reference(args, cfg):
@@ -153,14 +263,17 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     inp = workload.make_layer_inputs(cfg, rank=0)
-    # bounded sample: size each step so that warmup + steps fit in ~150 s of host time
+    # bounded sample: the largest whole-sequence prefix of the rank-0 batch (up to the full batch) such
+    # that the timed steps fit in ~180 s of host time (warm-up steps run a 64-token sample)
+    T = inp["X"].shape[0]
+    probe = min(T, 256)
     t0 = time.perf_counter()
-    cpu_oracle_step(cfg, inp, 64)
-    per_tok = (time.perf_counter() - t0) / 64
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    ntok = args.ref_tokens
-    while ntok > 8 and ntok * per_tok > budget:
-        ntok //= 2
+    cpu_oracle_step(cfg, inp, probe)
+    per_tok = (time.perf_counter() - t0) / probe
+    budget = 180.0 / max(1, args.steps)
+    ntok = min(T, args.ref_tokens) if args.ref_tokens > 0 else T
+    if ntok * per_tok > budget:
+        ntok = max(min(64, T), int(budget / per_tok) // cfg.seq_len * cfg.seq_len or int(budget / per_tok))
     for _ in range(args.warmup):
         cpu_oracle_step(cfg, inp, min(ntok, 64))
     times = []
@@ -176,7 +289,8 @@ def run_reference(args, cfg):
            "config": {"workload": cfg.name, "tokens_per_step": ntok, "E": cfg.num_experts, "k": cfg.top_k,
                       "d_model": cfg.d_model, "d_ffn": cfg.d_ffn, "h": cfg.h},
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": _threads(), "kind": "oracle",
-                            "sample": f"each step: fwd+bwd of the first {ntok} tokens of the {cfg.name} batch"},
+                            "sample": f"each step: fwd+bwd of the first {ntok} tokens (of {T}) of the {cfg.name} "
+                                      f"rank-0 batch, numpy fp64", "host": _host_info()},
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -189,10 +303,11 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--h", type=float, default=None)
     ap.add_argument("--impl", default="luffy", choices=["luffy", "reference"])
-    ap.add_argument("--ref-tokens", type=int, default=256)
-    ap.add_argument("--cpu-tokens", type=int, default=512)
+    ap.add_argument("--ref-tokens", type=int, default=0, help="reference-arm sample per step (0: auto, up to the full batch)")
+    ap.add_argument("--cpu-tokens", type=int, default=0, help="oracle sample (0: full batch if it fits ~30 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ktab", action="store_true", help="skip the CUPTI per-kernel pass (e.g. under ncu)")
     ap.add_argument("--migrate", type=int, default=0,
                     help="world > 1: sequence migration with Alg. 1 candidate-set size q (0 = off)")
     ap.add_argument("--kprof", type=int, default=0, help="also write a warm per-kernel table over this many steps")
@@ -418,27 +533,63 @@ def main():
         frac_remote = 1.0 - rr / rc if rc else None
         frac_all = 1.0 - rtot / ctot
 
-    # ---- roofline of the dominant kernel group (the tcgen05/SIMT grouped expert GEMMs)
+    # ---- rooflines.  Peaks: MEASURED_PEAKS.json burst figures (every timing here is a
+    # sub-second evented / CUPTI window, not a long sustained run).
     peaks, src = _peaks()
-    mult = 18 if cfg.act == "swiglu" else 12
-    flops = mult * R * cfg.d_model * cfg.d_ffn  # algorithmic fwd+bwd FFN flops of this rank's representatives
+    hbm_peak = float(peaks.get("hbm_gbs", 6550.0))
+    tc_peak = float(peaks.get("bf16_tflops", 1672.3)) if cfg.dtype == "bf16" else 80.0
+    tc_src = f"{src} bf16_tflops (burst)" if cfg.dtype == "bf16" else "fp32 SIMT nominal (148 SMs x 128 FFMA x 2 x 2.1 GHz)"
+    # (1) dominant group: the six grouped expert GEMMs (tcgen05), timed with CUDA events around the
+    # luffy_expert_ffn / luffy_expert_ffn_bwd calls (their only launches at world == 1)
+    R_avg = float(R)
     if world > 1:
-        t = torch.tensor([float(flops)], device=dev, dtype=torch.float64)
+        t = torch.tensor([float(R)], device=dev, dtype=torch.float64)
         dist.all_reduce(t)
-        flops = float(t.item()) / world  # per-rank average: each rank runs its experts' rows
+        R_avg = float(t.item()) / world  # each rank runs the rows its experts receive: R on average
+    flops, fbytes = ffn_work(cfg, R_avg, El)
     ffn_ms = breakdown["ffn"] + breakdown["ffn_bwd"]
-    achieved = flops / (ffn_ms / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", 1400.0)) if cfg.dtype == "bf16" else 80.0
-    traffic, tsrc = None, None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemm6_v5.json")
-    if args.config == "C2" and world == 1 and os.path.exists(prof):  # measured on this workload (ncu --set full)
-        with open(prof) as fh:
-            kk = [k for k in json.load(fh) if k["kernel"].startswith("gemm_tc_kernel")]
-        traffic = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in kk)
-        tsrc = "profiles/r01_ncu_gemm6_v5.json: DRAM read+write of the 6 GEMM launches of one step"
-    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "traffic_source": tsrc, "kernel": "expert FFN grouped GEMMs (fwd 2 + bwd 4 launches)",
-            "peak_source": f"{src} bf16_tflops_sustained" if cfg.dtype == "bf16" else "fp32 SIMT nominal"}
+    t_tc, t_hbm = flops / (tc_peak * 1e12), fbytes / (hbm_peak * 1e9)
+    traffic, gram_traffic, tsrc = ncu_traffic(args.config, world)
+    if t_tc >= t_hbm:
+        roof = {"bound": "tensor", "achieved": flops / (ffn_ms / 1e3) / 1e12, "peak": tc_peak, "unit": "TFLOP/s",
+                "peak_source": tc_src}
+    else:
+        roof = {"bound": "hbm", "achieved": fbytes / (ffn_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": f"{src} hbm_gbs (copy)"}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "traffic_source": tsrc,
+                 "kernel": "expert FFN grouped GEMMs (fwd 2 + bwd 4 tcgen05 launches per step)",
+                 "per": "one step (6 launches)", "algorithmic_flops": flops, "algorithmic_bytes": fbytes,
+                 "intensity_flop_per_byte": flops / fbytes, "ridge_flop_per_byte": tc_peak * 1e3 / hbm_peak,
+                 "roofline_time_us": max(t_tc, t_hbm) * 1e6, "measured_us": ffn_ms * 1e3,
+                 "timing": "CUDA events around the two FFN calls, evented pass after the timed region"})
+    # (2) per-kernel table (CUPTI, PDL off): the Gram and the memory-side kernels against their rooflines
+    ktab = kernel_table(step, steps=10) if not (mig or args.no_ktab) else {}
+    gram_roof, mem_roof, shares = None, None, None
+    if ktab:
+        tot = sum(us for _, us in ktab.values())
+        shares = {k: {"us_per_step": round(us, 2), "launches": c, "share": round(us / tot, 4)}
+                  for k, (c, us) in sorted(ktab.items(), key=lambda kv: -kv[1][1])}
+        gk = ktab.get("gram_tc_kernel") or ktab.get("gram_simt_kernel")
+        if gk and cfg.h <= 1.0:
+            n_g = copies_e.astype(np.float64)
+            gflops = float((n_g * (n_g + 1)).sum()) * cfg.d_model  # upper triangle incl. diagonal, 2 flop per MAC
+            gram_roof = {"bound": "tensor", "achieved": gflops / (gk[1] * 1e-6) / 1e12, "peak": tc_peak,
+                         "unit": "TFLOP/s", "frac": gflops / (gk[1] * 1e-6) / 1e12 / tc_peak,
+                         "traffic": gram_traffic, "kernel": "similarity Gram + threshold (gram_tc_kernel)",
+                         "algorithmic_flops": gflops, "measured_us": gk[1], "timing": "CUPTI, warm, PDL off"}
+        parts = (T + 31) // 32
+        mb, mus, used = 0.0, 0.0, []
+        for k_, (c, us) in ktab.items():
+            b_ = mem_kernel_bytes(k_, cfg, T, int(R_avg), int(R_avg) + E * 128, parts)
+            if b_ is not None:
+                mb += b_ * c
+                mus += us
+                used.append(k_)
+        if mus > 0:
+            mem_roof = {"bound": "hbm", "achieved": mb / (mus * 1e-6) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": mb / (mus * 1e-6) / 1e9 / hbm_peak, "traffic": None,
+                        "kernel": "memory-side kernels (sum): " + ", ".join(sorted(used)),
+                        "algorithmic_bytes": mb, "measured_us": mus, "timing": "CUPTI, warm, PDL off"}
 
     if rank == 0:
         cpu = None
@@ -456,7 +607,8 @@ def main():
                "condensed_frac_rows": frac_all, "a2a_bytes_condensed_frac": frac_remote,
                "greedy_rounds": rounds, "reps_rank0": R,
                "migration": ({"q": args.migrate, **mig_stats} if mig else None),
-               "breakdown_ms": breakdown, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+               "breakdown_ms": breakdown, "roofline": roof, "roofline_gram": gram_roof, "roofline_memory": mem_roof,
+               "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches), "host_enqueue_ms_per_step": host_ms, "clocks": clocks}
         print(json.dumps(out), flush=True)
     lay.close()

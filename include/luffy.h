@@ -134,6 +134,11 @@ LUFFY_API const char* luffy_last_error(void);
 /* Number of CUDA kernels this library has launched in this process (for the bench's gpu_launches). */
 LUFFY_API int64_t luffy_launch_count(void);
 
+/* Programmatic dependent launch for every following launch of the process (default on, or off with
+ * LUFFY_PDL=0).  Off: each kernel's device duration excludes the wait for its predecessor, which is what a
+ * per-kernel timing table needs; results are identical either way. */
+LUFFY_API void luffy_debug_set_pdl(int32_t on);
+
 /* Padded row counts after the forward calls (host, valid after luffy_dispatch returned):
  * send_rows = padded rows of this rank's send layout; recv_rows = padded rows of its expert layout. */
 LUFFY_API luffy_status luffy_layer_rows(const luffy_layer* layer, int64_t* send_rows, int64_t* recv_rows);

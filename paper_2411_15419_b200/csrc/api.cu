@@ -64,12 +64,17 @@ int smem_optin(const void* kernel, int bytes) {
   if (e == cudaSuccess) dev_cache_put(kernel, bytes, 1);
   return (int)e;
 }
+// Programmatic dependent launch on/off: LUFFY_PDL=0 in the environment, or luffy_debug_set_pdl at run time
+// (bench.py's per-kernel pass turns it off so a kernel's measured duration excludes its dependency wait).
+static std::atomic<int> g_pdl{-1};
 bool pdl_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("LUFFY_PDL");
-    return !(v && v[0] == '0');
-  }();
-  return on;
+  int v = g_pdl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = std::getenv("LUFFY_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_pdl.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
 }
 
 int gemm_rows_simt(int dtype, int epi, const void* A, const void* B, const void* B3, void* D, void* aux0,
@@ -371,6 +376,7 @@ luffy_status luffy_exchange_plan(int32_t world, int32_t rank, int32_t num_expert
   return LUFFY_OK;
 }
 int64_t luffy_launch_count(void) { return g_launches.load(); }
+void luffy_debug_set_pdl(int32_t on) { g_pdl.store(on ? 1 : 0, std::memory_order_relaxed); }
 
 luffy_status luffy_create(const luffy_config* cfg, luffy_ctx** out) {
   luffy_status st = validate(cfg);

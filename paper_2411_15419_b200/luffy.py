@@ -27,7 +27,7 @@ EXPORTED = [
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan", "luffy_layer_set_exchange_timeout",
-    "luffy_debug_gram_dump",
+    "luffy_debug_gram_dump", "luffy_debug_set_pdl",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -100,6 +100,7 @@ def _load():
         "luffy_exchange_plan": (I32, [I32, I32, I32, P, P, P, P, P, P, I64, P, P]),
         "luffy_layer_set_exchange_timeout": (I32, [P, I64]),
         "luffy_debug_gram_dump": (I32, [P, P, ctypes.c_size_t]),
+        "luffy_debug_set_pdl": (None, [I32]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -313,6 +314,10 @@ def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
     n = int(ro[-1])
     return dict(send_off=so, recv_off=ro, dst_base=db, rank_of=rk[:n], slot_of=sl[:n], send_rows_to=st,
                 recv_rows_from=rf)
+
+
+def luffy_debug_set_pdl(on: bool):
+    LIB.luffy_debug_set_pdl(1 if on else 0)
 
 
 def luffy_debug_gram_dump(layer, buf):

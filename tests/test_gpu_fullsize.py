@@ -41,7 +41,7 @@ def check_condense_full(cfg, inp, res, h):
     E = cfg.num_experts
     groups = O.group_members(res["idx"], E)
     overrides = []
-    rep_report = dict(copies=0, band_pairs=0, excluded=0, max_s_err=0.0)
+    rep_report = dict(copies=0, band_pairs=0, excluded=0, max_s_err=0.0, near_gaps=[])
     for e, (t, j) in enumerate(groups):
         n = t.size
         assert int(res["gcnt"][e]) == n
@@ -75,6 +75,9 @@ def check_condense_full(cfg, inp, res, h):
             plus = s >= h - BAND
         np.fill_diagonal(plus, False)
         bp = list(zip(*np.nonzero(np.triu(inband, 1))))
+        with np.errstate(invalid="ignore"):
+            gap = np.abs(s - h)[np.triu(np.ones_like(inband), 1)]
+        rep_report["near_gaps"].append(gap[gap <= 3 * BAND])
         bad = O.band_components(plus, bp)
         rep_ref = O.greedy_condense(ref)
         assert np.array_equal(rep_ref[~bad], rep_local[~bad]), f"map differs outside band components (group {e})"
@@ -104,8 +107,13 @@ def _run_full(cfg, h, numerics=True, tol_counts=True):
           f"gpu_band_pairs={st.ambiguous_pairs} headline_excluded={rep['excluded']} ({excl_frac:.2%}) "
           f"max|s_gpu-s_ref|={rep['max_s_err']:.3g} errs={errs}")
     # reported counts: the GPU's own near-threshold / near-tie reports agree with the oracle's
+    # (the GPU classifies with its fp32 Gram, off by at most max|s_gpu - s_ref| per pair: its count must lie
+    # between the oracle's counts for the band narrowed / widened by that error)
     if tol_counts:
-        assert abs(int(st.ambiguous_pairs) - rep["band_pairs"]) <= max(2, rep["band_pairs"] // 50)
+        gaps = np.concatenate(rep["near_gaps"]) if rep["near_gaps"] else np.zeros(0)
+        m = rep["max_s_err"] + 1e-6
+        lo, hi = int((gaps <= BAND - m).sum()), int((gaps <= BAND + m).sum())
+        assert lo <= int(st.ambiguous_pairs) <= hi, (lo, int(st.ambiguous_pairs), hi)
         assert abs(int(st.near_tie_tokens) - n_tie) <= max(2, n_tie // 20)
     assert tie_frac < 0.01, "near-tie exclusion above 1% of tokens"
     assert excl_frac < 0.5, "headline exclusion above half of the copies"

@@ -22,6 +22,9 @@ Parity status per function (what pins it, tests/test_oracle_*.py):
                         graphs; soundness / idempotence / coverage invariants.  The CHOICE of the
                         dynamic-degree reading (R8) is not discriminated by the paper: "parity
                         unpinned" for that reading only (R8).
+  fast_measure /        pinned: shortcut set == {s_prev > S1} U {s_prev < S2} and computed weights ==
+  condense_fast         all-pairs cosine (1e-12); S1=1, S2=0 or empty history == condense(); SPEC rule
+                        examples; a pair-loop brute force on tiny groups
   band_components       pinned: hand-built graphs (paths, triangles, singletons) and 200 random graphs vs
                         a transitive-closure reference (tests/test_oracle_pins.py::test_band_components_pins)
   pack / recv_layout    pinned: conservation, stable order == sorted() brute force
@@ -241,6 +244,70 @@ def condense(X: np.ndarray, idx: np.ndarray, E: int, h: float, band: float = 1e-
         rep[t, j] = t[r]
         adjs.append(adj); bands.append(bp); ss.append(s if keep_s else None)
     return Condensation(rep, groups, adjs, bands, ss)
+
+
+# ----------------------------------------------------------------------------------------------
+# Fast similarity measurement with history shortcuts (readings R20, R21)
+# ----------------------------------------------------------------------------------------------
+
+
+def fast_measure(Xg: np.ndarray, H_sub: np.ndarray, S1: float, S2: float):
+    """Fast similarity measurement of one group, steps 2 and 3 (step 1 -- only tokens pushed to
+    the same expert are compared -- is the grouping itself).
+
+    Step 2: with s_{b-1} the pair's finalized weight in the previous block (H_sub, nan = no history:
+    the pair shared no expert there, reading R20), the weight is 1 if s_{b-1} > S1 and 0 if s_{b-1} < S2,
+    and no cosine is computed.  Step 3: the remaining pairs get the normalized cosine (R4).
+    Zero-norm tokens keep no weight (nan) whatever their history (R7).
+    Returns (W [n, n] fp64 finalized weights, nan diagonal; computed [n, n] bool: pairs measured in step 3)."""
+    s = similarity_matrix(Xg)
+    H_sub = np.asarray(H_sub, np.float64)
+    with np.errstate(invalid="ignore"):
+        one = H_sub > S1
+        zero = H_sub < S2
+    W = np.where(one, 1.0, np.where(zero, 0.0, s))
+    valid = ~np.isnan(s)                        # both norms nonzero
+    W = np.where(valid, W, np.nan)
+    np.fill_diagonal(W, np.nan)
+    computed = valid & ~one & ~zero
+    np.fill_diagonal(computed, False)
+    return W, computed
+
+
+def condense_fast(X: np.ndarray, idx: np.ndarray, E: int, h: float, H_prev: np.ndarray, S1: float, S2: float,
+                  band: float = 1e-5, adjacency_override=None):
+    """Token condensation of one block with the fast similarity measurement: per expert group,
+    fast_measure against the previous block's finalized weights H_prev [T, T] (token-pair keyed, nan = none),
+    then the threshold graph (edge iff W >= h) and the highest-degree greedy.  Returns (Condensation,
+    H_new [T, T]: this block's finalized weights of every pair that shares an expert -- the history of the
+    next block, reading R21 -- and the number of pairs measured in step 3 (each unordered pair once per
+    group))."""
+    X = np.asarray(X, np.float64)
+    T, k = idx.shape
+    rep = np.full((T, k), -1, np.int64)
+    groups = group_members(idx, E)
+    H_new = np.full((T, T), np.nan)
+    adjs, bands, ws = [], [], []
+    n_computed = 0
+    for e, (t, j) in enumerate(groups):
+        n = t.size
+        if n == 0:
+            adjs.append(np.zeros((0, 0), bool)); bands.append([]); ws.append(None)
+            continue
+        W, computed = fast_measure(X[t], H_prev[np.ix_(t, t)], S1, S2)
+        n_computed += int(np.triu(computed, 1).sum())
+        if adjacency_override is not None and adjacency_override[e] is not None:
+            adj = np.asarray(adjacency_override[e], bool)
+        else:
+            adj = threshold_graph(W, h)
+        with np.errstate(invalid="ignore"):
+            a, b = np.nonzero(np.triu(computed & (np.abs(W - h) <= band), 1))
+        bands.append(list(zip(a.tolist(), b.tolist())))
+        r = greedy_condense(adj)
+        rep[t, j] = t[r]
+        H_new[np.ix_(t, t)] = W
+        adjs.append(adj); ws.append(W)
+    return Condensation(rep, groups, adjs, bands, ws), H_new, n_computed
 
 
 def band_components(adj_plus: np.ndarray, band_pairs) -> np.ndarray:

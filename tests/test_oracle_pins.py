@@ -240,6 +240,79 @@ def test_greedy_invariants():
     assert (O.greedy_condense(clique) == 0).all()                 # one representative per clique
 
 
+def test_fast_measure_spec_examples():
+    """SPEC S:343-345 and S:371 rule examples (fast similarity measurement)."""
+    rng = np.random.default_rng(3)
+    Xg = rng.standard_normal((7, 16))
+    n = Xg.shape[0]
+    none = np.full((n, n), np.nan)
+    # S1 = 1.0, S2 = 0.0, empty history -> every pair computed: C(n, 2)
+    W, comp = O.fast_measure(Xg, none, 1.0, 0.0)
+    assert int(np.triu(comp, 1).sum()) == n * (n - 1) // 2
+    # history {(a, b): 0.95}, S1 = 0.8 -> weight 1, not computed
+    H = none.copy()
+    H[1, 4] = H[4, 1] = 0.95
+    W, comp = O.fast_measure(Xg, H, 0.8, 0.2)
+    assert W[1, 4] == 1.0 and W[4, 1] == 1.0 and not comp[1, 4]
+    assert int(np.triu(comp, 1).sum()) == n * (n - 1) // 2 - 1
+    # history below S2 -> weight 0
+    H[2, 3] = H[3, 2] = 0.1
+    W, comp = O.fast_measure(Xg, H, 0.8, 0.2)
+    assert W[2, 3] == 0.0 and not comp[2, 3]
+    # rule chain (S:371): a computed 0.9 stored at block b short-circuits to 1 at b+1 with S1 = 0.8
+    X = np.array([[1.0, 0.0], [0.8, 0.6], [0.0, 1.0]])     # cos(0,1) = 0.8 -> s = 0.9
+    idx = np.zeros((3, 1), np.int64)
+    c1, H1, nc1 = O.condense_fast(X, idx, 1, 0.95, np.full((3, 3), np.nan), 0.8, 0.2)
+    assert abs(H1[0, 1] - 0.9) < 1e-12 and nc1 == 3
+    assert (c1.rep[:, 0] == [0, 1, 2]).all()                 # 0.9 < h = 0.95: no edge in block b
+    c2, H2, nc2 = O.condense_fast(X, idx, 1, 0.95, H1, 0.8, 0.2)
+    assert H2[0, 1] == 1.0 and nc2 == 2                        # (0, 1) short-circuits to 1 >= h
+    assert c2.rep[1, 0] == c2.rep[0, 0]
+
+
+def test_fast_measure_brute_force_and_reduction():
+    """Random groups with random history: the shortcut set is exactly {s_prev > S1} U {s_prev < S2}, the
+    computed weights equal the pairwise normalized cosine (a per-pair loop, 1e-12), and with no history
+    condense_fast equals condense (the plain all-pairs path)."""
+    rng = np.random.default_rng(8)
+    for trial in range(30):
+        n, d = int(rng.integers(2, 12)), 8
+        Xg = rng.standard_normal((n, d))
+        if trial % 5 == 0:
+            Xg[0] = 0.0                                        # zero-norm token (R7): never a weight
+        H = rng.uniform(0, 1, (n, n))
+        H = np.triu(H, 1) + np.triu(H, 1).T
+        H[rng.random((n, n)) < 0.3] = np.nan
+        H = np.where(np.isnan(H) | np.isnan(H.T), np.nan, H)
+        np.fill_diagonal(H, np.nan)
+        S1, S2 = 0.7, 0.3
+        W, comp = O.fast_measure(Xg, H, S1, S2)
+        for i in range(n):
+            for j in range(n):
+                if i == j:
+                    continue
+                c = O.normalized_cosine(Xg[i], Xg[j])
+                if math.isnan(c):
+                    assert math.isnan(W[i, j]) and not comp[i, j]
+                elif not math.isnan(H[i, j]) and H[i, j] > S1:
+                    assert W[i, j] == 1.0 and not comp[i, j]
+                elif not math.isnan(H[i, j]) and H[i, j] < S2:
+                    assert W[i, j] == 0.0 and not comp[i, j]
+                else:
+                    assert comp[i, j] and abs(W[i, j] - c) < 1e-12
+    cfg = workload.CONFIGS["C1"]
+    X, _, _ = workload.make_tokens(cfg)
+    r = O.route(X, workload.make_gate(cfg), cfg.top_k, True)
+    T = X.shape[0]
+    plain = O.condense(X, r.idx, cfg.num_experts, 0.9, keep_s=False)
+    fast, H, nc = O.condense_fast(X, r.idx, cfg.num_experts, 0.9, np.full((T, T), np.nan), 0.8, 0.2)
+    assert np.array_equal(plain.rep, fast.rep)
+    assert nc == sum(g[0].size * (g[0].size - 1) // 2 for g in plain.groups)
+    # shortcuts disabled by S1 = 1, S2 = 0 even with full history: identical to the plain path
+    fast2, _, _ = O.condense_fast(X, r.idx, cfg.num_experts, 0.9, H, 1.0, 0.0)
+    assert np.array_equal(plain.rep, fast2.rep)
+
+
 def _closure_components(adj: np.ndarray, nodes) -> np.ndarray:
     """Independent reference for band_components: nodes reachable from `nodes` by transitive closure of
     the boolean adjacency (repeated squaring of I + A), no graph walk."""

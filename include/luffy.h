@@ -87,6 +87,8 @@ typedef struct {
   int32_t max_tokens;     /* T capacity per rank */
   int32_t max_recv_rows;  /* expert-side row capacity incl. padding; 0: world*max_tokens*top_k + E_l*LUFFY_ROW_ALIGN */
   int32_t max_seqs;       /* sequences per rank for sequence migration (world > 1); 0: 256 */
+  int32_t fast_measure;   /* 1: keep the state of the fast similarity measurement with history shortcuts
+                             (luffy_layer_set_history; bf16 only); 0: off */
 } luffy_config;
 
 typedef struct luffy_ctx luffy_ctx;     /* per rank: config and device */
@@ -97,6 +99,8 @@ typedef struct {
   int64_t reps;                   /* representatives R (rows that are dispatched and run by experts) */
   int64_t ambiguous_pairs;        /* pairs i < j of a group with |s_ij - h| <= 1e-5 (R18), from the fp32 Gram */
   int64_t near_tie_tokens;        /* tokens whose k+1 largest logits have an adjacent gap <= 1e-5 max(1,|l_1|) (R2) */
+  int64_t decided_pairs;          /* fast measurement: pairs i < j decided by the previous block (not measured) */
+  int64_t skipped_tiles;          /* fast measurement: 256x256 Gram tiles skipped (every pair decided) */
   int32_t rounds;                 /* parallel selection rounds used */
   int32_t reps_per_expert[LUFFY_MAX_EXPERTS];
   int32_t copies_per_expert[LUFFY_MAX_EXPERTS];
@@ -164,6 +168,17 @@ LUFFY_API luffy_status luffy_route(luffy_layer* layer, const void* x, const floa
  * which must still be valid. */
 LUFFY_API luffy_status luffy_condense(luffy_layer* layer, const void* x, float h, int32_t* rep,
                             luffy_condense_stats* stats, void* stream);
+
+/* Fast similarity measurement, P:359-373 (needs luffy_config.fast_measure = 1, bf16).  Step 2:
+ * in this layer's following luffy_condense calls, a pair of tokens of one expert group whose finalized
+ * weight in `prev`'s last condensation (the previous block) was > S1 gets weight 1, < S2 weight 0, without
+ * measuring it (reading R20: history exists for pairs that shared an expert in prev; the first shared
+ * expert in the row token's top-k order is read); the rest are measured (step 3).  Every condense
+ * of a fast_measure layer records its own finalized weights' classification (> S1, < S2; shortcut values
+ * included, reading R21) for the next block.  Gram tiles whose pairs are all decided are skipped.
+ * prev: NULL (first block: classification only) or a fast_measure layer condensed earlier in the same
+ * step on the SAME tokens in the same order (its T must equal this layer's T).  0 <= S2 < S1 <= 1. */
+LUFFY_API luffy_status luffy_layer_set_history(luffy_layer* layer, const luffy_layer* prev, float S1, float S2);
 
 /* Dispatch phase: packs only the representatives.  world == 1: into `recv` (the send
  * layout is the expert layout).  world > 1 (recv = NULL): the representative counts are pushed to every
@@ -255,7 +270,12 @@ typedef enum {
   LUFFY_DBG_POS = 8,       /* int32 [T, k]  slot of the representative of copy (t, j) */
   LUFFY_DBG_NREP = 9,      /* int32 [E]     representatives per expert */
   LUFFY_DBG_ROUNDS = 10,   /* uint32 [1]    greedy rounds of the last condense */
-  LUFFY_DBG_GREEDY_TIMES = 11 /* uint32 [64] greedy control block: [3] = #stamps, [8+2i..9+2i] = %globaltimer ns at barrier i */
+  LUFFY_DBG_GREEDY_TIMES = 11, /* uint32 [64] greedy control block: [3] = #stamps, [8+2i..9+2i] = %globaltimer ns at barrier i */
+  LUFFY_DBG_HONE = 12,     /* uint32 [adjoff[E]] fast measurement: this block's finalized weight > S1 (adj layout) */
+  LUFFY_DBG_HZERO = 13,    /* uint32 [adjoff[E]] finalized weight < S2 */
+  LUFFY_DBG_DEC1 = 14,     /* uint32 [adjoff[E]] pairs decided by the previous block with weight 1 */
+  LUFFY_DBG_DEC0 = 15,     /* uint32 [adjoff[E]] pairs decided by the previous block with weight 0 */
+  LUFFY_DBG_TSKIP = 16     /* uint8 [tiles] skipped Gram tiles (pair tiles in upper-triangle order per group) */
 } luffy_debug_item;
 
 /* Synchronously copies an internal array of the layer's current forward to host memory `dst` (host).

@@ -139,6 +139,12 @@ Dims dims_of(const luffy_config* c) {
   return m;
 }
 
+// Upper bound of the 256x256 pair tiles over any split of the padded group rows into E groups.
+int64_t max_pair_tiles(const Dims& m) {
+  const int64_t nt = m.Cpad / 256 + m.E;
+  return nt * (nt + 1) / 2;
+}
+
 void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   const Dims m = dims_of(c);
   const size_t es = elem_size(c->dtype);
@@ -165,6 +171,13 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->win = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);
   o->stat64 = cv.take<uint64_t>(4);
+  if (c->fast_measure) {
+    o->hone = cv.take<uint32_t>(m.adjw);
+    o->hzero = cv.take<uint32_t>(m.adjw);
+    o->dec1 = cv.take<uint32_t>(m.adjw);
+    o->dec0 = cv.take<uint32_t>(m.adjw);
+    o->tskip = cv.take<uint8_t>(max_pair_tiles(m));
+  }
   o->nrep = cv.take<int32_t>(m.E);
   o->gnrep = cv.take<int32_t>(m.E);
   o->soff = cv.take<int32_t>(m.E + 1);
@@ -223,6 +236,9 @@ luffy_status validate(const luffy_config* c) {
   if (c->renormalize < -1 || c->renormalize > 1) return fail(LUFFY_E_INVALID, "renormalize must be -1, 0 or 1");
   if (c->max_tokens < 1) return fail(LUFFY_E_INVALID, "max_tokens must be >= 1");
   if (c->max_seqs < 0) return fail(LUFFY_E_INVALID, "max_seqs must be >= 0");
+  if (c->fast_measure != 0 && c->fast_measure != 1) return fail(LUFFY_E_INVALID, "fast_measure must be 0 or 1");
+  if (c->fast_measure && c->dtype != LUFFY_BF16)
+    return fail(LUFFY_E_UNSUPPORTED, "fast_measure (history shortcuts) needs the bf16 tcgen05 Gram");
   if (c->dtype == LUFFY_BF16 && (c->d_model % 256 || c->d_ffn % 256))
     return fail(LUFFY_E_UNSUPPORTED, "bf16 (tcgen05) path needs d_model and d_ffn multiples of 256");
   const Dims m = dims_of(c);
@@ -436,6 +452,9 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   L->recv_max = m.recv;
   L->adj_words_max = m.adjw;
   L->Smax = m.Smax;
+  L->fast_measure = ctx->cfg.fast_measure != 0;
+  L->hist_S1 = 0.8f;   // SPEC S:394 defaults (Fig. 7 probes 0.8 / 0.2); luffy_layer_set_history sets them
+  L->hist_S2 = 0.2f;
   if (L->P > 1) {
     // the peer-visible exchange region: allocated once here, mapped by the peers via CUDA IPC
     const XLayout xl = xlayout(L);
@@ -624,6 +643,12 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
                 "luffy_condense/near_tie");
   }
   LUFFY_CHECK(launch_group_build(L, x, stream), "luffy_condense/group_build");
+  if (L->hist_prev) {
+    const luffy_layer* P = L->hist_prev;
+    if (P->T != L->T || P->stage < 2)
+      return fail(LUFFY_E_STATE, "luffy_condense: the history layer must be condensed earlier in this step on the same T tokens");
+  }
+  L->hist_valid = false;
   if (h > 1.0f) {
     L->has_adj = false;
     LUFFY_CHECK(launch_identity_rep(L, stream), "luffy_condense/identity");
@@ -633,6 +658,7 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
     if (L->dtype == LUFFY_BF16) LUFFY_CHECK(launch_gram_tc(L, h, band, stream), "luffy_condense/gram");
     else LUFFY_CHECK(launch_gram_simt(L, h, band, stream), "luffy_condense/gram");
     LUFFY_CHECK(launch_greedy(L, stream), "luffy_condense/greedy");
+    L->hist_valid = L->fast_measure;
   }
   LUFFY_CHECK(launch_pack(L, x, nullptr, rep, stream), "luffy_condense/layout");
   L->stage = 2;
@@ -656,6 +682,8 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
     stats->rounds = (int32_t)rounds;
     stats->ambiguous_pairs = (int64_t)s64[0];
     stats->near_tie_tokens = (int64_t)s64[1];
+    stats->decided_pairs = (int64_t)s64[2];
+    stats->skipped_tiles = (int64_t)s64[3];
   }
   return LUFFY_OK;
 }
@@ -1032,6 +1060,19 @@ luffy_status luffy_migration_out_tokens(const luffy_layer* L, int32_t* home_rank
   return LUFFY_OK;
 }
 
+luffy_status luffy_layer_set_history(luffy_layer* L, const luffy_layer* prev, float S1, float S2) {
+  LUFFY_NEED(L);
+  if (!L->fast_measure) return fail(LUFFY_E_STATE, "luffy_layer_set_history: the layer was created without fast_measure");
+  if (!(S2 >= 0.f && S2 < S1 && S1 <= 1.f)) return fail(LUFFY_E_INVALID, "luffy_layer_set_history: need 0 <= S2 < S1 <= 1");
+  if (prev == L) return fail(LUFFY_E_INVALID, "luffy_layer_set_history: prev must be another layer");
+  if (prev && !prev->fast_measure) return fail(LUFFY_E_INVALID, "luffy_layer_set_history: prev was created without fast_measure");
+  if (prev && prev->ctx->device != L->ctx->device) return fail(LUFFY_E_INVALID, "luffy_layer_set_history: prev is on another device");
+  L->hist_prev = prev;
+  L->hist_S1 = S1;
+  L->hist_S2 = S2;
+  return LUFFY_OK;
+}
+
 luffy_status luffy_debug_gram_dump(luffy_layer* L, float* dst, size_t capacity_floats) {
   LUFFY_NEED(L);
   if (dst && reinterpret_cast<uintptr_t>(dst) % 16) return fail(LUFFY_E_INVALID, "luffy_debug_gram_dump: dst must be 16-byte aligned");
@@ -1083,6 +1124,22 @@ luffy_status luffy_debug_copy(luffy_layer* L, int32_t item, void* dst, size_t* b
     case LUFFY_DBG_NREP: src = L->nrep; n = sizeof(int32_t) * L->E; break;
     case LUFFY_DBG_ROUNDS: src = L->ctrl + 2; n = sizeof(uint32_t); break;
     case LUFFY_DBG_GREEDY_TIMES: src = L->ctrl; n = sizeof(uint32_t) * 64; break;
+    case LUFFY_DBG_HONE: src = L->hone; n = L->hist_valid ? sizeof(uint32_t) * adjE : 0; break;
+    case LUFFY_DBG_HZERO: src = L->hzero; n = L->hist_valid ? sizeof(uint32_t) * adjE : 0; break;
+    case LUFFY_DBG_DEC1: src = L->dec1; n = (L->hist_valid && L->hist_prev) ? sizeof(uint32_t) * adjE : 0; break;
+    case LUFFY_DBG_DEC0: src = L->dec0; n = (L->hist_valid && L->hist_prev) ? sizeof(uint32_t) * adjE : 0; break;
+    case LUFFY_DBG_TSKIP: {
+      int64_t nt = 0;
+      std::vector<int32_t> go(L->E + 1);
+      LUFFY_CHECK(cudaMemcpy(go.data(), L->goff, sizeof(int32_t) * (L->E + 1), cudaMemcpyDeviceToHost), "debug");
+      for (int e = 0; e < L->E; ++e) {
+        const int64_t pb = ((go[e + 1] - go[e]) / 128 + 1) / 2;
+        nt += pb * (pb + 1) / 2;
+      }
+      src = L->tskip;
+      n = (L->hist_valid && L->hist_prev) ? nt : 0;
+      break;
+    }
     default: return fail(LUFFY_E_INVALID, "luffy_debug_copy: unknown item");
   }
   if (dst == nullptr || *bytes < n) {

@@ -55,6 +55,16 @@ struct luffy_layer {
   uint32_t* alive;    // [Cpad_max/32]
   uint32_t* win;      // [Cpad_max/32]
   uint32_t* ctrl;     // [64 + kGreedyMaxRounds] grid barrier + per-round counters
+  // ---- fast similarity measurement (config fast_measure, readings R20/R21), adj layout
+  bool fast_measure;
+  uint32_t* hone;     // this block's finalized weight > S1 (history for the next block)
+  uint32_t* hzero;    // this block's finalized weight < S2
+  uint32_t* dec1;     // pairs decided by the previous block: weight 1
+  uint32_t* dec0;     //                                        weight 0
+  uint8_t* tskip;     // [tiles] Gram tiles whose pairs are all decided
+  const luffy_layer* hist_prev;  // previous block (luffy_layer_set_history), nullable
+  float hist_S1, hist_S2;
+  bool hist_valid;    // hone / hzero hold this step's classification
   // ---- pack / layout
   int32_t* nrep;      // [E] representatives per expert
   int32_t* gnrep;     // [E] representatives per group, published by representative selection

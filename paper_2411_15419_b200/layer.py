@@ -17,7 +17,7 @@ class CondensedMoELayer:
     def __init__(self, num_experts: int, top_k: int, d_model: int, d_ffn: int, max_tokens: int,
                  dtype: str = "bf16", act: str = "gelu", world: int = 1, rank: int = 0,
                  renormalize: int = -1, max_recv_rows: int = 0, device: torch.device | str = "cuda",
-                 group=None):
+                 group=None, fast_measure: bool = False, max_seqs: int = 0):
         self.device = torch.device(device)
         self.dt = L.BF16 if dtype == "bf16" else L.FP32
         self.tdt = _TORCH_DT[self.dt]
@@ -26,7 +26,7 @@ class CondensedMoELayer:
         self.world, self.rank = world, rank
         self.El = num_experts // world
         self.cfg = L.make_config(world, rank, num_experts, top_k, d_model, d_ffn, self.dt, self.act, renormalize,
-                                 max_tokens, max_recv_rows)
+                                 max_tokens, max_recv_rows, max_seqs, 1 if fast_measure else 0)
         self.ctx = L.luffy_create(self.cfg)
         nbytes = L.luffy_layer_workspace_bytes(self.cfg)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -69,6 +69,10 @@ class CondensedMoELayer:
         self.dwg = torch.empty(num_experts, d_model, dtype=torch.float32, device=dev)
         self.T = 0
         self.stats = None
+
+    def set_history(self, prev: "CondensedMoELayer | None", S1: float = 0.8, S2: float = 0.2):
+        """Fast similarity measurement with history shortcuts from the previous block."""
+        L.luffy_layer_set_history(self.layer, prev.layer if prev is not None else None, S1, S2)
 
     def close(self):
         if getattr(self, "layer", None):

@@ -27,7 +27,7 @@ EXPORTED = [
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan", "luffy_layer_set_exchange_timeout",
-    "luffy_debug_gram_dump", "luffy_debug_set_pdl",
+    "luffy_debug_gram_dump", "luffy_debug_set_pdl", "luffy_layer_set_history",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -42,12 +42,13 @@ class LuffyError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "world", "rank", "num_experts", "top_k", "d_model", "d_ffn", "dtype", "act", "renormalize",
-        "max_tokens", "max_recv_rows", "max_seqs")]
+        "max_tokens", "max_recv_rows", "max_seqs", "fast_measure")]
 
 
 class CondenseStats(ctypes.Structure):
     _fields_ = [("copies", ctypes.c_int64), ("reps", ctypes.c_int64), ("ambiguous_pairs", ctypes.c_int64),
-                ("near_tie_tokens", ctypes.c_int64), ("rounds", ctypes.c_int32),
+                ("near_tie_tokens", ctypes.c_int64), ("decided_pairs", ctypes.c_int64),
+                ("skipped_tiles", ctypes.c_int64), ("rounds", ctypes.c_int32),
                 ("reps_per_expert", ctypes.c_int32 * MAX_EXPERTS),
                 ("copies_per_expert", ctypes.c_int32 * MAX_EXPERTS)]
 
@@ -101,6 +102,7 @@ def _load():
         "luffy_layer_set_exchange_timeout": (I32, [P, I64]),
         "luffy_debug_gram_dump": (I32, [P, P, ctypes.c_size_t]),
         "luffy_debug_set_pdl": (None, [I32]),
+        "luffy_layer_set_history": (I32, [P, P, F32, F32]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -130,9 +132,9 @@ def _p(x):
 # ---------------------------------------------------------------- lifetime
 
 def make_config(world=1, rank=0, num_experts=8, top_k=2, d_model=1024, d_ffn=4096, dtype=BF16, act=GELU,
-                renormalize=-1, max_tokens=8192, max_recv_rows=0, max_seqs=0) -> Config:
+                renormalize=-1, max_tokens=8192, max_recv_rows=0, max_seqs=0, fast_measure=0) -> Config:
     return Config(world, rank, num_experts, top_k, d_model, d_ffn, dtype, act, renormalize, max_tokens,
-                  max_recv_rows, max_seqs)
+                  max_recv_rows, max_seqs, fast_measure)
 
 
 def luffy_create(cfg: Config) -> int:
@@ -277,7 +279,8 @@ def luffy_adaptive_threshold(l_ini: float, l_prev: float, scale2: bool = False) 
 
 DBG = dict(gcnt=(0, np.int32), goff=(1, np.int32), gtok=(2, np.int32), adjoff=(3, np.int64), adj=(4, np.uint32),
            rep_local=(5, np.int32), soff=(6, np.int32), perm=(7, np.int32), pos=(8, np.int32), nrep=(9, np.int32),
-           rounds=(10, np.uint32), greedy_times=(11, np.uint32))
+           rounds=(10, np.uint32), greedy_times=(11, np.uint32), hone=(12, np.uint32), hzero=(13, np.uint32),
+           dec1=(14, np.uint32), dec0=(15, np.uint32), tskip=(16, np.uint8))
 
 
 def luffy_debug_copy(layer, item: str, stream) -> np.ndarray:
@@ -314,6 +317,11 @@ def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
     n = int(ro[-1])
     return dict(send_off=so, recv_off=ro, dst_base=db, rank_of=rk[:n], slot_of=sl[:n], send_rows_to=st,
                 recv_rows_from=rf)
+
+
+def luffy_layer_set_history(layer, prev, S1: float = 0.8, S2: float = 0.2):
+    """Fast similarity measurement: take history shortcuts from `prev` (a luffy layer or None)."""
+    _check(LIB.luffy_layer_set_history(layer, prev, float(S1), float(S2)))
 
 
 def luffy_debug_set_pdl(on: bool):

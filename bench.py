@@ -366,6 +366,7 @@ def main():
         lens = [None] * world
         dist.all_gather_object(lens, seq_len)
         seq_len_all = np.array([v for ls in lens for v in ls], np.int32)
+        seq_counts = [len(v) for v in lens]
         y_out = torch.empty(world * T, cfg.d_model, dtype=tdt, device=dev)
         dy_out = torch.randn(world * T, cfg.d_model, device=dev).to(tdt)
         mig_stats = {"migrated_seqs": 0, "hosted_tokens": 0}
@@ -378,10 +379,10 @@ def main():
         L.luffy_route(lay.layer, x, wg, T, lay.idx, lay.w, s); m(1)
         L.luffy_condense(lay.layer, x, cfg.h, lay.rep, s)
         if mig:  # K9 -> Alg. 1 on every rank (host) -> destinations; the only host sync of the step
-            rows_at = L.luffy_sequence_rows(lay.layer, seq_len, world, s)
+            rows_at = L.luffy_sequence_rows(lay.layer, seq_len, world, s, counts=seq_counts)
             dest, _ = L.luffy_plan_migration(seq_len_all, rows_at, args.migrate, cfg.d_model * tdt.itemsize, cfg.d_model)
             n_out = L.luffy_set_migration(lay.layer, seq_len_all, dest, s)
-            mig_stats["migrated_seqs"] = int(np.sum(dest != np.repeat(np.arange(world), len(seq_len))))
+            mig_stats["migrated_seqs"] = int(np.sum(dest != np.repeat(np.arange(world), seq_counts)))
             mig_stats["hosted_tokens"] = int(n_out)
         m(2)
         L.luffy_dispatch(lay.layer, x, lay.recv, s); m(3)

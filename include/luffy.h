@@ -208,6 +208,15 @@ LUFFY_API luffy_status luffy_combine(luffy_layer* layer, const void* expert_out,
  * y[t] = sum_j topk_w[t, j] * gathered[slot of rep(t, j)], fp32 accumulation, y [T, d] (dtype). */
 LUFFY_API luffy_status luffy_uncondense(luffy_layer* layer, const void* gathered, void* y, void* stream);
 
+/* Residual block (a transformer block's MoE sub-layer, y = x + MoE(x)): luffy_uncondense with the residual
+ * branch added in the same pass, y[t] = x[t] + sum_j topk_w[t, j] * gathered[slot of rep(t, j)].  x is the
+ * layer input of luffy_route ([T, d], this rank's tokens).  With sequence migration the x rows of every
+ * token are pushed to the rank hosting its sequence (device-initiated, like the combine) and y holds the
+ * hosted tokens (luffy_migration_out_tokens order).  The backward counterpart is
+ * luffy_dispatch_bwd_residual. */
+LUFFY_API luffy_status luffy_uncondense_residual(luffy_layer* layer, const void* gathered, const void* x, void* y,
+                                                 void* stream);
+
 /* ---- backward: exact autograd of the forward with routing and rep as constants (R11) ------------- */
 
 /* d_gathered[slot] = sum over copies (t, j) represented by the slot (token order) of w[t,j] * dy[t];
@@ -229,6 +238,12 @@ LUFFY_API luffy_status luffy_expert_ffn_bwd(luffy_layer* layer, const void* d_ou
 /* Mirror of luffy_dispatch: d_send (send layout, internal for world > 1) <- d_recv (expert layout),
  * then dx[t] = sum over j with rep(t, j) == t of d_send[slot(t, j)] (dx overwritten, dtype). */
 LUFFY_API luffy_status luffy_dispatch_bwd(luffy_layer* layer, const void* d_recv, void* dx, void* stream);
+
+/* luffy_dispatch_bwd for a residual block: dx[t] = dy[t] + (expert-path gradient of x[t]).  dy: the dY
+ * given to luffy_uncondense_bwd (home order [T, d]); with sequence migration pass NULL (the dY rows the
+ * hosts returned to this rank are used).  Follow with luffy_route_bwd as usual (it accumulates). */
+LUFFY_API luffy_status luffy_dispatch_bwd_residual(luffy_layer* layer, const void* d_recv, const void* dy, void* dx,
+                                                   void* stream);
 
 /* Gate backward: renormalized: dl_j = w_j (dw_j - sum_i w_i dw_i) on the top-k; raw softmax:
  * dl = p * (g - <p, g>); dw_gate [E, d] fp32 = dl^T x (overwritten); dx += dl W_g (accumulated). */
@@ -302,14 +317,15 @@ LUFFY_API luffy_status luffy_debug_gemm(int32_t kind, int32_t dtype, int32_t epi
 /* ---- sequence migration in the layer (world > 1), P:264-299 -------------------------------------- */
 
 /* K9: after luffy_condense and before luffy_dispatch.  seq_len (host, [num_seqs], sums to T) splits this
- * rank's tokens into sequences; returns rows_at_all (host, [world * num_seqs][world], every rank's
- * sequences in rank order): the number of DISTINCT representative rows each sequence uses on each rank
- * (reading R16; Alg. 1 line 1 input).  Every rank gets the same table (device exchange).  [sync] */
+ * rank's tokens into sequences; num_seqs_all (host, [world], nullable = every rank has num_seqs) gives every
+ * rank's sequence count.  Returns rows_at_all (host, [sum of num_seqs_all][world], every rank's sequences in
+ * rank order): the number of DISTINCT representative rows each sequence uses on each rank (reading R16;
+ * Alg. 1 line 1 input).  Every rank gets the same table (device exchange).  [sync] */
 LUFFY_API luffy_status luffy_sequence_rows(luffy_layer* layer, const int32_t* seq_len, int32_t num_seqs,
-                                           int64_t* rows_at_all, void* stream);
+                                           const int32_t* num_seqs_all, int64_t* rows_at_all, void* stream);
 
 /* Registers the placement of this step (e.g. from luffy_plan_migration, run identically on every rank):
- * seq_len_all / seq_dest (host, [world * num_seqs]).  The combine then delivers each expert-output row to
+ * seq_len_all / seq_dest (host, [sum of num_seqs_all], rank order as in luffy_sequence_rows).  The combine then delivers each expert-output row to
  * every rank hosting a sequence that uses it (GEMM2 epilogue over NVLink); luffy_uncondense writes the
  * tokens this rank hosts (*out_rows of them, host) in (home rank, sequence, token) order -- see
  * luffy_migration_out_tokens; luffy_uncondense_bwd takes dY in that order and returns dY / d(gate weight)

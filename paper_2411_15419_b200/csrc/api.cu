@@ -57,11 +57,13 @@ int device_sms() {
   dev_cache_put(&tag, 0, n);
   return n;
 }
+// The attribute is an upper bound, so it only ever grows: the largest size set so far on this device is
+// cached (key extra = -2) and smaller requests are no-ops.
 int smem_optin(const void* kernel, int bytes) {
   int v = 0;
-  if (dev_cache_get(kernel, bytes, &v)) return 0;
+  if (dev_cache_get(kernel, -2, &v) && v >= bytes) return 0;
   const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) dev_cache_put(kernel, bytes, 1);
+  if (e == cudaSuccess) dev_cache_put(kernel, -2, bytes);
   return (int)e;
 }
 // Programmatic dependent launch on/off: LUFFY_PDL=0 in the environment, or luffy_debug_set_pdl at run time
@@ -218,6 +220,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
     o->x_peer_meta_w = cv.take<float*>(m.P);
     o->x_peer_dy_in = cv.take<void*>(m.P);
     o->x_peer_dw_in = cv.take<float*>(m.P);
+    o->x_peer_res = cv.take<void*>(m.P);
   }
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
   o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 31) / 32) * m.E * m.d);
@@ -287,7 +290,7 @@ int64_t expert_rows_bound(const luffy_layer* L) { return L->P == 1 ? L->Rpad_max
 
 // Exchange region layout (identical offsets on every rank).
 struct XLayout {
-  size_t recv[2], gathered, dexp, dsend, cnt, flags, counters, rowmask, mig, meta, meta_w, dy_in, dw_in, total;
+  size_t recv[2], gathered, dexp, dsend, cnt, flags, counters, rowmask, mig, meta, meta_w, dy_in, dw_in, res, total;
 };
 XLayout xlayout(const luffy_layer* L) {
   const size_t rb = (size_t)L->d * elem_size(L->dtype);
@@ -308,6 +311,7 @@ XLayout xlayout(const luffy_layer* L) {
   x.meta_w = take(sizeof(float) * (size_t)L->P * L->Tmax * L->k);
   x.dy_in = take((size_t)L->Tmax * rb);
   x.dw_in = take(sizeof(float) * (size_t)L->Tmax * L->k);
+  x.res = take((size_t)L->P * L->Tmax * rb);
   x.total = (o + 4095) / 4096 * 4096;
   return x;
 }
@@ -495,6 +499,7 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
     L->x_meta_w = reinterpret_cast<float*>(L->x_region + xl.meta_w);
     L->x_dy_in = L->x_region + xl.dy_in;
     L->x_dw_in = reinterpret_cast<float*>(L->x_region + xl.dw_in);
+    L->x_res = L->x_region + xl.res;
   }
   *out = L;
   return LUFFY_OK;
@@ -555,7 +560,7 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
   std::vector<uint32_t*> flag((size_t)XP_NUM * P);
   std::vector<unsigned long long*> rowmask(P);
   std::vector<float*> meta_w(P), dw_in(P);
-  std::vector<void*> dy_in(P);
+  std::vector<void*> dy_in(P), res(P);
   for (int p = 0; p < P; ++p) {
     char* b = static_cast<char*>(L->x_peer_base_h[p]);
     recv[p] = b + xl.recv[0];
@@ -570,6 +575,7 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
     rowmask[p] = reinterpret_cast<unsigned long long*>(b + xl.rowmask);
     dy_in[p] = b + xl.dy_in;
     dw_in[p] = reinterpret_cast<float*>(b + xl.dw_in);
+    res[p] = b + xl.res;
     for (int ph = 0; ph < XP_NUM; ++ph)
       flag[(size_t)ph * P + p] = reinterpret_cast<uint32_t*>(b + xl.flags) + ph * P + L->rank;
   }
@@ -585,6 +591,7 @@ luffy_status luffy_layer_ipc_open(luffy_layer* L, const uint8_t* all_handles) {
   LUFFY_CHECK(cudaMemcpy(L->x_peer_meta_w, meta_w.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
   LUFFY_CHECK(cudaMemcpy(L->x_peer_dy_in, dy_in.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
   LUFFY_CHECK(cudaMemcpy(L->x_peer_dw_in, dw_in.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
+  LUFFY_CHECK(cudaMemcpy(L->x_peer_res, res.data(), sizeof(void*) * P, cudaMemcpyHostToDevice), "ipc tables");
   L->x_open = true;
   return LUFFY_OK;
 }
@@ -820,26 +827,37 @@ luffy_status luffy_combine(luffy_layer* L, const void* expert_out, void* gathere
   return LUFFY_OK;
 }
 
-luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, void* stream) {
+static luffy_status uncondense_impl(luffy_layer* L, const void* gathered, const void* res, void* y, void* stream,
+                                    const char* name) {
   LUFFY_NEED(L);
-  LUFFY_HEALTHY(L, "luffy_uncondense");
+  LUFFY_HEALTHY(L, name);
   LUFFY_NEED(y);
   LUFFY_ALIGNED(y);
-  LUFFY_STAGE(L, 5, "luffy_uncondense");
+  LUFFY_STAGE(L, 5, name);
+  if (res) LUFFY_ALIGNED(res);
   if (L->P == 1) {
     LUFFY_NEED(gathered);
   } else {
-    LUFFY_OWN(gathered, home_gathered(L), "luffy_uncondense gathered");
+    LUFFY_OWN(gathered, home_gathered(L), name);
     gathered = home_gathered(L);
     if (L->mig) {  // y holds the tokens of the sequences this rank hosts (luffy_migration_out_tokens)
-      LUFFY_CHECK(launch_uncondense_mig(L, y, stream), "luffy_uncondense/migration");
+      LUFFY_CHECK(launch_uncondense_mig(L, res, y, stream), name);
       L->stage = 6;
       return LUFFY_OK;
     }
   }
-  LUFFY_CHECK(launch_uncondense(L, gathered, y, stream), "luffy_uncondense");
+  LUFFY_CHECK(launch_uncondense(L, gathered, res, y, stream), name);
   L->stage = 6;
   return LUFFY_OK;
+}
+
+luffy_status luffy_uncondense(luffy_layer* L, const void* gathered, void* y, void* stream) {
+  return uncondense_impl(L, gathered, nullptr, y, stream, "luffy_uncondense");
+}
+
+luffy_status luffy_uncondense_residual(luffy_layer* L, const void* gathered, const void* x, void* y, void* stream) {
+  LUFFY_NEED(x);
+  return uncondense_impl(L, gathered, x, y, stream, "luffy_uncondense_residual");
 }
 
 // ------------------------------------------------------------------------------------------ backward
@@ -944,22 +962,40 @@ luffy_status luffy_expert_ffn_bwd(luffy_layer* L, const void* d_out, const void*
   return LUFFY_OK;
 }
 
-luffy_status luffy_dispatch_bwd(luffy_layer* L, const void* d_recv, void* dx, void* stream) {
+static luffy_status dispatch_bwd_impl(luffy_layer* L, const void* d_recv, const void* dy_res, bool residual, void* dx,
+                                      void* stream, const char* name) {
   LUFFY_NEED(L);
-  LUFFY_HEALTHY(L, "luffy_dispatch_bwd");
+  LUFFY_HEALTHY(L, name);
   LUFFY_NEED(dx);
   LUFFY_ALIGNED(dx);
-  LUFFY_STAGE(L, 6, "luffy_dispatch_bwd");
+  LUFFY_STAGE(L, 6, name);
   const void* dsend = d_recv;
   if (L->P == 1) {
     LUFFY_NEED(d_recv);
   } else {
-    if (d_recv) return fail(LUFFY_E_INVALID, "luffy_dispatch_bwd: with world > 1 pass d_recv = NULL");
-    LUFFY_CHECK(launch_xwait(L, XP_DBWD, stream), "luffy_dispatch_bwd/wait");
+    if (d_recv) return fail(LUFFY_E_INVALID, std::string(name) + ": with world > 1 pass d_recv = NULL");
+    LUFFY_CHECK(launch_xwait(L, XP_DBWD, stream), name);
     dsend = L->x_dsend;
   }
-  LUFFY_CHECK(launch_unpack_bwd(L, dsend, dx, stream), "luffy_dispatch_bwd");
+  if (residual) {
+    if (L->P > 1 && L->mig) {  // the hosts returned every token's dY to its home (luffy_uncondense_bwd)
+      if (dy_res) return fail(LUFFY_E_INVALID, std::string(name) + ": with sequence migration pass dy = NULL");
+      dy_res = L->x_dy_in;
+    } else {
+      LUFFY_NEED(dy_res);
+      LUFFY_ALIGNED(dy_res);
+    }
+  }
+  LUFFY_CHECK(launch_unpack_bwd(L, dsend, residual ? dy_res : nullptr, dx, stream), name);
   return LUFFY_OK;
+}
+
+luffy_status luffy_dispatch_bwd(luffy_layer* L, const void* d_recv, void* dx, void* stream) {
+  return dispatch_bwd_impl(L, d_recv, nullptr, false, dx, stream, "luffy_dispatch_bwd");
+}
+
+luffy_status luffy_dispatch_bwd_residual(luffy_layer* L, const void* d_recv, const void* dy, void* dx, void* stream) {
+  return dispatch_bwd_impl(L, d_recv, dy, true, dx, stream, "luffy_dispatch_bwd_residual");
 }
 
 luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate, const float* d_topk_w, void* dx,
@@ -978,8 +1014,8 @@ luffy_status luffy_route_bwd(luffy_layer* L, const void* x, const float* w_gate,
 
 // ------------------------------------------------------------------------------- sequence migration
 
-luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t num_seqs, int64_t* rows_at_all,
-                                 void* stream) {
+luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t num_seqs,
+                                 const int32_t* num_seqs_all, int64_t* rows_at_all, void* stream) {
   LUFFY_NEED(L);
   LUFFY_HEALTHY(L, "luffy_sequence_rows");
   LUFFY_NEED(seq_len);
@@ -995,6 +1031,12 @@ luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t
     start[s + 1] = start[s] + seq_len[s];
   }
   if (start[num_seqs] != L->T) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: lengths must sum to T");
+  for (int q = 0; q < L->P; ++q) {
+    const int32_t c = num_seqs_all ? num_seqs_all[q] : num_seqs;
+    if (c < 1 || c > L->Smax) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: 1 <= num_seqs_all[q] <= max_seqs");
+    L->Sq[q] = c;
+  }
+  if (L->Sq[L->rank] != num_seqs) return fail(LUFFY_E_INVALID, "luffy_sequence_rows: num_seqs_all[rank] != num_seqs");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   LUFFY_CHECK(cudaMemcpyAsync(L->seq_start, start.data(), sizeof(int32_t) * (num_seqs + 1), cudaMemcpyHostToDevice, st),
               "seq_start");
@@ -1004,10 +1046,10 @@ luffy_status luffy_sequence_rows(luffy_layer* L, const int32_t* seq_len, int32_t
   LUFFY_CHECK(cudaMemcpyAsync(all.data(), L->x_mig_inbox, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost, st),
               "rows_at D2H");
   LUFFY_CHECK(cudaStreamSynchronize(st), "rows_at sync");
+  size_t row = 0;
   for (int q = 0; q < L->P; ++q)
-    for (int s = 0; s < num_seqs; ++s)
-      for (int j = 0; j < L->P; ++j)
-        rows_at_all[((size_t)q * num_seqs + s) * L->P + j] = all[((size_t)q * L->Smax + s) * L->P + j];
+    for (int s = 0; s < L->Sq[q]; ++s, ++row)
+      for (int j = 0; j < L->P; ++j) rows_at_all[row * L->P + j] = all[((size_t)q * L->Smax + s) * L->P + j];
   return LUFFY_OK;
 }
 
@@ -1020,19 +1062,22 @@ luffy_status luffy_set_migration(luffy_layer* L, const int32_t* seq_len_all, con
   if (L->S < 1) return fail(LUFFY_E_STATE, "luffy_set_migration: call luffy_sequence_rows first (this step)");
   if (L->stage >= 3) return fail(LUFFY_E_STATE, "luffy_set_migration: must precede luffy_dispatch");
   const int P = L->P, S = L->S;
-  for (int i = 0; i < P * S; ++i)
+  int total = 0;
+  for (int q = 0; q < P; ++q) total += L->Sq[q];
+  for (int i = 0; i < total; ++i)
     if (seq_dest[i] < 0 || seq_dest[i] >= P) return fail(LUFFY_E_INVALID, "luffy_set_migration: seq_dest out of range");
   // output rows of each destination: sequences in (home rank, sequence) order
   std::vector<int64_t> fill(P, 0);
   std::vector<int32_t> out_start(S), dest(S);
+  int i = 0;
   for (int q = 0; q < P; ++q)
-    for (int s = 0; s < S; ++s) {
-      const int g = seq_dest[q * S + s];
+    for (int s = 0; s < L->Sq[q]; ++s, ++i) {
+      const int g = seq_dest[i];
       if (q == L->rank) {
         out_start[s] = (int32_t)fill[g];
         dest[s] = g;
       }
-      fill[g] += seq_len_all[q * S + s];
+      fill[g] += seq_len_all[i];
     }
   if (fill[L->rank] > (int64_t)P * L->Tmax) return fail(LUFFY_E_CAPACITY, "luffy_set_migration: output capacity");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -22,7 +22,7 @@
 namespace luffy {
 
 enum XPhase { XP_CNT = 0, XP_DISP = 1, XP_COMB = 2, XP_CBWD = 3, XP_DBWD = 4, XP_MIG = 5, XP_META = 6, XP_MIGB = 7,
-              XP_NUM = 8 };
+              XP_RES = 8, XP_NUM = 9 };
 constexpr int kMaxWorld = 64;
 
 // Completion signal of one producing kernel.

@@ -303,7 +303,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   } else {
     auto coresident = [&](auto kern, int size) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_optin((const void*)kern, (int)smem);
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(size);
       cfg.blockDim = dim3(GC_THREADS);

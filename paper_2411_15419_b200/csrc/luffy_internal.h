@@ -130,6 +130,7 @@ struct luffy_layer {
   // ---- sequence migration (world > 1), Alg. 1 decides seq_dest; migration.cu
   int Smax;                // sequence capacity per rank
   int S;                   // sequences of the current step (0 = not registered)
+  int32_t Sq[64];          // sequences of every rank this step (luffy_sequence_rows)
   bool mig;                // seq_dest set for the current step
   int64_t n_out;           // output rows of this rank (tokens of the sequences it hosts)
   int32_t* seq_start;      // [Smax+1] token range of each of my sequences
@@ -143,6 +144,8 @@ struct luffy_layer {
   int32_t* x_meta;         // region [P*Tmax][2 + k] (home rank, home token, pos[k]) of my output rows
   float* x_meta_w;         // region [P*Tmax][k]
   void* x_dy_in;           // region [Tmax][d] dY of my tokens returned by their destinations
+  void* x_res;             // region [P*Tmax][d] residual rows x of the tokens this rank hosts
+  void** x_peer_res;       // [P]
   float* x_dw_in;          // region [Tmax][k]
   unsigned long long** x_peer_rowmask;  // [P]
   int32_t** x_peer_mig;    // [P]
@@ -163,16 +166,16 @@ int launch_gram_tc(luffy_layer* L, float h, unsigned long long* band, void* s);
 int launch_near_tie(const luffy_layer* L, const void* x, const float* wg, unsigned long long* out, void* s);
 int launch_greedy(luffy_layer* L, void* s);
 int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out, void* s);
-int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void* s);
+int launch_uncondense(const luffy_layer* L, const void* gathered, const void* res, void* y, void* s);
 int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gathered, void* dg, float* dw, void* s);
-int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s);
+int launch_unpack_bwd(const luffy_layer* L, const void* dsend, const void* res, void* dx, void* s);
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s);
 int launch_xdispatch(luffy_layer* L, const void* x, void* s);
 int launch_xwait(const luffy_layer* L, int phase, void* s);
 int launch_seq_rows(luffy_layer* L, void* s);
 int launch_set_migration(luffy_layer* L, void* s);
 int launch_mig_meta_push(luffy_layer* L, void* s);
-int launch_uncondense_mig(const luffy_layer* L, void* y, void* s);
+int launch_uncondense_mig(const luffy_layer* L, const void* x_res, void* y, void* s);
 int launch_mig_bwd_push(const luffy_layer* L, const void* dy, void* s);
 
 // Grouped GEMM epilogues (gemm_simt.cu / gemm_tc.cu).  EPI_GELU stores GeLU(acc) and aux = GeLU'(acc);

@@ -102,7 +102,7 @@ __global__ void mig_meta_push_kernel(const int32_t* __restrict__ pos, const floa
 template <typename T>
 __global__ void __launch_bounds__(256) uncondense_mig_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ meta,
                                                              const float* __restrict__ meta_w, int64_t n_out, int k, int d,
-                                                             int64_t Rpad, T* __restrict__ y) {
+                                                             int64_t Rpad, const T* __restrict__ res, T* __restrict__ y) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(256) uncondense_mig_kernel(const T* __restrict
     const int64_t h = m[0];
     for (int c = lane * 8; c < d; c += 256) {
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (res != nullptr) load8(res + i * d + c, acc);  // residual row pushed from the home rank
       for (int j = 0; j < k; ++j) {
         const float wj = meta_w[i * k + j];
         float v[8];
@@ -121,6 +122,31 @@ __global__ void __launch_bounds__(256) uncondense_mig_kernel(const T* __restrict
       store8(y + i * d + c, acc);
     }
   }
+}
+
+// Residual rows of a block y = x + MoE(x): x of every token to the rank hosting its sequence (row order of
+// the hosted tokens: home rank, sequence, token).
+template <typename T>
+__global__ void __launch_bounds__(256) res_push_kernel(const T* __restrict__ x, const int32_t* __restrict__ seq_start,
+                                                       const int32_t* __restrict__ seq_dest,
+                                                       const int32_t* __restrict__ out_start, int S, int T_, int d,
+                                                       void* const* peer_res, XSignal sig) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += (gridDim.x * blockDim.x) >> 5) {
+    const int s = seq_of(seq_start, S, t);
+    const int64_t i = out_start[s] + (t - seq_start[s]);
+    T* dst = static_cast<T*>(peer_res[seq_dest[s]]) + i * d;
+    for (int c = lane * 8; c < d; c += 256) {
+      if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(x + (int64_t)t * d + c);
+      } else {
+        *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(x + (int64_t)t * d + c);
+        *reinterpret_cast<float4*>(dst + c + 4) = *reinterpret_cast<const float4*>(x + (int64_t)t * d + c + 4);
+      }
+    }
+  }
+  xsignal_done(sig);
 }
 
 // Backward at the destination: d(gate weight) and dY of every hosted token back to its home rank.
@@ -200,15 +226,30 @@ int launch_mig_meta_push(luffy_layer* L, void* s) {
   return 0;
 }
 
-int launch_uncondense_mig(const luffy_layer* L, void* y, void* s) {
+int launch_uncondense_mig(const luffy_layer* L, const void* x_res, void* y, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
+  const void* res = nullptr;
+  if (x_res) {  // residual block: push this rank's x rows to the hosts of their sequences, then wait
+    const int bp = blocks_for(L->T, 8);
+    if (L->dtype == LUFFY_BF16)
+      launch_pdl(res_push_kernel<bf16>, bp, 256, 0, st, static_cast<const bf16*>(x_res), L->seq_start, L->seq_dest_l,
+                 L->out_start, L->S, L->T, L->d, L->x_peer_res, make_signal(L, XP_RES));
+    else
+      launch_pdl(res_push_kernel<float>, bp, 256, 0, st, static_cast<const float*>(x_res), L->seq_start, L->seq_dest_l,
+                 L->out_start, L->S, L->T, L->d, L->x_peer_res, make_signal(L, XP_RES));
+    LUFFY_LAUNCHED();
+    LUFFY_CUDA_TRY(launch_xwait(L, XP_RES, s));
+    res = L->x_res;
+  }
   const int b = blocks_for(L->n_out, 8);
   if (L->dtype == LUFFY_BF16)
     launch_pdl(uncondense_mig_kernel<bf16>, b, 256, 0, st, static_cast<const bf16*>(L->x_gathered), L->x_meta, L->x_meta_w,
-                                                   L->n_out, L->k, L->d, L->Rpad_max, static_cast<bf16*>(y));
+                                                   L->n_out, L->k, L->d, L->Rpad_max, static_cast<const bf16*>(res),
+                                                   static_cast<bf16*>(y));
   else
     launch_pdl(uncondense_mig_kernel<float>, b, 256, 0, st, static_cast<const float*>(L->x_gathered), L->x_meta, L->x_meta_w,
-                                                    L->n_out, L->k, L->d, L->Rpad_max, static_cast<float*>(y));
+                                                    L->n_out, L->k, L->d, L->Rpad_max, static_cast<const float*>(res),
+                                                    static_cast<float*>(y));
   LUFFY_LAUNCHED();
   return 0;
 }

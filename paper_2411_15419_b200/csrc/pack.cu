@@ -335,11 +335,11 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ x,
 template <typename T, int KM>
 __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ pos,
                                                          const float* __restrict__ w, int T_, int k, int d,
-                                                         T* __restrict__ y);
+                                                         const T* __restrict__ res, T* __restrict__ y);
 template <typename T, int KM>
 __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ dsend, const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ rep, int T_, int k, int d,
-                                                         T* __restrict__ dx);
+                                                         const T* __restrict__ res, T* __restrict__ dx);
 
 // d_gathered[slot] = sum_{members m of the slot, token order} gw[m] * dy[gtok[m]]; padding -> 0.
 //
@@ -560,11 +560,12 @@ __global__ void __launch_bounds__(256) uncondense_bwd_window_kernel(
   }
 }
 
-// dx[t] = sum_{j : rep(t, j) == t} d_send[pos_tj]   (condensed copies get no expert-path gradient, R11)
+// dx[t] = [res[t] +] sum_{j : rep(t, j) == t} d_send[pos_tj]   (condensed copies get no expert-path
+// gradient, R11; res: the residual branch's gradient dY of a block y = x + MoE(x))
 template <typename T, int KM>
 __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ dsend, const int32_t* __restrict__ pos,
                                                          const int32_t* __restrict__ rep, int T_, int k, int d,
-                                                         T* __restrict__ dx) {
+                                                         const T* __restrict__ res, T* __restrict__ dx) {
   pdl_enter();
   using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
   constexpr int HC = KM <= 2 ? 2 : 1;  // 256-column chunks per load batch
@@ -590,6 +591,7 @@ __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ d
         const int c = c0 + h * 256 + lane * 8;
         if (c >= d) break;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (res != nullptr) load8(res + (size_t)t * d + c, acc);
 #pragma unroll
         for (int j = 0; j < KM; ++j) {
           if (j < k && row[j] >= 0) {
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(256) unpack_bwd_kernel(const T* __restrict__ d
 template <typename T, int KM>
 __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ gathered, const int32_t* __restrict__ pos,
                                                          const float* __restrict__ w, int T_, int k, int d,
-                                                         T* __restrict__ y) {
+                                                         const T* __restrict__ res, T* __restrict__ y) {
   pdl_enter();
   using R = decltype(ldraw8(static_cast<const T*>(nullptr)));
   constexpr int HC = KM <= 2 ? 2 : 1;
@@ -642,6 +644,7 @@ __global__ void __launch_bounds__(256) uncondense_kernel(const T* __restrict__ g
         const int c = c0 + h * 256 + lane * 8;
         if (c >= d) break;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (res != nullptr) load8(res + (size_t)t * d + c, acc);  // residual block: y = x + sum_j w o
 #pragma unroll
         for (int j = 0; j < KM; ++j) {
           if (j < k) {
@@ -705,15 +708,15 @@ int launch_pack_rows(luffy_layer* L, const void* x, void* dst_rows, void* s) {
   return 0;
 }
 
-int launch_uncondense(const luffy_layer* L, const void* gathered, void* y, void* s) {
+int launch_uncondense(const luffy_layer* L, const void* gathered, const void* res, void* y, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
     launch_pdl(L->k <= 2 ? uncondense_kernel<bf16, 2> : uncondense_kernel<bf16, 8>, blocks, 256, 0, st, static_cast<const bf16*>(gathered), L->pos, L->w, L->T, L->k, L->d,
-                                                    static_cast<bf16*>(y));
+                                                    static_cast<const bf16*>(res), static_cast<bf16*>(y));
   else
     launch_pdl(L->k <= 2 ? uncondense_kernel<float, 2> : uncondense_kernel<float, 8>, blocks, 256, 0, st, static_cast<const float*>(gathered), L->pos, L->w, L->T, L->k, L->d,
-                                                     static_cast<float*>(y));
+                                                     static_cast<const float*>(res), static_cast<float*>(y));
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -745,15 +748,15 @@ int launch_uncondense_bwd(const luffy_layer* L, const void* dy, const void* gath
   return 0;
 }
 
-int launch_unpack_bwd(const luffy_layer* L, const void* dsend, void* dx, void* s) {
+int launch_unpack_bwd(const luffy_layer* L, const void* dsend, const void* res, void* dx, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int blocks = grid_for_warps(L->T);
   if (L->dtype == LUFFY_BF16)
     launch_pdl(L->k <= 2 ? unpack_bwd_kernel<bf16, 2> : unpack_bwd_kernel<bf16, 8>, blocks, 256, 0, st, static_cast<const bf16*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
-                                                    static_cast<bf16*>(dx));
+                                                    static_cast<const bf16*>(res), static_cast<bf16*>(dx));
   else
     launch_pdl(L->k <= 2 ? unpack_bwd_kernel<float, 2> : unpack_bwd_kernel<float, 8>, blocks, 256, 0, st, static_cast<const float*>(dsend), L->pos, L->rep, L->T, L->k, L->d,
-                                                     static_cast<float*>(dx));
+                                                     static_cast<const float*>(res), static_cast<float*>(dx));
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -93,21 +93,28 @@ class CondensedMoELayer:
         return torch.cuda.current_stream().cuda_stream
 
     def forward(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
-                stats: bool = False, want_rows: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+                stats: bool = False, want_rows: bool = False, out: torch.Tensor | None = None,
+                residual: bool = False) -> torch.Tensor:
+        """y = MoE(x), or x + MoE(x) with residual=True (luffy_uncondense_residual)."""
         T = x.shape[0]
         s = self._stream()
         self.T = T
+        self.mig = False
         y = self.y if out is None else out
         L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
         self.stats = L.luffy_condense(self.layer, x, h, self.rep, s, stats=stats)
         self.rows = L.luffy_dispatch(self.layer, x, self.recv, s, want_rows=want_rows)
         L.luffy_expert_ffn(self.layer, self.recv, w1, w2, w3, self.out, self.pre, self.act_buf, s)
         L.luffy_combine(self.layer, self.out, self.gathered, s)
-        L.luffy_uncondense(self.layer, self.gathered, y, s)
+        if residual:
+            L.luffy_uncondense_residual(self.layer, self.gathered, x, y, s)
+        else:
+            L.luffy_uncondense(self.layer, self.gathered, y, s)
         return y[:T]
 
     def forward_migrated(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
-                         seq_len=None, q: int = 1, seq_dest=None, capacity: int = 0, objective: int = 0, group=None):
+                         seq_len=None, q: int = 1, seq_dest=None, capacity: int = 0, objective: int = 0, group=None,
+                         residual: bool = False, stats: bool = False):
         """Forward with sequence migration (world > 1): K9 rows -> Alg. 1 on every rank (the
         C-ABI planner, or a given `seq_dest`) -> the combine delivers each sequence's expert outputs to
         the rank hosting it.  Returns (y [n_out, d] for the hosted tokens, home_rank, home_token,
@@ -119,11 +126,12 @@ class CondensedMoELayer:
         s = self._stream()
         self.T = T
         L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
-        self.stats = L.luffy_condense(self.layer, x, h, self.rep, s)
-        rows_at = L.luffy_sequence_rows(self.layer, seq_len, self.world, s)
+        self.stats = L.luffy_condense(self.layer, x, h, self.rep, s, stats=stats)
+        self.mig = True
         lens = [None] * self.world
         dist.all_gather_object(lens, [int(v) for v in seq_len], group=group)
         seq_len_all = np.array([v for ls in lens for v in ls], np.int32)
+        rows_at = L.luffy_sequence_rows(self.layer, seq_len, self.world, s, counts=[len(v) for v in lens])
         if seq_dest is None:
             esize = 2 if self.dt == L.BF16 else 4
             seq_dest, _ = L.luffy_plan_migration(seq_len_all, rows_at, q, self.d * esize, self.d,
@@ -133,18 +141,26 @@ class CondensedMoELayer:
         L.luffy_expert_ffn(self.layer, None, w1, w2, w3, None, self.pre, self.act_buf, s)
         L.luffy_combine(self.layer, None, None, s)
         self.y_out = torch.empty(max(n_out, 1), self.d, dtype=self.tdt, device=self.device)
-        L.luffy_uncondense(self.layer, None, self.y_out, s)
+        if residual:
+            L.luffy_uncondense_residual(self.layer, None, x, self.y_out, s)
+        else:
+            L.luffy_uncondense(self.layer, None, self.y_out, s)
         torch.cuda.current_stream().synchronize()
         home_rank, home_tok = L.luffy_migration_out_tokens(self.layer, n_out)
         return self.y_out[:n_out], home_rank, home_tok, np.asarray(seq_dest), rows_at
 
-    def backward(self, dy: torch.Tensor, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None):
+    def backward(self, dy: torch.Tensor, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None,
+                 residual: bool = False):
+        """Backward of forward / forward_migrated; residual=True adds the residual branch's dY to dx."""
         s = self._stream()
         L.luffy_uncondense_bwd(self.layer, dy, self.gathered, self.d_gathered, self.dw, s)
         L.luffy_combine_bwd(self.layer, self.d_gathered, self.d_out, s)
         L.luffy_expert_ffn_bwd(self.layer, self.d_out, self.recv, w1, w2, w3, self.pre, self.act_buf, self.dpre,
                                self.d_recv, self.dw1, self.dw2, self.dw3, s)
-        L.luffy_dispatch_bwd(self.layer, self.d_recv, self.dx, s)
+        if residual:
+            L.luffy_dispatch_bwd_residual(self.layer, self.d_recv, None if getattr(self, "mig", False) else dy, self.dx, s)
+        else:
+            L.luffy_dispatch_bwd(self.layer, self.d_recv, self.dx, s)
         L.luffy_route_bwd(self.layer, x, w_gate, self.dw, self.dx, self.dwg, s)
         T = self.T
         return dict(dx=self.dx[:T], dwg=self.dwg, dw1=self.dw1, dw2=self.dw2, dw3=self.dw3, dw=self.dw[:T])

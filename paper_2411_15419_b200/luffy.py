@@ -27,7 +27,8 @@ EXPORTED = [
     "luffy_combine", "luffy_uncondense", "luffy_uncondense_bwd", "luffy_combine_bwd",
     "luffy_expert_ffn_bwd", "luffy_dispatch_bwd", "luffy_route_bwd", "luffy_plan_migration",
     "luffy_attention_cost", "luffy_adaptive_threshold", "luffy_debug_copy", "luffy_debug_gemm", "luffy_exchange_plan", "luffy_layer_set_exchange_timeout",
-    "luffy_debug_gram_dump", "luffy_debug_set_pdl", "luffy_layer_set_history",
+    "luffy_debug_gram_dump", "luffy_debug_set_pdl", "luffy_layer_set_history", "luffy_uncondense_residual",
+    "luffy_dispatch_bwd_residual",
     "luffy_ipc_handle_bytes", "luffy_layer_ipc_handle", "luffy_layer_ipc_open", "luffy_layer_exchange_buffers",
     "luffy_sequence_rows", "luffy_set_migration", "luffy_migration_out_tokens",
 ]
@@ -71,7 +72,7 @@ def _load():
         "luffy_ipc_handle_bytes": (SZ, []),
         "luffy_layer_ipc_handle": (I32, [P, P]),
         "luffy_layer_ipc_open": (I32, [P, P]),
-        "luffy_sequence_rows": (I32, [P, P, I32, P, P]),
+        "luffy_sequence_rows": (I32, [P, P, I32, P, P, P]),
         "luffy_set_migration": (I32, [P, P, P, ctypes.POINTER(I64), P]),
         "luffy_migration_out_tokens": (I32, [P, P, P]),
         "luffy_layer_exchange_buffers": (I32, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
@@ -103,6 +104,8 @@ def _load():
         "luffy_debug_gram_dump": (I32, [P, P, ctypes.c_size_t]),
         "luffy_debug_set_pdl": (None, [I32]),
         "luffy_layer_set_history": (I32, [P, P, F32, F32]),
+        "luffy_uncondense_residual": (I32, [P, P, P, P, P]),
+        "luffy_dispatch_bwd_residual": (I32, [P, P, P, P, P]),
         "luffy_debug_gemm": (I32, [I32, I32, I32, P, P, P, P, P, P, I32, P, I32, I64, I32, I32, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
@@ -319,6 +322,14 @@ def luffy_exchange_plan(world: int, rank: int, num_experts: int, counts_all):
                 recv_rows_from=rf)
 
 
+def luffy_uncondense_residual(layer, gathered, x, y, stream):
+    _check(LIB.luffy_uncondense_residual(layer, _p(gathered), _p(x), _p(y), stream))
+
+
+def luffy_dispatch_bwd_residual(layer, d_recv, dy, dx, stream):
+    _check(LIB.luffy_dispatch_bwd_residual(layer, _p(d_recv), _p(dy), _p(dx), stream))
+
+
 def luffy_layer_set_history(layer, prev, S1: float = 0.8, S2: float = 0.2):
     """Fast similarity measurement: take history shortcuts from `prev` (a luffy layer or None)."""
     _check(LIB.luffy_layer_set_history(layer, prev, float(S1), float(S2)))
@@ -340,12 +351,14 @@ def luffy_layer_set_exchange_timeout(layer, ms: int):
     _check(LIB.luffy_layer_set_exchange_timeout(layer, int(ms)))
 
 
-def luffy_sequence_rows(layer, seq_len, world, stream):
-    """K9: distinct representative rows of every rank's sequences on every rank -> [world*S, world] int64."""
+def luffy_sequence_rows(layer, seq_len, world, stream, counts=None):
+    """K9: distinct representative rows of every rank's sequences on every rank -> [sum(counts), world] int64.
+    counts: sequences per rank (None: every rank has len(seq_len))."""
     seq_len = np.ascontiguousarray(seq_len, dtype=np.int32)
     S = seq_len.size
-    out = np.empty((world * S, world), np.int64)
-    _check(LIB.luffy_sequence_rows(layer, seq_len.ctypes.data, S, out.ctypes.data, stream))
+    cnt = np.full(world, S, np.int32) if counts is None else np.ascontiguousarray(counts, dtype=np.int32)
+    out = np.empty((int(cnt.sum()), world), np.int64)
+    _check(LIB.luffy_sequence_rows(layer, seq_len.ctypes.data, S, cnt.ctypes.data, out.ctypes.data, stream))
     return out
 
 

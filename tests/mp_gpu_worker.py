@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--h", type=float, default=0.9)
     ap.add_argument("--migrate", default="none", choices=["none", "plan", "rotate"])
     ap.add_argument("--q", type=int, default=2)
+    ap.add_argument("--residual", action="store_true", help="residual block y = x + MoE(x) (luffy_uncondense_residual)")
+    ap.add_argument("--uneven", action="store_true", help="different sequence counts per rank (migration)")
     args = ap.parse_args()
     from paper_2411_15419_b200 import layer as LY
     from paper_2411_15419_b200 import luffy as L
@@ -66,26 +68,36 @@ def main():
                                world=world, rank=rank, device=dev)
     mig = None
     if args.migrate == "none":
-        y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True)
-        g = lay.backward(dy, x, wg, w1, w2, w3)
+        y = lay.forward(x, wg, w1, w2, w3, h=args.h, stats=True, want_rows=True, residual=args.residual)
+        g = lay.backward(dy, x, wg, w1, w2, w3, residual=args.residual)
     else:
         # sequences: the workload's own (seqs_per_rank x seq_len), split unevenly to exercise Eq. (1)
-        L_ = cfg.seq_len
-        seq_len = []
-        for _ in range(cfg.seqs_per_rank):
-            seq_len += [L_ // 4, L_ - L_ // 4]
+        def split(q_):
+            L_ = cfg.seq_len
+            sl = []
+            for _ in range(cfg.seqs_per_rank):
+                if args.uneven and q_ % 2 == 1:
+                    sl += [L_ // 8, L_ // 8, L_ // 4, L_ // 2]
+                else:
+                    sl += [L_ // 4, L_ - L_ // 4]
+            return sl
+        seq_len = split(rank)
         S = len(seq_len)
+        counts = [len(split(q_)) for q_ in range(world)]
         forced = None
         if args.migrate == "rotate":
-            forced = np.array([((q + 1) % world) for q in range(world) for _ in range(S)], np.int32)
+            forced = np.array([((q + 1) % world) for q in range(world) for _ in range(counts[q])], np.int32)
         y, home_rank, home_tok, seq_dest, rows_at = lay.forward_migrated(x, wg, w1, w2, w3, h=args.h, seq_len=seq_len,
-                                                                         q=args.q, seq_dest=forced)
-        mig = dict(S=S, seq_len=seq_len, home_rank=home_rank, home_tok=home_tok, seq_dest=seq_dest, rows_at=rows_at)
+                                                                         q=args.q, seq_dest=forced, residual=args.residual,
+                                                                         stats=True)
+        mig = dict(S=S, seq_len=seq_len, home_rank=home_rank, home_tok=home_tok, seq_dest=seq_dest, rows_at=rows_at,
+                   counts=counts, splits=[split(q_) for q_ in range(world)])
         # dY of the hosted tokens, from every home rank's seeded dY
         dys = {q: workload.make_layer_inputs(cfg, rank=q)["dY"] for q in set(home_rank.tolist())}
         dy_out = np.stack([dys[int(h_)][int(t_)] for h_, t_ in zip(home_rank, home_tok)]) if len(home_rank) else \
             np.zeros((0, cfg.d_model), np.float32)
-        g = lay.backward(dt(dy_out) if len(dy_out) else dt(np.zeros((1, cfg.d_model), np.float32)), x, wg, w1, w2, w3)
+        g = lay.backward(dt(dy_out) if len(dy_out) else dt(np.zeros((1, cfg.d_model), np.float32)), x, wg, w1, w2, w3,
+                         residual=args.residual)
     torch.cuda.synchronize()
     idx = lay.idx[:T].cpu().numpy().astype(np.int64)
     rep = lay.rep[:T].cpu().numpy().astype(np.int64)
@@ -106,20 +118,23 @@ def main():
                               renormalize=cfg.renormalize)
         dW1 += gr.dW1[loc]
         dW2 += gr.dW2[loc]
-        oracle_Y[q] = st.Y
+        # residual block y = x + MoE(x): the identity branch adds x to Y and dY to dX
+        oracle_Y[q] = st.Y + (iq["X"] if args.residual else 0.0)
+        dX_ref = gr.dX + (iq["dY"] if args.residual else 0.0)
         if mig is not None:
             # K9 pin: distinct representative rows of each of rank q's sequences on each rank
-            starts = np.concatenate([[0], np.cumsum(mig["seq_len"])])
-            for s_ in range(mig["S"]):
+            starts = np.concatenate([[0], np.cumsum(mig["splits"][q])])
+            base = int(sum(mig["counts"][:q]))
+            for s_ in range(mig["counts"][q]):
                 slots = set(st.pk.pos[starts[s_]:starts[s_ + 1]].ravel().tolist())
                 owner = [int(st.pk.slot_expert[u]) // El for u in slots]
                 exp_rows = np.bincount(owner, minlength=world)
-                if not np.array_equal(exp_rows, mig["rows_at"][q * mig["S"] + s_]):
+                if not np.array_equal(exp_rows, mig["rows_at"][base + s_]):
                     errs["rows_at"] = 1.0
         if q == rank:
             if mig is None:
-                errs["Y"] = rel(y.float().cpu().numpy(), st.Y)
-            errs["dx"] = rel(g["dx"].float().cpu().numpy(), gr.dX)
+                errs["Y"] = rel(y.float().cpu().numpy(), oracle_Y[q])
+            errs["dx"] = rel(g["dx"].float().cpu().numpy(), dX_ref)
             errs["dwg"] = rel(g["dwg"].cpu().numpy(), gr.dWg)
             errs["dw"] = rel(g["dw"].cpu().numpy(), gr.dw)
     if mig is not None:
@@ -129,7 +144,7 @@ def main():
         errs.setdefault("rows_at", 0.0)
         # the planner on every rank agrees with the oracle's Alg. 1 on the same table
         if args.migrate == "plan":
-            lens_all = np.array(mig["seq_len"] * world, np.int64)
+            lens_all = np.array([v for sl in mig["splits"] for v in sl], np.int64)
             od, _ = O.plan_migration(lens_all, mig["rows_at"], args.q, cfg.d_model * 2, cfg.d_model)
             errs["plan"] = 0.0 if np.array_equal(od, mig["seq_dest"]) else 1.0
     errs["dw1"] = rel(g["dw1"].cpu().numpy(), dW1)
@@ -141,7 +156,7 @@ def main():
     ok = route_ok and all(v <= tol for v in errs.values())
     extra = {}
     if mig is not None:
-        extra = {"migrated_seqs": int(np.sum(mig["seq_dest"] != np.repeat(np.arange(world), mig["S"]))),
+        extra = {"migrated_seqs": int(np.sum(mig["seq_dest"] != np.repeat(np.arange(world), mig["counts"]))),
                  "hosted_tokens": int(len(mig["home_rank"]))}
     print(json.dumps({"rank": rank, "world": world, "ok": ok, "route_ok": route_ok, "errs": errs, **extra,
                       "reps": int(lay.stats.reps) if lay.stats else -1,

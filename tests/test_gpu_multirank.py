@@ -38,12 +38,24 @@ def test_expert_parallel_parity(n, config, h):
     assert r.stdout.count('"ok": true') == n
 
 
-@pytest.mark.parametrize("n,mode", [(2, "rotate"), (2, "plan"), (4, "plan"), (4, "rotate")])
-def test_sequence_migration_parity(n, mode):
+@pytest.mark.parametrize("n,extra", [(2, ("--residual",)), (4, ("--residual",))])
+def test_residual_block_parity(n, extra):
+    """Residual block y = x + MoE(x) (luffy_uncondense_residual / luffy_dispatch_bwd_residual) at world > 1."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    r = _run(n, "C2S", 0.9, extra=extra)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"ok": true') == n
+
+
+@pytest.mark.parametrize("n,mode,extra", [(2, "rotate", ()), (2, "plan", ()), (4, "plan", ()), (4, "rotate", ()),
+                                          (2, "plan", ("--residual", "--uneven")),
+                                          (4, "rotate", ("--residual", "--uneven"))])
+def test_sequence_migration_parity(n, mode, extra):
     """Alg. 1 in the layer: K9 rows_at exact vs the oracle, the planner's seq_dest equal to the oracle's
     Alg. 1, outputs at the hosting rank and all gradients at home / expert ranks within tolerance."""
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    r = _run(n, "C2S", 0.9, extra=("--migrate", mode, "--q", "2"))
+    r = _run(n, "C2S", 0.9, extra=("--migrate", mode, "--q", "2") + tuple(extra))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count('"ok": true') == n

@@ -298,3 +298,26 @@ def test_fallback_paths_subprocess():
                         "test_ragged_bf16 or test_c1_fp32_simulated_ranks or test_fp32_fused_gate_backward"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_residual_block():
+    """y = x + MoE(x) (luffy_uncondense_residual) and dx = dy + ... (luffy_dispatch_bwd_residual), world 1."""
+    import torch
+    from paper_2411_15419_b200 import layer as LY
+    cfg = C2S
+    inp = _inputs(cfg)
+    T = inp["X"].shape[0]
+    lay = LY.CondensedMoELayer(cfg.num_experts, cfg.top_k, cfg.d_model, cfg.d_ffn, max_tokens=T)
+    from parity_util import to_dev
+    x, dy = to_dev(inp["X"], "bf16"), to_dev(inp["dY"], "bf16")
+    w1, w2 = to_dev(inp["W1"], "bf16"), to_dev(inp["W2"], "bf16")
+    wg = torch.from_numpy(inp["Wg"]).cuda()
+    y = lay.forward(x, wg, w1, w2, None, h=0.9, residual=True).float().cpu().numpy()
+    g = lay.backward(dy, x, wg, w1, w2, None, residual=True)
+    torch.cuda.synchronize()
+    res = dict(T=T, idx=lay.idx[:T].cpu().numpy().astype(np.int64), rep=lay.rep[:T].cpu().numpy().astype(np.int64))
+    st, gr = oracle_frozen(cfg, inp, res, 0.9)
+    assert rel_err(y, st.Y + inp["X"]) < 2e-2
+    assert rel_err(g["dx"].float().cpu().numpy(), gr.dX + inp["dY"]) < 2e-2
+    assert rel_err(g["dw1"].cpu().numpy(), gr.dW1) < 2e-2
+    lay.close()

@@ -295,6 +295,124 @@ def run_reference(args, cfg):
     print(json.dumps(out), flush=True)
 
 
+def stack_lengths(T: int, rng) -> list[int]:
+    """Variable sequence lengths l ~ U{256, ..., 1024 step 64} summing to T (the padding premise of
+    sequence migration, P:88 / P:296; SURVEY §8(d) C4 lengths)."""
+    lens = []
+    while sum(lens) < T:
+        lens.append(int(min(rng.choice(np.arange(256, 1025, 64)), T - sum(lens))))
+    return lens
+
+
+def run_stack(args, cfg):
+    """BASELINE config 4: the C4 block stack (attention at the hosting rank + condensed MoE, residuals),
+    fwd+bwd per step, migration on (--migrate q) or off, history shortcuts (--history S1,S2)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_15419_b200 import stack as SK
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T = cfg.tokens_per_rank
+    X, _, _ = workload.make_tokens(cfg, rank=rank)
+    x0 = torch.from_numpy(X).to(dev, torch.bfloat16)
+    lens0 = stack_lengths(T, np.random.default_rng(4242 + rank))
+    hist = tuple(float(v) for v in args.history.split(",")) if args.history else None
+    st = SK.MoEStack(args.stack, cfg.num_experts, cfg.top_k, cfg.d_model, cfg.d_ffn, T, world=world, rank=rank,
+                     device=dev, h=cfg.h, migrate_q=args.migrate, history=hist, gate=workload.make_gate(cfg),
+                     total_seqs=max(256, 4 * len(lens0) * world))
+    g = torch.Generator(device=dev)
+    g.manual_seed(99 + rank)
+    dy_pool = torch.randn(st.cap, cfg.d_model, generator=g, device=dev).to(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(local).start()
+    for _ in range(args.warmup):
+        st.step(x0, lens0, dy_pool)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host0 = time.time()
+    a.record(stream)
+    for _ in range(args.steps):
+        st.step(x0, lens0, dy_pool)
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk.window = (t_host0, time.time())
+    time.sleep(0.06)
+    clk.stop()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    # ---- diagnostic pass: attention forward per block (CUDA events) against Eq. (1); condensation stats
+    samples, mig, hstats = [], [], []
+    for blk in st.blocks:
+        blk.want_stats = True
+    x, lens = x0, lens0
+    for blk in st.blocks:
+        blk.lens_in = list(lens)
+        if st.migrate:
+            blk.lens_all = [None] * world
+            dist.all_gather_object(blk.lens_all, [int(v) for v in lens])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.no_grad():
+            for _ in range(2):
+                blk.attention(x)          # warm
+            e0.record(stream)
+            for _ in range(5):
+                xa = blk.attention(x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            Bq, Lm = len(lens), max(lens)
+            samples.append((Bq, Lm, sum(lens), e0.elapsed_time(e1) / 5))
+            x = blk.moe_forward(xa)
+        lens = blk.lens_out
+        s_ = blk.layer.stats
+        if s_ is not None:
+            hstats.append({"reps": int(s_.reps), "copies": int(s_.copies), "decided_pairs": int(s_.decided_pairs),
+                           "skipped_tiles": int(s_.skipped_tiles)})
+        mig.append(dict(blk.mig_info))
+        blk.want_stats = False
+    allsamples = [samples]
+    if world > 1:
+        allsamples = [None] * world
+        dist.all_gather_object(allsamples, samples)
+    flat = [s_ for r_ in allsamples for s_ in r_]
+    ops = np.array([SK.attention_flops(B_, L_, cfg.d_model) for B_, L_, _, _ in flat], np.float64)
+    tms = np.array([t_ for _, _, _, t_ in flat], np.float64)
+    c = float((ops * tms).sum() / (ops * ops).sum())         # t = ops / P_eff, least squares
+    rel = np.abs(tms - c * ops) / tms
+    pad_eff = float(sum(n_ for _, _, n_, _ in flat) / sum(B_ * L_ for B_, L_, _, _ in flat))
+    att_ms = float(np.mean([sum(t_ for _, _, _, t_ in r_) for r_ in allsamples]))
+    if rank == 0:
+        out = {"metric": "MoE stack fwd+bwd tokens/s", "value": world * T * args.steps / (ms / 1e3), "unit": UNIT,
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+               "config": {"workload": f"{cfg.name} x {args.stack} blocks (attention + condensed MoE, residual)",
+                          "tokens_per_rank": T, "E": cfg.num_experts, "k": cfg.top_k, "d_model": cfg.d_model,
+                          "d_ffn": cfg.d_ffn, "h": cfg.h, "seq_len": "U{256..1024 step 64}",
+                          "migration_q": args.migrate if st.migrate else 0, "history_S1_S2": hist,
+                          "parallelism": f"ep{world}"},
+               "attention": {"fwd_ms_per_step_mean_rank": att_ms, "padding_efficiency": pad_eff,
+                             "eq1_fit": {"P_eff_ops_per_s": 1.0 / c * 1e3, "mean_rel_err": float(rel.mean()),
+                                         "max_rel_err": float(rel.max()), "samples": len(flat),
+                                         "model": "t = (3 B L d^2 + 2 B L^2 d) / P (Eq. 1, P:307), least squares"}},
+               "migration_per_block_rank0": mig if st.migrate else None, "condense_per_block_rank0": hstats,
+               "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -310,6 +428,8 @@ def main():
     ap.add_argument("--no-ktab", action="store_true", help="skip the CUPTI per-kernel pass (e.g. under ncu)")
     ap.add_argument("--migrate", type=int, default=0,
                     help="world > 1: sequence migration with Alg. 1 candidate-set size q (0 = off)")
+    ap.add_argument("--stack", type=int, default=0, help="run the N-block stack (attention + MoE) instead of one layer")
+    ap.add_argument("--history", default=None, help="S1,S2: fast similarity measurement across blocks (stack)")
     ap.add_argument("--kprof", type=int, default=0, help="also write a warm per-kernel table over this many steps")
     ap.add_argument("--kprof-dir", default=os.path.join(ROOT, "gpurun_out"))
     args = ap.parse_args()
@@ -320,6 +440,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.stack > 0:
+        return run_stack(args, cfg)
 
     import torch
     import torch.distributed as dist

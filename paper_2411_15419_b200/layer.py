@@ -114,7 +114,7 @@ class CondensedMoELayer:
 
     def forward_migrated(self, x: torch.Tensor, w_gate: torch.Tensor, w1, w2, w3=None, h: float = 0.9,
                          seq_len=None, q: int = 1, seq_dest=None, capacity: int = 0, objective: int = 0, group=None,
-                         residual: bool = False, stats: bool = False):
+                         residual: bool = False, stats: bool = False, lens_all=None, want_tokens: bool = True):
         """Forward with sequence migration (world > 1): K9 rows -> Alg. 1 on every rank (the
         C-ABI planner, or a given `seq_dest`) -> the combine delivers each sequence's expert outputs to
         the rank hosting it.  Returns (y [n_out, d] for the hosted tokens, home_rank, home_token,
@@ -128,8 +128,10 @@ class CondensedMoELayer:
         L.luffy_route(self.layer, x, w_gate, T, self.idx, self.w, s)
         self.stats = L.luffy_condense(self.layer, x, h, self.rep, s, stats=stats)
         self.mig = True
-        lens = [None] * self.world
-        dist.all_gather_object(lens, [int(v) for v in seq_len], group=group)
+        lens = lens_all
+        if lens is None:
+            lens = [None] * self.world
+            dist.all_gather_object(lens, [int(v) for v in seq_len], group=group)
         seq_len_all = np.array([v for ls in lens for v in ls], np.int32)
         rows_at = L.luffy_sequence_rows(self.layer, seq_len, self.world, s, counts=[len(v) for v in lens])
         if seq_dest is None:
@@ -145,6 +147,8 @@ class CondensedMoELayer:
             L.luffy_uncondense_residual(self.layer, None, x, self.y_out, s)
         else:
             L.luffy_uncondense(self.layer, None, self.y_out, s)
+        if not want_tokens:
+            return self.y_out[:n_out], None, None, np.asarray(seq_dest), rows_at
         torch.cuda.current_stream().synchronize()
         home_rank, home_tok = L.luffy_migration_out_tokens(self.layer, n_out)
         return self.y_out[:n_out], home_rank, home_tok, np.asarray(seq_dest), rows_at

@@ -161,6 +161,8 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->gloc = cv.take<int32_t>(m.C);
   o->gcopy = cv.take<int32_t>(m.Cpad);
   o->gw = cv.take<float>(m.Cpad);
+  o->gchunk = cv.take<int32_t>((size_t)((m.Tmax + 127) / 128) * m.E);
+  o->gticket = cv.take<uint32_t>(1);
   o->xg = cv.take<char>(m.Cpad * m.d * es);
   o->gnorm = cv.take<double>(m.Cpad);
   o->adjoff = cv.take<int64_t>(m.E + 1);
@@ -437,6 +439,13 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   std::memset(L, 0, sizeof(*L));
   Carver cv{static_cast<char*>(ws)};
   carve(&ctx->cfg, cv, L);
+  {  // the grouping's last-CTA ticket starts at zero (every launch leaves it at zero)
+    cudaError_t e = cudaMemset(L->gticket, 0, sizeof(uint32_t));
+    if (e != cudaSuccess) {
+      delete L;
+      return cuda_fail(e, "luffy_layer_create (workspace init)");
+    }
+  }
   const Dims m = dims_of(&ctx->cfg);
   L->ctx = ctx;
   L->P = m.P;

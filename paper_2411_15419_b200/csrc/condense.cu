@@ -21,151 +21,139 @@
 namespace luffy {
 namespace {
 
-// One CTA per expert (every CTA recounts all experts).  When T*k fits (staged != 0), idx and w are first
-// copied to shared memory with coalesced loads, so the histogram and the in-order scan over the tokens
-// read no global memory inside their loops.
-__global__ void __launch_bounds__(1024) group_build_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w,
-                                                           int T, int k, int E, int staged, int32_t* __restrict__ gcnt,
-                                                           int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
-                                                           float* __restrict__ gw, int32_t* __restrict__ gloc,
-                                                           int32_t* __restrict__ gcopy) {
+// Grouping (fast-similarity step 1) in two launches over token chunks of GB_TCH tokens:
+//  group_count_kernel   per chunk, copies per expert; the last CTA to finish (ticket) scans the chunk
+//                       counts per expert into chunk prefixes and derives gcnt, goff (segments padded to
+//                       kRowAlign), the adjacency word offsets and the greedy control block;
+//  group_place_kernel   per chunk, the group row of every copy = goff[e] + chunk prefix + rank among the
+//                       chunk's copies of e in token order (per-expert token bitmaps in shared memory), then
+//                       one warp per token copies its row into each of its k group rows and writes the fp64
+//                       norm -- x is read once per token.  Padding rows are zeroed.
+constexpr int GB_TCH = 128;
+
+__global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __restrict__ idx, int T, int k, int E,
+                                                            int32_t* __restrict__ chunk, uint32_t* __restrict__ ticket,
+                                                            int32_t* __restrict__ gcnt, int32_t* __restrict__ goff,
+                                                            int64_t* __restrict__ adjoff, uint32_t* __restrict__ ctrl) {
   pdl_enter();
-  extern __shared__ __align__(16) int32_t gb_smem[];  // staged: idx [T*k] then w [T*k]
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
-  __shared__ int offs[LUFFY_MAX_EXPERTS + 1];
-  __shared__ int warp_sums[33];
-  const int e = blockIdx.x;
-  const int n = T * k;
-  const int32_t* ix = idx;
-  const float* wx = w;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = 0;
-  if (staged) {
-    int32_t* si = gb_smem;
-    float* sw = reinterpret_cast<float*>(gb_smem + ((n + 3) & ~3));
-    const bool vec = (n & 3) == 0;
-    if (vec) {
-      for (int i = threadIdx.x; i < n / 4; i += blockDim.x) {
-        reinterpret_cast<int4*>(si)[i] = reinterpret_cast<const int4*>(idx)[i];
-        reinterpret_cast<float4*>(sw)[i] = reinterpret_cast<const float4*>(w)[i];
-      }
-    } else {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        si[i] = idx[i];
-        sw[i] = w[i];
-      }
-    }
-    ix = si;
-    wx = sw;
-  }
+  __shared__ bool last;
+  const int c = blockIdx.x, nch = gridDim.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[ix[i]], 1);
+  const int t = c * GB_TCH + threadIdx.x;
+  if (t < T)
+    for (int j = 0; j < k; ++j) atomicAdd(&cnt[idx[(size_t)t * k + j]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) chunk[(size_t)c * E + e] = cnt[e];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == (uint32_t)nch - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last CTA: exclusive prefix over chunks per expert (in place), totals, padded offsets
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int cc = 0; cc < nch; ++cc) {
+      const int v = __ldcg(chunk + (size_t)cc * E + e);
+      chunk[(size_t)cc * E + e] = run;
+      run += v;
+    }
+    cnt[e] = run;
+    gcnt[e] = run;
+  }
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block reset
   __syncthreads();
   if (threadIdx.x == 0) {
-    offs[0] = 0;
-    for (int g = 0; g < E; ++g) offs[g + 1] = offs[g] + (cnt[g] + kRowAlign - 1) / kRowAlign * kRowAlign;
-  }
-  __syncthreads();
-  if (e == 0) {
-    for (int i = threadIdx.x; i <= E; i += blockDim.x) {
-      goff[i] = offs[i];
-      if (i < E) gcnt[i] = cnt[i];
+    int o = 0;
+    int64_t w = 0;
+    for (int e = 0; e < E; ++e) {
+      goff[e] = o;
+      adjoff[e] = w;
+      const int np = (cnt[e] + kRowAlign - 1) / kRowAlign * kRowAlign;
+      o += np;
+      w += (int64_t)np * np / 32;
     }
-  }
-  // every warp owns a contiguous token range: count its copies of expert e, one block-wide scan of the
-  // 32 counts, then each warp places its copies in token order (ballot ranks) -- one scan instead of one
-  // per 1024 tokens
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int per = (T + nw - 1) / nw;
-  const int ta = min(T, wid * per), tb = min(T, ta + per);
-  auto slot_of = [&](int t) {
-    int jj = -1;
-    if (t < tb)
-      for (int j = 0; j < k; ++j)
-        if (ix[(size_t)t * k + j] == e) jj = j;
-    return jj;
-  };
-  int mine = 0;
-  for (int t0 = ta; t0 < tb; t0 += 32) mine += __popc(__ballot_sync(0xffffffffu, slot_of(t0 + lane) >= 0));
-  if (lane == 0) warp_sums[wid] = mine;
-  __syncthreads();
-  if (wid == 0) {
-    const int v = lane < nw ? warp_sums[lane] : 0;
-    int inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    if (lane < nw) warp_sums[lane] = inc - v;
-  }
-  __syncthreads();
-  int base = offs[e] + warp_sums[wid];
-  for (int t0 = ta; t0 < tb; t0 += 32) {
-    const int t = t0 + lane;
-    const int jj = slot_of(t);
-    const unsigned b = __ballot_sync(0xffffffffu, jj >= 0);
-    if (jj >= 0) {
-      const int g = base + __popc(b & ((1u << lane) - 1u));
-      gtok[g] = t;
-      gw[g] = wx[(size_t)t * k + jj];
-      gloc[(size_t)t * k + jj] = g;
-      gcopy[g] = t * k + jj;
-    }
-    base += __popc(b);
-  }
-  for (int g = offs[e] + cnt[e] + threadIdx.x; g < offs[e + 1]; g += blockDim.x) {
-    gtok[g] = -1;
-    gw[g] = 0.f;
-    gcopy[g] = -1;
+    goff[E] = o;
+    adjoff[E] = w;
+    *ticket = 0u;
   }
 }
 
-// xg[g] = x[gtok[g]] (zero for padding), gnorm[g] = |x| in fp64.  One warp per padded row.
 template <typename T>
-__global__ void __launch_bounds__(256) gather_norm_kernel(const T* __restrict__ x, const int32_t* __restrict__ gtok,
-                                                          const int32_t* __restrict__ goff, int E, int d,
-                                                          T* __restrict__ xg, double* __restrict__ gnorm,
-                                                          int64_t* __restrict__ adjoff, uint32_t* __restrict__ ctrl) {
+__global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ x, const int32_t* __restrict__ idx,
+                                                          const float* __restrict__ w, int Tn, int k, int E, int d,
+                                                          const int32_t* __restrict__ chunk, const int32_t* __restrict__ gcnt,
+                                                          const int32_t* __restrict__ goff, int32_t* __restrict__ gtok,
+                                                          float* __restrict__ gw, int32_t* __restrict__ gloc,
+                                                          int32_t* __restrict__ gcopy, T* __restrict__ xg,
+                                                          double* __restrict__ gnorm) {
   pdl_enter();
-  if (blockIdx.x == 0) {  // also: word offsets of each group's adjacency (sum of npad^2 / 32) and the greedy
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // control block reset
-    if (threadIdx.x == 0) {
-      int64_t o = 0;
-      for (int e = 0; e < E; ++e) {
-        adjoff[e] = o;
-        const int64_t np = goff[e + 1] - goff[e];
-        o += np * np / 32;
-      }
-      adjoff[E] = o;
-    }
+  __shared__ uint32_t bits[LUFFY_MAX_EXPERTS][GB_TCH / 32];
+  __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
+  __shared__ int32_t rows_s[GB_TCH][8];
+  const int c = blockIdx.x, nch = gridDim.x;
+  const int t0 = c * GB_TCH;
+  const int nt = min(GB_TCH, Tn - t0);
+  for (int i = threadIdx.x; i < E * (GB_TCH / 32); i += blockDim.x) bits[i / (GB_TCH / 32)][i % (GB_TCH / 32)] = 0u;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) base_s[e] = goff[e] + chunk[(size_t)c * E + e];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int tl = i / k;
+    atomicOr(&bits[idx[(size_t)(t0 + tl) * k + i % k]][tl >> 5], 1u << (tl & 31));
   }
-  const int lane = threadIdx.x & 31;
-  const int64_t rows = goff[E];
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < rows; g += nw) {
-    const int t = gtok[g];
-    T* dst = xg + g * d;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int tl = i / k, j = i % k;
+    const int t = t0 + tl;
+    const int e = idx[(size_t)t * k + j];
+    int rank = __popc(bits[e][tl >> 5] & ((1u << (tl & 31)) - 1u));
+    for (int q = 0; q < (tl >> 5); ++q) rank += __popc(bits[e][q]);
+    const int g = base_s[e] + rank;
+    rows_s[tl][j] = g;
+    gtok[g] = t;
+    gw[g] = w[(size_t)t * k + j];
+    gloc[(size_t)t * k + j] = g;
+    gcopy[g] = t * k + j;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int tl = wid; tl < nt; tl += nw) {  // one warp per token: its row into each of its k group rows
+    const T* src = x + (size_t)(t0 + tl) * d;
     double ss = 0.0;
-    if (t < 0) {
-      for (int c = lane * 8; c < d; c += 256) zero8(dst + c);
-    } else {
-      const T* src = x + (size_t)t * d;
-      for (int c = lane * 8; c < d; c += 256) {
-        if constexpr (sizeof(T) == 2) {
-          uint4 u = *reinterpret_cast<const uint4*>(src + c);
-          *reinterpret_cast<uint4*>(dst + c) = u;
-        } else {
-          *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
-          *reinterpret_cast<float4*>(dst + c + 4) = *reinterpret_cast<const float4*>(src + c + 4);
+    for (int cc = lane * 8; cc < d; cc += 256) {
+      if constexpr (sizeof(T) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(src + cc);
+        for (int j = 0; j < k; ++j) *reinterpret_cast<uint4*>(xg + (size_t)rows_s[tl][j] * d + cc) = u;
+      } else {
+        const float4 u0 = *reinterpret_cast<const float4*>(src + cc);
+        const float4 u1 = *reinterpret_cast<const float4*>(src + cc + 4);
+        for (int j = 0; j < k; ++j) {
+          *reinterpret_cast<float4*>(xg + (size_t)rows_s[tl][j] * d + cc) = u0;
+          *reinterpret_cast<float4*>(xg + (size_t)rows_s[tl][j] * d + cc + 4) = u1;
         }
-        float v[8];
-        load8(src + c, v);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss += (double)v[i] * (double)v[i];
       }
+      float v[8];
+      load8(src + cc, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += (double)v[i] * (double)v[i];
     }
     ss = warp_sum_d(ss);
-    if (lane == 0) gnorm[g] = sqrt(ss);
+    if (lane < k) gnorm[rows_s[tl][lane]] = sqrt(ss);
+  }
+  // padding rows of the group row space: zero rows, no token; spread over the CTAs
+  for (int e = 0; e < E; ++e) {
+    const int p0 = goff[e] + gcnt[e], p1 = goff[e + 1];
+    for (int r = p0 + c * nw + wid; r < p1; r += nch * nw) {
+      for (int cc = lane * 8; cc < d; cc += 256) zero8(xg + (size_t)r * d + cc);
+      if (lane == 0) {
+        gtok[r] = -1;
+        gw[r] = 0.f;
+        gcopy[r] = -1;
+        gnorm[r] = 0.0;
+      }
+    }
   }
 }
 
@@ -502,22 +490,19 @@ __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int3
 
 int launch_group_build(luffy_layer* L, const void* x, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  // idx and w staged in shared memory when they fit (T*k <= 25600 copies: 200 KiB)
-  constexpr int kStageMax = 25600;
-  LUFFY_CUDA_TRY(smem_optin((const void*)group_build_kernel, kStageMax * 8 + 16));
-  const int n = L->T * L->k;
-  const int staged = n <= kStageMax ? 1 : 0;
-  const size_t smem = staged ? (size_t)((n + 3) & ~3) * 8 : 0;
-  launch_pdl(group_build_kernel, L->E, 1024, smem, st, L->idx, L->w, L->T, L->k, L->E, staged, L->gcnt, L->goff, L->gtok,
-                                            L->gw, L->gloc, L->gcopy);
+  if (L->k > 8) return (int)cudaErrorInvalidValue;
+  const int nch = (L->T + GB_TCH - 1) / GB_TCH;
+  launch_pdl(group_count_kernel, nch, GB_TCH, 0, st, (const int32_t*)L->idx, L->T, L->k, L->E, L->gchunk, L->gticket,
+             L->gcnt, L->goff, L->adjoff, L->ctrl);
   LUFFY_LAUNCHED();
-  int blocks = (int)std::min<int64_t>((L->Cpad_max + 7) / 8, 148 * 16);
   if (L->dtype == LUFFY_BF16)
-    launch_pdl(gather_norm_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->gtok, L->goff, L->E, L->d,
-                                                     static_cast<bf16*>(L->xg), L->gnorm, L->adjoff, L->ctrl);
+    launch_pdl(group_place_kernel<bf16>, nch, 256, 0, st, static_cast<const bf16*>(x), (const int32_t*)L->idx,
+               (const float*)L->w, L->T, L->k, L->E, L->d, (const int32_t*)L->gchunk, (const int32_t*)L->gcnt,
+               (const int32_t*)L->goff, L->gtok, L->gw, L->gloc, L->gcopy, static_cast<bf16*>(L->xg), L->gnorm);
   else
-    launch_pdl(gather_norm_kernel<float>, blocks, 256, 0, st, static_cast<const float*>(x), L->gtok, L->goff, L->E, L->d,
-                                                      static_cast<float*>(L->xg), L->gnorm, L->adjoff, L->ctrl);
+    launch_pdl(group_place_kernel<float>, nch, 256, 0, st, static_cast<const float*>(x), (const int32_t*)L->idx,
+               (const float*)L->w, L->T, L->k, L->E, L->d, (const int32_t*)L->gchunk, (const int32_t*)L->gcnt,
+               (const int32_t*)L->goff, L->gtok, L->gw, L->gloc, L->gcopy, static_cast<float*>(L->xg), L->gnorm);
   LUFFY_LAUNCHED();
   return 0;
 }

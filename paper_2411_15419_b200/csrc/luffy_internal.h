@@ -44,6 +44,8 @@ struct luffy_layer {
   int32_t* gloc;      // [Tmax, k] group row (global, padded space) of copy (t, j)
   int32_t* gcopy;     // [Cpad_max] copy t * k + j of each group row (-1 = padding)
   float* gw;          // [Cpad_max] gate weight of each group row (0 for padding)
+  int32_t* gchunk;    // [ceil(Tmax / 128)][E] per-chunk copies per expert -> chunk prefixes (grouping)
+  uint32_t* gticket;  // [1] last-CTA ticket of the grouping count (zero between launches)
   void* xg;           // [Cpad_max, d] gathered group rows (dtype)
   double* gnorm;      // [Cpad_max] |x| in fp64
   int64_t* adjoff;    // [E+1] word offsets of each group's bit adjacency

@@ -16,8 +16,11 @@ disabled"); SURVEY §8(f) rows 1 and 3.
   from block b-1 (luffy_layer_set_history) -- only without migration, where consecutive blocks see the same
   tokens in the same order on a rank.
 
-Weights are random-initialised on the device (N(0, 0.02^2)); gates follow workload.make_gate with a
-per-block perturbation so that routing changes from block to block.
+Weights are random-initialised on the device, GPT-2 style: N(0, 0.02^2), with the two projections that write
+into the residual stream (the attention's value projection -- Eq. (1) has no separate output projection --
+and the experts' W2) scaled by 1/sqrt(2 n_blocks), so every block perturbs the residual stream by a small
+step as in a trained-from-init transformer; gates follow workload.make_gate with a per-block perturbation
+so that routing changes from block to block.
 """
 from __future__ import annotations
 
@@ -48,7 +51,8 @@ class _MoEFn(torch.autograd.Function):
 
 class Block:
     def __init__(self, index: int, E: int, k: int, d: int, f: int, max_tokens: int, world: int, rank: int,
-                 device, h: float, migrate_q: int, fast_measure: bool, max_seqs: int, gate: np.ndarray, seed: int):
+                 device, h: float, migrate_q: int, fast_measure: bool, max_seqs: int, gate: np.ndarray, seed: int,
+                 n_blocks: int = 1):
         self.i, self.E, self.k, self.d, self.f, self.h = index, E, k, d, f, h
         self.world, self.rank, self.q = world, rank, migrate_q
         self.dev = device
@@ -58,9 +62,12 @@ class Block:
         g = torch.Generator(device=device)
         g.manual_seed(seed + 7919 * index)
         rnd = lambda *shape: (torch.randn(*shape, generator=g, device=device) * 0.02).to(torch.bfloat16)
+        res_scale = 1.0 / np.sqrt(2.0 * n_blocks)  # residual-branch projections (GPT-2 init)
         self.w1 = rnd(El, f, d)
-        self.w2 = rnd(El, d, f)
-        self.wqkv = rnd(d, 3 * d).requires_grad_(True)
+        self.w2 = (rnd(El, d, f).float() * res_scale).to(torch.bfloat16)
+        wqkv = rnd(d, 3 * d)
+        wqkv[:, 2 * d:] = (wqkv[:, 2 * d:].float() * res_scale).to(torch.bfloat16)
+        self.wqkv = wqkv.requires_grad_(True)
         rng = np.random.default_rng(seed + index)
         self.wg = torch.from_numpy((gate * (1.0 + 0.1 * rng.standard_normal(gate.shape))).astype(np.float32)).to(device)
         self.heads = d // 128
@@ -121,7 +128,7 @@ class MoEStack:
             gate = (rng.standard_normal((E, d)) * 0.02).astype(np.float32)
         fm = history is not None and not self.migrate
         self.blocks = [Block(i, E, k, d, f, cap, world, rank, device, h, migrate_q if self.migrate else 0, fm,
-                             total_seqs, gate, seed) for i in range(n_blocks)]
+                             total_seqs, gate, seed, n_blocks) for i in range(n_blocks)]
         if fm:
             S1, S2 = history
             for i, b in enumerate(self.blocks):

@@ -193,6 +193,34 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvlinkCounter:
+    """NVML NVLink data throughput counters of one GPU (KiB, summed over its links): bytes that really
+    crossed NVLink during a window -- the evidence for the fused device-initiated exchanges."""
+
+    def __init__(self, dev: int):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.p = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.read()
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            v = self.p.nvmlDeviceGetFieldValues(self.h, [(self.p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 0xFFFFFFFF),
+                                                         (self.p.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 0xFFFFFFFF)])
+            if any(x.nvmlReturn != 0 for x in v):
+                return None
+            return (v[0].value.ullVal * 1024, v[1].value.ullVal * 1024)
+        except Exception:
+            return None
+
+
 def _bind_local_cpus(dev: int):
     """Pin this process to the CPUs NVML reports as local to the GPU (first-touch placement of the pinned
     host buffers on the GPU's NUMA node); no-op when NVML or the affinity call is unavailable."""
@@ -533,10 +561,12 @@ def main():
         dist.barrier()
     n_ev = len(marks) + 1
     start, stop = ev(), ev()
+    nvl = NvlinkCounter(local) if world > 1 else None
     launches0 = L.luffy_launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    nvl0 = nvl.read() if nvl else None
     t_host0 = time.time()
     start.record(stream)
     for i in range(args.steps):
@@ -544,6 +574,7 @@ def main():
     stop.record(stream)
     host_ms = (time.time() - t_host0) * 1e3 / args.steps  # enqueue time per step (no host sync in the step)
     torch.cuda.synchronize()
+    nvl1 = nvl.read() if nvl else None
     launches = (L.luffy_launch_count() - launches0) // args.steps
     clk.window = (t_host0, time.time())
     time.sleep(0.06)
@@ -714,6 +745,29 @@ def main():
                         "kernel": "memory-side kernels (sum): " + ", ".join(sorted(used)),
                         "algorithmic_bytes": mb, "measured_us": mus, "timing": "CUPTI, warm, PDL off"}
 
+    # ---- NVLink (world > 1): bytes that crossed NVLink per step (NVML counters over the timed region) against
+    # the algorithmic 4 R_remote d B (dispatch, combine and both backward exchanges), and the push bandwidth of
+    # the dispatch kernel alone (its remote bytes / its CUPTI duration) against 900 GB/s nominal and the
+    # 770 GB/s measured peer copy (B200_PROFILING.md)
+    nvlink = None
+    if world > 1:
+        B_ = 2 if cfg.dtype == "bf16" else 4
+        remote_rows = int(reps_e[[e // El != rank for e in range(E)]].sum())
+        alg = 4 * remote_rows * cfg.d_model * B_
+        nv = None
+        if nvl0 and nvl1:
+            nv = {"tx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps, "rx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps}
+        push = None
+        pk = ktab.get("xpack_push_kernel") if ktab else None
+        if pk:
+            gbs = remote_rows * cfg.d_model * B_ / (pk[1] * 1e-6) / 1e9
+            push = {"kernel": "xpack_push_kernel (fused pack + dispatch push)", "remote_bytes": remote_rows * cfg.d_model * B_,
+                    "us": pk[1], "GBps": gbs, "frac_of_900_nominal": gbs / 900.0, "frac_of_770_measured_peer_copy": gbs / 770.0}
+        nvlink = {"algorithmic_bytes_per_step_rank": alg, "nvml_counters_rank": nv, "dispatch_push": push,
+                  "step_avg_GBps_rank": alg / (ms_step * 1e-3) / 1e9}
+        allnv = [None] * world
+        dist.all_gather_object(allnv, nvlink)
+        nvlink = {"per_rank": allnv}
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -731,7 +785,7 @@ def main():
                "greedy_rounds": rounds, "reps_rank0": R,
                "migration": ({"q": args.migrate, **mig_stats} if mig else None),
                "breakdown_ms": breakdown, "roofline": roof, "roofline_gram": gram_roof, "roofline_memory": mem_roof,
-               "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
+               "kernel_shares": shares, "nvlink": nvlink, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches), "host_enqueue_ms_per_step": host_ms, "clocks": clocks}
         print(json.dumps(out), flush=True)
     lay.close()

@@ -52,13 +52,19 @@ __global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __re
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last CTA: exclusive prefix over chunks per expert (in place), totals, padded offsets
+  // last CTA: exclusive prefix over chunks per expert (in place), totals, padded offsets.  The chunk
+  // counts are read with independent loads (batches of 8 per thread) before the running sums.
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int run = 0;
-    for (int cc = 0; cc < nch; ++cc) {
-      const int v = __ldcg(chunk + (size_t)cc * E + e);
-      chunk[(size_t)cc * E + e] = run;
-      run += v;
+    for (int c0 = 0; c0 < nch; c0 += 8) {
+      int v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = c0 + i < nch ? __ldcg(chunk + (size_t)(c0 + i) * E + e) : 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (c0 + i < nch) chunk[(size_t)(c0 + i) * E + e] = run;
+        run += v[i];
+      }
     }
     cnt[e] = run;
     gcnt[e] = run;
@@ -81,6 +87,8 @@ __global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __re
   }
 }
 
+constexpr int GB_SUB = 4;  // placement CTAs per count chunk (GB_TCH / GB_SUB tokens each)
+
 template <typename T>
 __global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ x, const int32_t* __restrict__ idx,
                                                           const float* __restrict__ w, int Tn, int k, int E, int d,
@@ -90,28 +98,30 @@ __global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ 
                                                           int32_t* __restrict__ gcopy, T* __restrict__ xg,
                                                           double* __restrict__ gnorm) {
   pdl_enter();
+  constexpr int SUB = GB_TCH / GB_SUB;
   __shared__ uint32_t bits[LUFFY_MAX_EXPERTS][GB_TCH / 32];
   __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
-  __shared__ int32_t rows_s[GB_TCH][8];
-  const int c = blockIdx.x, nch = gridDim.x;
+  __shared__ int32_t rows_s[SUB][8];
+  const int c = blockIdx.x / GB_SUB, sub = blockIdx.x % GB_SUB, ncta = gridDim.x;
   const int t0 = c * GB_TCH;
-  const int nt = min(GB_TCH, Tn - t0);
+  const int nt = min(GB_TCH, Tn - t0);                 // tokens of the chunk
+  const int s0 = sub * SUB, ns = max(0, min(SUB, nt - s0));  // this CTA's tokens within the chunk
   for (int i = threadIdx.x; i < E * (GB_TCH / 32); i += blockDim.x) bits[i / (GB_TCH / 32)][i % (GB_TCH / 32)] = 0u;
   for (int e = threadIdx.x; e < E; e += blockDim.x) base_s[e] = goff[e] + chunk[(size_t)c * E + e];
   __syncthreads();
-  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+  for (int i = threadIdx.x; i < (s0 + ns) * k; i += blockDim.x) {  // bitmaps of the chunk's tokens up to ours
     const int tl = i / k;
     atomicOr(&bits[idx[(size_t)(t0 + tl) * k + i % k]][tl >> 5], 1u << (tl & 31));
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
-    const int tl = i / k, j = i % k;
+  for (int i = threadIdx.x; i < ns * k; i += blockDim.x) {
+    const int tl = s0 + i / k, j = i % k;
     const int t = t0 + tl;
     const int e = idx[(size_t)t * k + j];
     int rank = __popc(bits[e][tl >> 5] & ((1u << (tl & 31)) - 1u));
     for (int q = 0; q < (tl >> 5); ++q) rank += __popc(bits[e][q]);
     const int g = base_s[e] + rank;
-    rows_s[tl][j] = g;
+    rows_s[tl - s0][j] = g;
     gtok[g] = t;
     gw[g] = w[(size_t)t * k + j];
     gloc[(size_t)t * k + j] = g;
@@ -119,25 +129,31 @@ __global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int tl = wid; tl < nt; tl += nw) {  // one warp per token: its row into each of its k group rows
-    const T* src = x + (size_t)(t0 + tl) * d;
+  for (int tl = wid; tl < ns; tl += nw) {  // one warp per token: its row into each of its k group rows
+    const T* src = x + (size_t)(t0 + s0 + tl) * d;
     double ss = 0.0;
-    for (int cc = lane * 8; cc < d; cc += 256) {
-      if constexpr (sizeof(T) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(src + cc);
-        for (int j = 0; j < k; ++j) *reinterpret_cast<uint4*>(xg + (size_t)rows_s[tl][j] * d + cc) = u;
-      } else {
-        const float4 u0 = *reinterpret_cast<const float4*>(src + cc);
-        const float4 u1 = *reinterpret_cast<const float4*>(src + cc + 4);
-        for (int j = 0; j < k; ++j) {
-          *reinterpret_cast<float4*>(xg + (size_t)rows_s[tl][j] * d + cc) = u0;
-          *reinterpret_cast<float4*>(xg + (size_t)rows_s[tl][j] * d + cc + 4) = u1;
-        }
-      }
-      float v[8];
-      load8(src + cc, v);
+    for (int cb = 0; cb < d; cb += 4 * 256) {  // batches of 4 independent 16-byte loads per lane (bf16)
+      uint4 u[4][sizeof(T) / 2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) ss += (double)v[i] * (double)v[i];
+      for (int b = 0; b < 4; ++b) {
+        const int cc = cb + b * 256 + lane * 8;
+        if (cc < d)
+#pragma unroll
+          for (int h = 0; h < (int)(sizeof(T) / 2); ++h) u[b][h] = reinterpret_cast<const uint4*>(src + cc)[h];
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int cc = cb + b * 256 + lane * 8;
+        if (cc >= d) break;
+        for (int j = 0; j < k; ++j)
+#pragma unroll
+          for (int h = 0; h < (int)(sizeof(T) / 2); ++h)
+            reinterpret_cast<uint4*>(xg + (size_t)rows_s[tl][j] * d + cc)[h] = u[b][h];
+        float v[8];
+        load8(reinterpret_cast<const T*>(&u[b][0]), v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss += (double)v[i] * (double)v[i];
+      }
     }
     ss = warp_sum_d(ss);
     if (lane < k) gnorm[rows_s[tl][lane]] = sqrt(ss);
@@ -145,7 +161,7 @@ __global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ 
   // padding rows of the group row space: zero rows, no token; spread over the CTAs
   for (int e = 0; e < E; ++e) {
     const int p0 = goff[e] + gcnt[e], p1 = goff[e + 1];
-    for (int r = p0 + c * nw + wid; r < p1; r += nch * nw) {
+    for (int r = p0 + blockIdx.x * nw + wid; r < p1; r += ncta * nw) {
       for (int cc = lane * 8; cc < d; cc += 256) zero8(xg + (size_t)r * d + cc);
       if (lane == 0) {
         gtok[r] = -1;
@@ -496,11 +512,11 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
              L->gcnt, L->goff, L->adjoff, L->ctrl);
   LUFFY_LAUNCHED();
   if (L->dtype == LUFFY_BF16)
-    launch_pdl(group_place_kernel<bf16>, nch, 256, 0, st, static_cast<const bf16*>(x), (const int32_t*)L->idx,
+    launch_pdl(group_place_kernel<bf16>, nch * GB_SUB, 256, 0, st, static_cast<const bf16*>(x), (const int32_t*)L->idx,
                (const float*)L->w, L->T, L->k, L->E, L->d, (const int32_t*)L->gchunk, (const int32_t*)L->gcnt,
                (const int32_t*)L->goff, L->gtok, L->gw, L->gloc, L->gcopy, static_cast<bf16*>(L->xg), L->gnorm);
   else
-    launch_pdl(group_place_kernel<float>, nch, 256, 0, st, static_cast<const float*>(x), (const int32_t*)L->idx,
+    launch_pdl(group_place_kernel<float>, nch * GB_SUB, 256, 0, st, static_cast<const float*>(x), (const int32_t*)L->idx,
                (const float*)L->w, L->T, L->k, L->E, L->d, (const int32_t*)L->gchunk, (const int32_t*)L->gcnt,
                (const int32_t*)L->goff, L->gtok, L->gw, L->gloc, L->gcopy, static_cast<float*>(L->xg), L->gnorm);
   LUFFY_LAUNCHED();

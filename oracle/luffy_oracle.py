@@ -14,7 +14,7 @@ intermediate rounding (reading R13).  Library primitives used as single steps: n
 
 Parity status per function (what pins it, tests/test_oracle_*.py):
   attention_cost        pinned: SPEC worked values 5, 2048; closed-form scaling laws
-  adaptive_threshold    pinned: 0.5, 0.26894, 0.37754
+  adaptive_threshold    pinned: 0.5, 0.26894, 0.37754; c = 2 (reading R17): the same values x 2
   route                 pinned: torch.topk / torch.softmax on fp64 logits; brute force E<=4; sum(w)=1
   normalized_cosine     pinned: s(u,u)=1, s(u,-u)=0, orthogonal=0.5; numpy Gram
   greedy_condense       pinned: SPEC star / two triangles / identity; path 0-1-2-4-3
@@ -55,14 +55,16 @@ def attention_cost(B: int, L: int, d: int, P: int = 1):
     return num if P == 1 else num / P
 
 
-def adaptive_threshold(l_ini: float, l_prev: float) -> float:
-    """Eq. (2), P:384-387, as printed: h_t = 1/(1+exp(l_norm)), l_norm = (l_ini - l_prev)/l_ini.
+def adaptive_threshold(l_ini: float, l_prev: float, c: float = 1.0) -> float:
+    """Eq. (2), P:384-387: h_t = c/(1+exp(l_norm)), l_norm = (l_ini - l_prev)/l_ini; c = 1 as printed.
 
-    Not on the hot path (h is a per-call input; reading R17).  l_prev > l_ini clamps l_norm to 0."""
+    Reading R17: the driver uses c = 2, h in (0.538, 1] -- the printed c = 1 confines h to
+    (0.269, 0.5], contradicting "a high threshold" early in training and Table IV (adaptive keeps
+    accuracy that a static 0.3 loses and beats a static 0.8).  l_prev > l_ini clamps l_norm to 0."""
     if l_ini <= 0:
         raise ValueError("l_ini must be > 0")
     l_norm = max(0.0, (l_ini - l_prev) / l_ini)
-    return 1.0 / (1.0 + math.exp(l_norm))
+    return c / (1.0 + math.exp(l_norm))
 
 
 # ----------------------------------------------------------------------------------------------

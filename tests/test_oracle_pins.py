@@ -71,8 +71,10 @@ def test_eq2_worked_values():
     for line in _rows("eq2_adaptive_threshold.txt"):
         li, lp, exp = map(float, line.split())
         assert abs(O.adaptive_threshold(li, lp) - exp) < 5e-6
+        assert abs(O.adaptive_threshold(li, lp, c=2.0) - 2 * exp) < 1e-5   # reading R17: c = 2
     xs = [O.adaptive_threshold(10.0, lp) for lp in np.linspace(10, 0, 21)]
     assert all(a > b for a, b in zip(xs, xs[1:]))     # strictly decreasing in l_norm
+    assert O.adaptive_threshold(10.0, 12.0, c=2.0) == 1.0   # a rising loss clamps l_norm to 0: maximum caution
 
 
 # ---------------------------------------------------------------- similarity

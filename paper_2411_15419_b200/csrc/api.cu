@@ -175,6 +175,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->win = cv.take<uint32_t>(m.Cpad / 32 + 1);
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);
   o->stat64 = cv.take<uint64_t>(4);
+  o->x_errw = cv.take<uint32_t>(2);
   if (c->fast_measure) {
     o->hone = cv.take<uint32_t>(m.adjw);
     o->hzero = cv.take<uint32_t>(m.adjw);
@@ -193,6 +194,8 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->mstart = cv.take<int32_t>(m.Rpad);
   o->mcnt = cv.take<int32_t>(m.Rpad);
   o->mcur = cv.take<int32_t>(m.Rpad);
+  o->lb_flag = cv.take<uint32_t>(m.Cpad / 128 + 1);
+  o->lb_val = cv.take<unsigned long long>(2 * (m.Cpad / 128 + 1));
   o->marr = cv.take<int32_t>(m.Rpad);
   o->members = cv.take<int32_t>(m.Cpad);
   o->mslot = cv.take<int32_t>(m.Cpad);
@@ -441,6 +444,8 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   carve(&ctx->cfg, cv, L);
   {  // the grouping's last-CTA ticket starts at zero (every launch leaves it at zero)
     cudaError_t e = cudaMemset(L->gticket, 0, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(L->x_errw, 0, 2 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(L->lb_flag, 0, sizeof(uint32_t) * (dims_of(&ctx->cfg).Cpad / 128 + 1));
     if (e != cudaSuccess) {
       delete L;
       return cuda_fail(e, "luffy_layer_create (workspace init)");

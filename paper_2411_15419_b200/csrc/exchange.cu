@@ -129,7 +129,8 @@ int launch_xwait(const luffy_layer* L, int phase, void* s) {
 
 XErr make_xerr(const luffy_layer* L) {
   XErr e;
-  e.word = L->x_err_d;
+  e.word = L->x_errw;
+  e.host = L->x_err_d;
   e.timeout_ns = L->x_timeout_ns;
   return e;
 }

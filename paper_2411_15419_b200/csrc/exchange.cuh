@@ -71,12 +71,14 @@ __device__ __forceinline__ void xsignal_done(const XSignal& s) {
 XSignal make_signal(const luffy_layer* L, int phase);
 
 // Bounded cross-rank wait.  A peer that stops publishing must not hang or kill this rank's context: after
-// `timeout_ns` the waiter records (phase + 1, seq) in the layer's error word -- pinned host memory mapped
-// into the device, so the host reads it without a synchronisation -- and proceeds as if the flag had
-// arrived (the data of that step is garbage; flags are left unchanged).  Every later wait of the layer
+// `timeout_ns` the waiter records (phase + 1, seq) in the layer's error word (device memory, mirrored into
+// pinned host memory mapped into the device, so the host reads it without a synchronisation) and proceeds
+// as if the flag had arrived (the data of that step is garbage; flags are left unchanged).  Every later wait of the layer
 // sees the error word and returns at once, and the next luffy_* call on the layer returns LUFFY_E_STATE.
 struct XErr {
-  uint32_t* word;        // [2] mapped host memory: (phase + 1, seq) of the first timed-out wait, 0 = none
+  uint32_t* word;        // [2] device memory (L2): (phase + 1, seq) of the first timed-out wait, 0 = none
+  uint32_t* host;        // [2] its mirror in mapped pinned host memory (read by the host without a sync;
+                         //     written only on a timeout -- device-side polling never touches PCIe)
   uint64_t timeout_ns;
 };
 
@@ -100,7 +102,11 @@ __device__ __forceinline__ bool xwait_flag(const uint32_t* flag, uint32_t seq, c
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (ld_volatile_u32(e.word) != 0u) return false;
       if (t - t0 > e.timeout_ns) {
-        if (atomicCAS_system(e.word, 0u, (uint32_t)phase + 1u) == 0u) atomicExch_system(e.word + 1, seq);
+        if (atomicCAS(e.word, 0u, (uint32_t)phase + 1u) == 0u) {
+          atomicExch(e.word + 1, seq);
+          atomicExch_system(e.host + 1, seq);
+          atomicExch_system(e.host, (uint32_t)phase + 1u);
+        }
         __threadfence_system();
         return false;
       }

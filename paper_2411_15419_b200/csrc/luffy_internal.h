@@ -80,6 +80,9 @@ struct luffy_layer {
   int32_t* mstart;    // [Rpad_max] first member (group-row space) of each slot's member list
   int32_t* mcnt;      // [Rpad_max] members per slot
   int32_t* mcur;      // [Rpad_max] placement cursor
+  uint32_t* lb_flag;  // [Cpad_max/128] look-back flags of the multi-CTA layout (epoch * 4 + status)
+  unsigned long long* lb_val;  // [2 * Cpad_max/128] look-back aggregates / inclusive prefixes
+  uint32_t lb_epoch;  // host: layout launches so far
   int32_t* marr;      // [Rpad_max] arrivals of the window partials of a slot (uncondense backward)
   int32_t* members;   // [Cpad_max] member group rows, slot-major, token order within a slot
   int32_t* mslot;     // [Cpad_max] slot of each member entry (-1 = padding)
@@ -110,6 +113,7 @@ struct luffy_layer {
   bool x_open;
   uint32_t* x_err_h;     // [2] mapped pinned host memory: first timed-out exchange wait (phase + 1, seq)
   uint32_t* x_err_d;     // its device alias
+  uint32_t* x_errw;      // [2] device copy polled by the waits (workspace)
   uint64_t x_timeout_ns; // bound of every cross-rank wait (LUFFY_EXCHANGE_TIMEOUT_MS, luffy_layer_set_exchange_timeout)
   void* x_recv[2];     // own buffers inside the region
   void* x_gathered;

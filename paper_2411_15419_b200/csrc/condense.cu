@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) group_place_kernel(const T* __restrict__ 
   const int c = blockIdx.x / GB_SUB, sub = blockIdx.x % GB_SUB, ncta = gridDim.x;
   const int t0 = c * GB_TCH;
   const int nt = min(GB_TCH, Tn - t0);                 // tokens of the chunk
-  const int s0 = sub * SUB, ns = max(0, min(SUB, nt - s0));  // this CTA's tokens within the chunk
+  const int s0 = min(sub * SUB, nt), ns = min(SUB, nt - s0);  // this CTA's tokens within the chunk (may be 0)
   for (int i = threadIdx.x; i < E * (GB_TCH / 32); i += blockDim.x) bits[i / (GB_TCH / 32)][i % (GB_TCH / 32)] = 0u;
   for (int e = threadIdx.x; e < E; e += blockDim.x) base_s[e] = goff[e] + chunk[(size_t)c * E + e];
   __syncthreads();

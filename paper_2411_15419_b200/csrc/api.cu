@@ -194,8 +194,6 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->mstart = cv.take<int32_t>(m.Rpad);
   o->mcnt = cv.take<int32_t>(m.Rpad);
   o->mcur = cv.take<int32_t>(m.Rpad);
-  o->lb_flag = cv.take<uint32_t>(m.Cpad / 128 + 1);
-  o->lb_val = cv.take<unsigned long long>(2 * (m.Cpad / 128 + 1));
   o->marr = cv.take<int32_t>(m.Rpad);
   o->members = cv.take<int32_t>(m.Cpad);
   o->mslot = cv.take<int32_t>(m.Cpad);
@@ -445,7 +443,6 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   {  // the grouping's last-CTA ticket starts at zero (every launch leaves it at zero)
     cudaError_t e = cudaMemset(L->gticket, 0, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(L->x_errw, 0, 2 * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMemset(L->lb_flag, 0, sizeof(uint32_t) * (dims_of(&ctx->cfg).Cpad / 128 + 1));
     if (e != cudaSuccess) {
       delete L;
       return cuda_fail(e, "luffy_layer_create (workspace init)");

@@ -52,23 +52,31 @@ __global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __re
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last CTA: exclusive prefix over chunks per expert (in place), totals, padded offsets.  The chunk
-  // counts are read with independent loads (batches of 8 per thread) before the running sums.
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int c0 = 0; c0 < nch; c0 += 8) {
-      int v[8];
+  // last CTA: exclusive prefix over chunks per expert (in place), totals, padded offsets.  One warp per
+  // expert scans its chunk column (lanes over chunks, all loads independent, warp shuffles for the sums).
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = wid; e < E; e += nw) {
+      int carry = 0;
+      for (int c0 = 0; c0 < nch; c0 += 32) {
+        const int cc = c0 + lane;
+        const int v = cc < nch ? __ldcg(chunk + (size_t)cc * E + e) : 0;
+        int inc = v;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = c0 + i < nch ? __ldcg(chunk + (size_t)(c0 + i) * E + e) : 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (c0 + i < nch) chunk[(size_t)(c0 + i) * E + e] = run;
-        run += v[i];
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
+        }
+        if (cc < nch) chunk[(size_t)cc * E + e] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) {
+        cnt[e] = carry;
+        gcnt[e] = carry;
       }
     }
-    cnt[e] = run;
-    gcnt[e] = run;
   }
+  __syncthreads();
   for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block reset
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -80,9 +80,6 @@ struct luffy_layer {
   int32_t* mstart;    // [Rpad_max] first member (group-row space) of each slot's member list
   int32_t* mcnt;      // [Rpad_max] members per slot
   int32_t* mcur;      // [Rpad_max] placement cursor
-  uint32_t* lb_flag;  // [Cpad_max/128] look-back flags of the multi-CTA layout (epoch * 4 + status)
-  unsigned long long* lb_val;  // [2 * Cpad_max/128] look-back aggregates / inclusive prefixes
-  uint32_t lb_epoch;  // host: layout launches so far
   int32_t* marr;      // [Rpad_max] arrivals of the window partials of a slot (uncondense backward)
   int32_t* members;   // [Cpad_max] member group rows, slot-major, token order within a slot
   int32_t* mslot;     // [Cpad_max] slot of each member entry (-1 = padding)

@@ -303,195 +303,6 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
   }
 }
 
-// ---------------------------------------------------------------------------------------------------
-// Layout, multi-CTA (default when representative selection published the per-group counts gnrep): one
-// CTA per 128-row chunk of the group row space (expert segments are 128-row aligned, so a chunk lies in
-// one group).  Slots and member-list starts need prefixes over the chunks of a group: each CTA publishes
-// its (representatives, members) aggregate and finds its exclusive prefix by a decoupled look-back over
-// the group's earlier chunks (flags tagged with the launch epoch, so nothing is reset between launches).
-// A representative's members are the rows whose representative it is; they are its (original) graph
-// neighbours plus itself (claims are of alive neighbours, R9), so one warp walks the representative's
-// adjacency row in word order, which lists the members in token order (R15 / the uncondense backward's
-// summation order) with no sort.
-constexpr int LC = 128;  // rows per chunk = threads per CTA
-
-__device__ __forceinline__ uint32_t member_mask(const uint32_t* __restrict__ arow, const int32_t* __restrict__ rep_local,
-                                                int g0, int n, int li, int w, int g) {
-  // members of representative g (group-local li) among the 32 rows of word w
-  uint32_t bits = arow ? arow[w] : 0u;
-  if ((li >> 5) == w) bits |= 1u << (li & 31);
-  uint32_t m = 0;
-  while (bits) {
-    const int b = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const int r = 32 * w + b;
-    if (r < n && rep_local[g0 + r] == g) m |= 1u << b;
-  }
-  return m;
-}
-
-__global__ void __launch_bounds__(LC) layout_lb_kernel(
-    const int32_t* __restrict__ goff, const int32_t* __restrict__ gcnt, const int32_t* __restrict__ gtok,
-    const int32_t* __restrict__ gcopy, const int32_t* __restrict__ rep_local, const int64_t* __restrict__ adjoff,
-    const uint32_t* __restrict__ adj, int E, int k, const int32_t* __restrict__ gnrep, int32_t* __restrict__ nrep,
-    int32_t* __restrict__ soff, int32_t* __restrict__ lslot, int32_t* __restrict__ perm, int32_t* __restrict__ slot_gl,
-    int32_t* __restrict__ pos, int32_t* __restrict__ rep, int32_t* __restrict__ rep_out, int32_t* __restrict__ mstart,
-    int32_t* __restrict__ mcnt, int32_t* __restrict__ marr, int32_t* __restrict__ members, int32_t* __restrict__ mslot,
-    uint32_t* __restrict__ lb_flag, unsigned long long* __restrict__ lb_val, uint32_t epoch) {
-  pdl_enter();
-  __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
-  __shared__ int32_t soff_s[LUFFY_MAX_EXPERTS + 1];
-  __shared__ int32_t mc_s[LC];
-  __shared__ int warp_sums[33];
-  __shared__ unsigned long long excl_s;
-  __shared__ unsigned rep_words[LC / 32];
-  __shared__ int32_t slot_s[LC], mst_s[LC];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int i = tid; i <= E; i += blockDim.x) goff_s[i] = goff[i];
-  __syncthreads();
-  if (tid == 0) {
-    int o = 0;
-    for (int e = 0; e < E; ++e) {
-      soff_s[e] = o;
-      o += (gnrep[e] + kRowAlign - 1) / kRowAlign * kRowAlign;
-    }
-    soff_s[E] = o;
-  }
-  __syncthreads();
-  const int c = blockIdx.x;
-  if (c == 0)
-    for (int i = tid; i <= E; i += blockDim.x) {
-      soff[i] = soff_s[i];
-      if (i < E) nrep[i] = gnrep[i];
-    }
-  const int g_lo = c * LC;
-  if (g_lo >= goff_s[E]) return;
-  const int e = find_group(goff_s, E, g_lo);
-  const int g0 = goff_s[e], n = gcnt[e], W = (goff_s[e + 1] - g0) >> 5;
-  const uint32_t* A = adj ? adj + adjoff[e] : nullptr;
-  const int g = g_lo + tid, li = g - g0;
-  const bool valid = li < n;
-  const bool isrep = valid && rep_local[g] == g;
-  // member count of every representative of the chunk (warp per representative, lanes over words)
-  mc_s[tid] = 0;
-  __syncthreads();
-  const unsigned repmask_w = __ballot_sync(0xffffffffu, isrep);  // this warp's representatives
-  if (lane == 0) rep_words[wid] = repmask_w;
-  __syncthreads();
-  // the chunk's representatives, in row order, distributed over the warps
-  for (int q = wid; q < LC; q += LC / 32) {
-    if (!((rep_words[q >> 5] >> (q & 31)) & 1u)) continue;
-    const int rg = g_lo + q, rli = rg - g0;
-    const uint32_t* arow = A ? A + (size_t)rli * W : nullptr;
-    int cnt = 0;
-    for (int w = lane; w < W; w += 32) cnt += __popc(member_mask(arow, rep_local, g0, n, rli, w, rg));
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) mc_s[q] = cnt;
-  }
-  __syncthreads();
-  // in-chunk exclusive prefixes: representative rank and member offset (row order)
-  const int my_mc = mc_s[tid];
-  int incR = isrep ? 1 : 0, incM = my_mc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int uR = __shfl_up_sync(0xffffffffu, incR, o), uM = __shfl_up_sync(0xffffffffu, incM, o);
-    if (lane >= o) { incR += uR; incM += uM; }
-  }
-  if (lane == 31) { warp_sums[wid] = incR; warp_sums[8 + wid] = incM; }
-  __syncthreads();
-  int baseR = 0, baseM = 0, totR = 0, totM = 0;
-  for (int q = 0; q < LC / 32; ++q) {
-    if (q < wid) { baseR += warp_sums[q]; baseM += warp_sums[8 + q]; }
-    totR += warp_sums[q];
-    totM += warp_sums[8 + q];
-  }
-  const int rankR = baseR + incR - (isrep ? 1 : 0), rankM = baseM + incM - my_mc;
-  // decoupled look-back over the group's earlier chunks (aggregate: status 1, inclusive prefix: status 2)
-  if (tid == 0) {
-    const int cg0 = g0 / LC;
-    const unsigned long long agg = ((unsigned long long)totR << 32) | (unsigned)totM;
-    unsigned long long ex = 0;
-    if (c > cg0) {
-      lb_val[2 * c] = agg;
-      __threadfence();
-      atomicExch(lb_flag + c, epoch * 4u + 1u);
-      for (int p = c - 1; p >= cg0; --p) {
-        uint32_t f;
-        do { f = atomicAdd(lb_flag + p, 0u); } while ((f >> 2) != epoch);
-        __threadfence();
-        if ((f & 3u) == 2u) { ex += __ldcg(lb_val + 2 * p + 1); break; }
-        ex += __ldcg(lb_val + 2 * p);
-      }
-    }
-    lb_val[2 * c + 1] = ex + agg;
-    __threadfence();
-    atomicExch(lb_flag + c, epoch * 4u + 2u);
-    excl_s = ex;
-  }
-  __syncthreads();
-  const int exR = (int)(excl_s >> 32), exM = (int)(excl_s & 0xffffffffu);
-  const int s0 = soff_s[e];
-  slot_s[tid] = s0 + exR + rankR;
-  mst_s[tid] = g0 + exM + rankM;
-  if (isrep) {
-    const int slot = s0 + exR + rankR;
-    lslot[g] = slot;
-    perm[slot] = gtok[g];
-    slot_gl[slot] = g;
-    mcnt[slot] = my_mc;
-    marr[slot] = 0;
-    mstart[slot] = g0 + exM + rankM;
-  } else if (valid) {
-    lslot[g] = -1;
-  } else {
-    members[g] = -1;   // padding rows of the group row space
-    mslot[g] = -1;
-  }
-  if (c == g0 / LC)  // padding slots of the group's send segment
-    for (int sl = s0 + gnrep[e] + tid; sl < soff_s[e + 1]; sl += blockDim.x) {
-      perm[sl] = -1;
-      slot_gl[sl] = -1;
-      mcnt[sl] = 0;
-      marr[sl] = 0;
-    }
-  __syncthreads();
-  // member lists in token order, and pos / rep of every member copy (warp per representative)
-  for (int q = wid; q < LC; q += LC / 32) {
-    const int rg = g_lo + q, rli = rg - g0;
-    if (!((rep_words[q >> 5] >> (q & 31)) & 1u)) continue;
-    const int slot = slot_s[q];
-    const int tr = gtok[rg];
-    const uint32_t* arow = A ? A + (size_t)rli * W : nullptr;
-    int base = mst_s[q];
-    for (int w0 = 0; w0 < W; w0 += 32) {
-      const int w = w0 + lane;
-      const uint32_t mm = w < W ? member_mask(arow, rep_local, g0, n, rli, w, rg) : 0u;
-      const int cntw = __popc(mm);
-      int inc = cntw;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
-      }
-      int p = base + inc - cntw;
-      uint32_t bits = mm;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const int m = g0 + 32 * w + b;
-        members[p] = m;
-        mslot[p] = slot;
-        const int cp = gcopy[m];
-        pos[cp] = slot;
-        rep[cp] = tr;
-        if (rep_out) rep_out[cp] = tr;
-        ++p;
-      }
-      base += __shfl_sync(0xffffffffu, inc, 31);
-    }
-  }
-}
-
 template <typename T>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const T* __restrict__ x, const int32_t* __restrict__ perm,
                                                         const int32_t* __restrict__ soff, int E, int d,
@@ -864,23 +675,12 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
     const char* v = std::getenv("LUFFY_LAYOUT_SMEM");
     return v && v[0] == '0' ? 0 : 40000;
   }();
-  if (L->gnrep_valid && cur_cap > 0) {  // multi-CTA layout (per-group counts published by the selection)
-    const int nch = (int)(L->Cpad_max / LC);
-    const uint32_t epoch = ++L->lb_epoch;
-    launch_pdl(layout_lb_kernel, nch, LC, 0, st, (const int32_t*)L->goff, (const int32_t*)L->gcnt, (const int32_t*)L->gtok,
-               (const int32_t*)L->gcopy, (const int32_t*)L->rep_local, (const int64_t*)L->adjoff,
-               (const uint32_t*)(L->has_adj ? L->adj : nullptr), L->E, L->k, (const int32_t*)L->gnrep, L->nrep, L->soff,
-               L->lslot, L->perm, L->slot_gl, L->pos, L->rep, rep_out, L->mstart, L->mcnt, L->marr, L->members, L->mslot,
-               L->lb_flag, L->lb_val, epoch);
-    LUFFY_LAUNCHED();
-  } else {
   LUFFY_CUDA_TRY(smem_optin((const void*)layout_kernel, 40000 * 4));
   launch_pdl(layout_kernel, L->E, 1024, (size_t)std::max(cur_cap, 1) * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
                                                  L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out,
                                                  L->gnrep_valid ? L->gnrep : nullptr, cur_cap);
   LUFFY_LAUNCHED();
-  }
 
   if (dst_rows) {
     const int blocks = grid_for_warps(L->Rpad_max);

@@ -35,7 +35,7 @@ class AdaptiveThreshold:
         return self.h
 
 
-def train_adaptive(cfg, inp: dict, iters: int = 40, lr: float = 0.05, scale2: bool = True, device="cuda"):
+def train_adaptive(cfg, inp: dict, iters: int = 40, lr: float = 0.02, scale2: bool = True, device="cuda"):
     """Returns a list of per-iteration dicts: h used, loss, condensed fraction of the copies."""
     dev = torch.device(device)
     bf = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev, torch.bfloat16)

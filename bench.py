@@ -385,11 +385,13 @@ def run_stack(args, cfg):
     for blk in st.blocks:
         blk.want_stats = True
     x, lens = x0, lens0
+    lens_all = None
+    if st.migrate:
+        lens_all = [None] * world
+        dist.all_gather_object(lens_all, [int(v) for v in lens])
     for blk in st.blocks:
         blk.lens_in = list(lens)
-        if st.migrate:
-            blk.lens_all = [None] * world
-            dist.all_gather_object(blk.lens_all, [int(v) for v in lens])
+        blk.lens_all = lens_all
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.no_grad():
             for _ in range(2):
@@ -403,6 +405,7 @@ def run_stack(args, cfg):
             samples.append((Bq, Lm, sum(lens), e0.elapsed_time(e1) / 5))
             x = blk.moe_forward(xa)
         lens = blk.lens_out
+        lens_all = getattr(blk, "lens_all_out", None)
         s_ = blk.layer.stats
         if s_ is not None:
             hstats.append({"reps": int(s_.reps), "copies": int(s_.copies), "decided_pairs": int(s_.decided_pairs),

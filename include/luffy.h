@@ -329,7 +329,9 @@ LUFFY_API luffy_status luffy_sequence_rows(luffy_layer* layer, const int32_t* se
  * every rank hosting a sequence that uses it (GEMM2 epilogue over NVLink); luffy_uncondense writes the
  * tokens this rank hosts (*out_rows of them, host) in (home rank, sequence, token) order -- see
  * luffy_migration_out_tokens; luffy_uncondense_bwd takes dY in that order and returns dY / d(gate weight)
- * to the home ranks.  Before luffy_dispatch.  [sync] */
+ * to the home ranks.  Before luffy_dispatch.  Stream-ordered: the per-sequence tables are copied from the
+ * layer's pinned staging buffer without a stream synchronisation (the call only waits, if at all, for the
+ * previous call's copy to have left that buffer). */
 LUFFY_API luffy_status luffy_set_migration(luffy_layer* layer, const int32_t* seq_len_all, const int32_t* seq_dest,
                                            int64_t* out_rows, void* stream);
 

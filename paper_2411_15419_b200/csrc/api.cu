@@ -523,6 +523,8 @@ void luffy_layer_destroy(luffy_layer* L) {
       if (p != L->rank && L->x_peer_base_h[p]) cudaIpcCloseMemHandle(L->x_peer_base_h[p]);
   if (L->x_region) cudaFree(L->x_region);
   if (L->x_err_h) cudaFreeHost(L->x_err_h);
+  if (L->mig_stage_h) cudaFreeHost(L->mig_stage_h);
+  if (L->mig_stage_ev) cudaEventDestroy(static_cast<cudaEvent_t>(L->mig_stage_ev));
   delete L;
 }
 
@@ -1092,10 +1094,24 @@ luffy_status luffy_set_migration(luffy_layer* L, const int32_t* seq_len_all, con
     }
   if (fill[L->rank] > (int64_t)P * L->Tmax) return fail(LUFFY_E_CAPACITY, "luffy_set_migration: output capacity");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  LUFFY_CHECK(cudaMemcpyAsync(L->seq_dest_l, dest.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st), "seq_dest");
-  LUFFY_CHECK(cudaMemcpyAsync(L->out_start, out_start.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice, st), "out_start");
+  // the per-sequence tables go through the layer's pinned staging buffer (no stream synchronisation): the
+  // previous call's copy must have left it first
+  if (!L->mig_stage_h) {
+    LUFFY_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&L->mig_stage_h), sizeof(int32_t) * 2 * L->Smax, cudaHostAllocDefault),
+                "migration staging");
+    cudaEvent_t ev;
+    LUFFY_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "migration staging event");
+    L->mig_stage_ev = ev;
+  } else {
+    LUFFY_CHECK(cudaEventSynchronize(static_cast<cudaEvent_t>(L->mig_stage_ev)), "migration staging");
+  }
+  std::memcpy(L->mig_stage_h, dest.data(), sizeof(int32_t) * S);
+  std::memcpy(L->mig_stage_h + L->Smax, out_start.data(), sizeof(int32_t) * S);
+  LUFFY_CHECK(cudaMemcpyAsync(L->seq_dest_l, L->mig_stage_h, sizeof(int32_t) * S, cudaMemcpyHostToDevice, st), "seq_dest");
+  LUFFY_CHECK(cudaMemcpyAsync(L->out_start, L->mig_stage_h + L->Smax, sizeof(int32_t) * S, cudaMemcpyHostToDevice, st),
+              "out_start");
+  LUFFY_CHECK(cudaEventRecord(static_cast<cudaEvent_t>(L->mig_stage_ev), st), "migration staging event");
   LUFFY_CHECK(launch_set_migration(L, stream), "luffy_set_migration");
-  LUFFY_CHECK(cudaStreamSynchronize(st), "set_migration sync");  // host vectors go out of scope
   L->n_out = fill[L->rank];
   L->mig = true;
   if (out_rows) *out_rows = L->n_out;

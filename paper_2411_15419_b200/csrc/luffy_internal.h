@@ -134,6 +134,8 @@ struct luffy_layer {
   int Smax;                // sequence capacity per rank
   int S;                   // sequences of the current step (0 = not registered)
   int32_t Sq[64];          // sequences of every rank this step (luffy_sequence_rows)
+  int32_t* mig_stage_h;    // pinned host staging [2 * Smax] (seq_dest, out_start) of luffy_set_migration
+  void* mig_stage_ev;      // cudaEvent_t: the staging copy of the previous call has completed
   bool mig;                // seq_dest set for the current step
   int64_t n_out;           // output rows of this rank (tokens of the sequences it hosts)
   int32_t* seq_start;      // [Smax+1] token range of each of my sequences

@@ -98,9 +98,11 @@ class Block:
         y, _, _, dest, _ = lay.forward_migrated(x, self.wg, self.w1, self.w2, None, h=self.h, seq_len=self.lens_in,
                                                 q=self.q, residual=True, lens_all=self.lens_all, want_tokens=False,
                                                 stats=self.want_stats)
-        # the sequences this rank hosts next, in (home rank, sequence) order (luffy_set_migration's order)
+        # the sequences every rank hosts next, in (home rank, sequence) order (luffy_set_migration's order):
+        # every rank derives the next block's lens_all from the same plan, so no collective is needed
         flat = [(q, l_) for q, ls in enumerate(self.lens_all) for l_ in ls]
-        self.lens_out = [l_ for (q, l_), g in zip(flat, dest) if int(g) == self.rank]
+        self.lens_all_out = [[l_ for (q, l_), g in zip(flat, dest) if int(g) == r] for r in range(self.world)]
+        self.lens_out = self.lens_all_out[self.rank]
         home = np.repeat(np.arange(self.world), [len(v) for v in self.lens_all])
         self.mig_info = {"migrated_seqs": int(np.sum(np.asarray(dest) != home)), "hosted_seqs": len(self.lens_out)}
         return y
@@ -138,14 +140,17 @@ class MoEStack:
         """x [T, d] (this rank's sequences, lengths `lens`); returns (y [T', d], lens') for the sequences this
         rank hosts after the last block."""
         import torch.distributed as dist
+        lens_all = None
+        if self.migrate:  # once per step; later blocks derive every rank's sequences from the plan
+            lens_all = [None] * self.world
+            dist.all_gather_object(lens_all, [int(v) for v in lens])
         for b in self.blocks:
             b.lens_in = list(lens)
-            if self.migrate:
-                b.lens_all = [None] * self.world
-                dist.all_gather_object(b.lens_all, [int(v) for v in lens])
+            b.lens_all = lens_all
             x = b.attention(x)
             x = _MoEFn.apply(x, b)
             lens = b.lens_out
+            lens_all = getattr(b, "lens_all_out", None)
         return x, lens
 
     def step(self, x: torch.Tensor, lens: list[int], dy_pool: torch.Tensor):

@@ -2,8 +2,11 @@
 // pack-and-push of representative rows into the owning ranks' receive buffers (P:143 dispatch phase,
 // only representatives).  No host synchronisation: every rank derives every layout from
 // the all-to-all counts on the device.  See exchange.cuh for the buffers and the signalling protocol.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "exchange.cuh"
+#include "tc_common.cuh"
 
 namespace luffy {
 namespace {
@@ -113,6 +116,68 @@ __global__ void __launch_bounds__(256) xpack_push_kernel(const T* __restrict__ x
   xsignal_done(sig);
 }
 
+// The same fused pack + dispatch through the TMA engine: every representative row streams through a ring of
+// shared-memory row buffers -- bulk load of x[t] (mbarrier completion), then one bulk store of the whole row
+// into its owner's receive buffer (a peer's memory over NVLink, or this GPU's) -- so each row crosses NVLink
+// as one large transfer issued by one thread instead of 16-byte stores from a warp.  Rows are processed in
+// batches of `stages` (all loads of a batch first, then the stores as the loads land).
+template <typename T>
+__global__ void __launch_bounds__(32) xpack_push_tma_kernel(const T* __restrict__ x, const int32_t* __restrict__ perm,
+                                                            const int32_t* __restrict__ soff,
+                                                            const int32_t* __restrict__ dst_base, int E, int El, int d,
+                                                            void* const* peer_recv, XSignal sig,
+                                                            const unsigned long long* __restrict__ dmask,
+                                                            unsigned long long* const* peer_rowmask, int me, int stages) {
+  pdl_enter();
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ int32_t soff_s[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int32_t base_s[LUFFY_MAX_EXPERTS];
+  __shared__ __align__(8) uint64_t bar[32];
+  const int lane = threadIdx.x;
+  for (int i = lane; i <= E; i += 32) {
+    soff_s[i] = soff[i];
+    if (i < E) base_s[i] = dst_base[i];
+  }
+  const uint32_t rb = (uint32_t)(d * sizeof(T));
+  if (lane == 0) {
+    for (int j = 0; j < stages; ++j) tc::mbar_init(&bar[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int64_t rows = soff_s[E];
+    uint32_t phase = 0;
+    for (int64_t b0 = blockIdx.x; b0 < rows; b0 += (int64_t)gridDim.x * stages) {
+      tc::bulk_wait_read();  // the previous batch's stores have read the ring
+      int tj[32];
+      for (int j = 0; j < stages; ++j) {
+        const int64_t s = b0 + (int64_t)j * gridDim.x;
+        tj[j] = s < rows ? perm[s] : -1;
+        if (tj[j] >= 0) {
+          tc::mbar_expect_tx(&bar[j], rb);
+          tc::bulk_load(ring + (size_t)j * rb, x + (size_t)tj[j] * d, rb, &bar[j]);
+        }
+      }
+      for (int j = 0; j < stages; ++j) {
+        if (tj[j] < 0) continue;
+        const int64_t s = b0 + (int64_t)j * gridDim.x;
+        const int e = find_group(soff_s, E, s);
+        const int p = e / El;
+        const int64_t drow = (int64_t)base_s[e] + (s - soff_s[e]);
+        peer_rowmask[p][drow] = dmask ? dmask[s] : (1ull << me);
+        tc::mbar_wait(&bar[j], phase);
+        tc::bulk_store(static_cast<T*>(peer_recv[p]) + drow * d, ring + (size_t)j * rb, rb);
+        tc::bulk_commit();
+      }
+      phase ^= 1u;
+    }
+    tc::bulk_wait_all();                                   // the rows have been written ...
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and are ordered before the release below
+  }
+  __syncwarp();
+  xsignal_done(sig);
+}
+
 inline int grid_warps(int64_t warps) {
   int64_t b = (warps + 7) / 8;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8));
@@ -156,6 +221,32 @@ int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),
                                          static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4, L->x_rowmask);
   LUFFY_LAUNCHED();
+  static const bool tma_push = [] {
+    const char* v = std::getenv("LUFFY_PUSH_TMA");
+    return !(v && v[0] == '0');
+  }();
+  if (tma_push) {  // bulk-copy push (default); LUFFY_PUSH_TMA=0 selects the warp-store push (A/B)
+    const size_t rb = (size_t)L->d * (L->dtype == LUFFY_BF16 ? 2 : 4);
+    const int stages = (int)std::max<size_t>(2, std::min<size_t>(16, (96 * 1024) / rb));
+    const int smem = (int)(stages * rb);
+    const int grid = 2 * device_sms();
+    if (L->dtype == LUFFY_BF16) {
+      LUFFY_CUDA_TRY(smem_optin((const void*)xpack_push_tma_kernel<bf16>, smem));
+      launch_pdl(xpack_push_tma_kernel<bf16>, grid, 32, smem, st, static_cast<const bf16*>(x), (const int32_t*)L->perm,
+                 (const int32_t*)L->soff, (const int32_t*)L->x_dst_base, L->E, L->El, L->d, L->x_peer_recv + par * L->P,
+                 make_signal(L, XP_DISP), (const unsigned long long*)(L->mig ? L->dmask : nullptr), L->x_peer_rowmask,
+                 L->rank, stages);
+    } else {
+      LUFFY_CUDA_TRY(smem_optin((const void*)xpack_push_tma_kernel<float>, smem));
+      launch_pdl(xpack_push_tma_kernel<float>, grid, 32, smem, st, static_cast<const float*>(x), (const int32_t*)L->perm,
+                 (const int32_t*)L->soff, (const int32_t*)L->x_dst_base, L->E, L->El, L->d, L->x_peer_recv + par * L->P,
+                 make_signal(L, XP_DISP), (const unsigned long long*)(L->mig ? L->dmask : nullptr), L->x_peer_rowmask,
+                 L->rank, stages);
+    }
+    LUFFY_LAUNCHED();
+    if (L->dtype == LUFFY_BF16) return 0;
+    return launch_xwait(L, XP_DISP, s);
+  }
   const int blocks = grid_warps(L->Rpad_max);
   if (L->dtype == LUFFY_BF16)
     launch_pdl(xpack_push_kernel<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(x), L->perm, L->soff, L->x_dst_base, L->E,

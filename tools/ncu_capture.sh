@@ -12,3 +12,6 @@ CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-
   python bench.py --config $C --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-ktab "$@" > gpurun_out/${TAG}_ncu_full_${C}.log 2>&1
 python profiles/ncu_summary.py gpurun_out/${TAG}_ncu_full_${C}.ncu-rep --json profiles/${TAG}_ncu_full_${C}_n1.json \
   > profiles/${TAG}_ncu_full_${C}_n1.txt
+cp profiles/${TAG}_ncu_full_${C}_n1.* gpurun_out/
+# the full report stays on the box unless KEEP_REP=1 (gpurun brings back at most 64 MiB)
+[ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/${TAG}_ncu_full_${C}.ncu-rep

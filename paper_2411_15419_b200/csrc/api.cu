@@ -185,6 +185,8 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   }
   o->nrep = cv.take<int32_t>(m.E);
   o->gnrep = cv.take<int32_t>(m.E);
+  o->mrank = cv.take<int32_t>(m.Cpad);
+  o->mcnt_row = cv.take<int32_t>(m.Cpad);
   o->soff = cv.take<int32_t>(m.E + 1);
   o->lslot = cv.take<int32_t>(m.Cpad);
   o->perm = cv.take<int32_t>(m.Rpad);

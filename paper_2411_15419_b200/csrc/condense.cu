@@ -500,11 +500,15 @@ __global__ void __launch_bounds__(256) greedy_kernel(GreedyArgs a) {
 // h > 1: no edges -- every copy represents itself.
 __global__ void identity_rep_kernel(const int32_t* __restrict__ goff, const int32_t* __restrict__ gtok, int E,
                                     int32_t* __restrict__ rep_local, uint32_t* __restrict__ ctrl,
-                                    const int32_t* __restrict__ gcnt, int32_t* __restrict__ gnrep) {
+                                    const int32_t* __restrict__ gcnt, int32_t* __restrict__ gnrep,
+                                    int32_t* __restrict__ mrank, int32_t* __restrict__ mcnt_row) {
   pdl_enter();
   const int rows = goff[E];
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
     rep_local[r] = gtok[r] >= 0 ? (int32_t)r : -1;
+    mrank[r] = 0;     // every copy is the only member of its own list
+    mcnt_row[r] = 1;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) ctrl[2] = 0u;
   if (blockIdx.x == 0)
     for (int e = threadIdx.x; e < E; e += blockDim.x) gnrep[e] = gcnt[e];  // every copy represents itself
@@ -533,9 +537,11 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
 
 int launch_identity_rep(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(identity_rep_kernel, 148, 256, 0, st, L->goff, L->gtok, L->E, L->rep_local, L->ctrl, L->gcnt, L->gnrep);
+  launch_pdl(identity_rep_kernel, 148, 256, 0, st, L->goff, L->gtok, L->E, L->rep_local, L->ctrl, L->gcnt, L->gnrep,
+             L->mrank, L->mcnt_row);
   LUFFY_LAUNCHED();
   L->gnrep_valid = true;
+  L->mrank_valid = true;
   return 0;
 }
 
@@ -562,6 +568,7 @@ int launch_greedy(luffy_layer* L, void* s) {
   // fast path: one thread-block cluster per group with DSMEM replicas (greedy_cluster.cu)
   const int rc = launch_greedy_cluster(L, s);
   L->gnrep_valid = rc == 0;  // the cluster kernel publishes the per-group representative counts
+  L->mrank_valid = rc == 0;  // ... and the member ranks / list lengths
   if (rc >= 0) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(s);
   LUFFY_CUDA_TRY(cudaMemsetAsync(L->ctrl, 0, sizeof(uint32_t) * (64 + kGreedyMaxRounds), st));

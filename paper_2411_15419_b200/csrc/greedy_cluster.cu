@@ -34,7 +34,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       int32_t* __restrict__ rep_local,
                                                                       uint32_t* __restrict__ ctrl, int nmax,
                                                                       int max_rounds, int cache_words, int E,
-                                                                      int32_t* __restrict__ gnrep) {
+                                                                      int32_t* __restrict__ gnrep,
+                                                                      int32_t* __restrict__ mrank,
+                                                                      int32_t* __restrict__ mcnt_row) {
   pdl_enter();
   extern __shared__ __align__(16) uint8_t gsm[];
   __shared__ int order_s[LUFFY_MAX_EXPERTS];
@@ -209,6 +211,36 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     gather_words(win);
     __syncthreads();
     STAMP();
+    // ---- D0: member lists of this slice's winners, for the layout: a winner claims itself and its alive
+    // neighbours (the alive replica still holds the state before this phase's claims), so its members in
+    // token order are the set bits of (row & alive) | self -- each member's rank in that list and the
+    // list's length are written here, which makes the layout's member placement a direct store
+    for (int r = r0 + wid; r < r1; r += nwarp) {
+      if (!((win[r >> 5] >> (r & 31)) & 1u)) continue;
+      const uint32_t* row = ROW(r);
+      int base = 0;
+      for (int w0 = 0; w0 < W; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t m = w < W ? (row[w] & alive[w]) : 0u;
+        if (w == (r >> 5)) m |= 1u << (r & 31);
+        const int cnt = __popc(m);
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
+        }
+        int k = base + inc - cnt;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1u;
+          mrank[g0 + 32 * w + b] = k++;
+        }
+        base += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) mcnt_row[g0 + r] = base;
+    }
+    __syncthreads();  // the alive replica is read above before this CTA's own claims clear its words
     // ---- D: claims (a non-winner has at most one winner neighbour: winners are >= 3 hops apart)
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
@@ -274,7 +306,7 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int n
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
-                                    kGreedyMaxRounds, cache_words, L->E, L->gnrep));
+                                    kGreedyMaxRounds, cache_words, L->E, L->gnrep, L->mrank, L->mcnt_row));
   LUFFY_LAUNCHED();
   return 0;
 }

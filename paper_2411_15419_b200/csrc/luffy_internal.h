@@ -71,6 +71,9 @@ struct luffy_layer {
   int32_t* nrep;      // [E] representatives per expert
   int32_t* gnrep;     // [E] representatives per group, published by representative selection
   bool gnrep_valid;   // set when the selection kernel of this step published gnrep
+  int32_t* mrank;     // [Cpad_max] rank of each row in its representative's member list (token order)
+  int32_t* mcnt_row;  // [Cpad_max] member-list length of each representative row
+  bool mrank_valid;   // set when the selection kernel of this step published mrank / mcnt_row
   int32_t* soff;      // [E+1] padded send offsets
   int32_t* lslot;     // [Cpad_max] slot of a group row that is a representative (-1 otherwise)
   int32_t* perm;      // [Rpad_max] slot -> token (-1 = padding)

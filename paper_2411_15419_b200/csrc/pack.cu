@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ marr,
                                                       int32_t* __restrict__ members, int32_t* __restrict__ mslot,
                                                       int32_t* __restrict__ rep_out,
-                                                      const int32_t* __restrict__ gnrep, int cur_cap) {
+                                                      const int32_t* __restrict__ gnrep, int cur_cap,
+                                                      const int32_t* __restrict__ mrank,
+                                                      const int32_t* __restrict__ mcnt_row) {
   pdl_enter();
   extern __shared__ int cur_smem[];
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
@@ -141,6 +143,53 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
       mslot[g] = -1;
     }
     __syncthreads();
+    if (mrank) {
+      // member ranks and list lengths came from representative selection (greedy_cluster_kernel, phase D0):
+      // slots and list starts are two prefix sums over the group's rows, every member a direct store
+      int* s_mst = s_cnt;  // [n] start of the member list of each representative row (reuses s_cnt/s_cur)
+      int baseR = 0, baseM = g0;
+      for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+        const int c = c0 + threadIdx.x;
+        const bool inr = c < n;
+        const bool isrep = inr && s_rep[c] == c;
+        const int mc = isrep ? mcnt_row[g0 + c] : 0;
+        int totR, totM;
+        const int preR = block_scan_flag2(isrep, warp_sums, totR);
+        const int preM = block_scan_value(mc, warp_sums, totM);
+        if (isrep) {
+          const int ls = baseR + preR;
+          s_ls[c] = ls;
+          s_mst[c] = baseM + preM;
+          lslot[g0 + c] = s0 + ls;
+          perm[s0 + ls] = s_tok[c];
+          slot_gl[s0 + ls] = g0 + c;
+          mstart[s0 + ls] = baseM + preM;
+          mcnt[s0 + ls] = mc;
+          marr[s0 + ls] = 0;
+        } else if (inr) {
+          s_ls[c] = -1;
+          lslot[g0 + c] = -1;
+        }
+        baseR += totR;
+        baseM += totM;
+      }
+      __syncthreads();
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const int t = s_tok[c];
+        const int r = s_rep[c];
+        int jj = 0;
+        for (int j = 0; j < k; ++j)
+          if (idx[(size_t)t * k + j] == e) jj = j;
+        const int ls = s_ls[r];
+        pos[(size_t)t * k + jj] = s0 + ls;
+        rep[(size_t)t * k + jj] = s_tok[r];
+        if (rep_out) rep_out[(size_t)t * k + jj] = s_tok[r];
+        const int p = s_mst[r] + mrank[g0 + c];
+        members[p] = g0 + c;
+        mslot[p] = s0 + ls;
+      }
+      return;
+    }
     int base = 0;
     for (int c0 = 0; c0 < n; c0 += blockDim.x) {
       const int c = c0 + threadIdx.x;
@@ -679,7 +728,8 @@ int launch_pack(luffy_layer* L, const void* x, void* dst_rows, int32_t* rep_out,
   launch_pdl(layout_kernel, L->E, 1024, (size_t)std::max(cur_cap, 1) * 4, st, L->goff, L->gcnt, L->gtok, L->rep_local, L->idx, L->E, L->k, L->nrep,
                                                  L->soff, L->lslot, L->perm, L->slot_gl, L->pos, L->rep, L->mstart,
                                                  L->mcnt, L->mcur, L->marr, L->members, L->mslot, rep_out,
-                                                 L->gnrep_valid ? L->gnrep : nullptr, cur_cap);
+                                                 L->gnrep_valid ? L->gnrep : nullptr, cur_cap,
+                                                 L->mrank_valid ? L->mrank : nullptr, L->mcnt_row);
   LUFFY_LAUNCHED();
 
   if (dst_rows) {

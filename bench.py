@@ -781,10 +781,14 @@ def main():
                 nv = {"tx_bytes_per_step": (c1[0] - c0[0]) / 10, "rx_bytes_per_step": (c1[1] - c0[1]) / 10,
                       "window": "10 steps after the timed region (the counters perturb the exchange)"}
         push = None
-        pk = ktab.get("xpack_push_kernel") if ktab else None
+        pk, pkn = None, None
+        for kn in ("xpack_push_tma_kernel", "xpack_push_kernel"):
+            if ktab and kn in ktab:
+                pk, pkn = ktab[kn], kn
+                break
         if pk:
             gbs = remote_rows * cfg.d_model * B_ / (pk[1] * 1e-6) / 1e9
-            push = {"kernel": "xpack_push_kernel (fused pack + dispatch push)", "remote_bytes": remote_rows * cfg.d_model * B_,
+            push = {"kernel": f"{pkn} (fused pack + dispatch push)", "remote_bytes": remote_rows * cfg.d_model * B_,
                     "us": pk[1], "GBps": gbs, "frac_of_900_nominal": gbs / 900.0, "frac_of_770_measured_peer_copy": gbs / 770.0}
         nvlink = {"algorithmic_bytes_per_step_rank": alg, "nvml_counters_rank": nv, "dispatch_push": push,
                   "step_avg_GBps_rank": alg / (ms_step * 1e-3) / 1e9}

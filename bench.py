@@ -443,6 +443,8 @@ def run_stack(args, cfg):
                           "migration_q": args.migrate if st.migrate else 0, "history_S1_S2": hist,
                           "parallelism": f"ep{world}"},
                "attention": {"fwd_ms_per_step_mean_rank": att_ms, "padding_efficiency": pad_eff,
+                             "eq1_ops_total": float(ops.sum()),
+                             "max_rank_fwd_ms": float(max(sum(t_ for _, _, _, t_ in r_) for r_ in allsamples)),
                              "eq1_fit": {"P_eff_ops_per_s": 1.0 / c * 1e3, "mean_rel_err": float(rel.mean()),
                                          "max_rel_err": float(rel.max()), "samples": len(flat),
                                          "model": "t = (3 B L d^2 + 2 B L^2 d) / P (Eq. 1, P:307), least squares"}},

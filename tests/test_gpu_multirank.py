@@ -20,11 +20,12 @@ def _port():
     return p
 
 
-def _run(n, config, h=0.9, extra=()):
+def _run(n, config, h=0.9, extra=(), env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_gpu_worker.py"),
            "--config", config, "--h", str(h), *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env=dict(os.environ, **(env or {})))
     print(r.stdout[-4000:], r.stderr[-4000:])
     return r
 
@@ -36,6 +37,15 @@ def test_expert_parallel_parity(n, config, h):
     r = _run(n, config, h)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count('"ok": true') == n
+
+
+def test_expert_parallel_parity_warp_push():
+    """The warp-store dispatch push (LUFFY_PUSH_TMA=0) against the same oracle as the default TMA push."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    r = _run(2, "C2S", 0.9, env={"LUFFY_PUSH_TMA": "0"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"ok": true') == 2
 
 
 @pytest.mark.parametrize("n,extra", [(2, ("--residual",)), (4, ("--residual",))])

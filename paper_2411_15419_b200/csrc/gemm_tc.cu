@@ -30,12 +30,11 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 64;  // BM: accumulator rows per CTA (the pair's tile is 256 x 256)
 constexpr int A_BYTES = BM * BK * 2;   // 16 KiB per CTA
 constexpr int EPI_WARPS = 8;
-constexpr int STG_BYTES = 8192;  // per epilogue warp: output staging, two 4 KiB buffers used alternately by the
-                                 // TMA-store epilogue (a chunk's stores drain while the next chunk is staged)
+constexpr int STG_BYTES = 4096;  // per epilogue warp: output staging (coalesced stores)
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 per TMEM lane quarter)
 template <int CG>
 struct Pipe {
-  static constexpr int STAGES = CG == 1 ? 3 : 5;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int B_ROWS = BN / CG;           // N rows of B staged by one CTA
   static constexpr int B_BYTES = B_ROWS * BK * 2;  // 32 KiB single, 16 KiB in the pair
   static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + EPI_WARPS * STG_BYTES + 1024 + 256;
@@ -381,7 +380,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int hc = (warp - 2) >> 2;  // column half handled by this warp
     const int rt = 32 * q + lane;
     uint8_t* stg = sStg + (warp - 2) * STG_BYTES;  // [0, 2K) and [2K, 4K): two bf16 blocks or one fp32 block
-    uint32_t cbuf = 0;  // TMA-store chunks issued by this warp: buffer (cbuf & 1) of stg
     int acc = 0;
     uint32_t aphase = 0;
     // aux (pre-activation) blocks of the backward epilogues are prefetched one 32-column chunk ahead with
@@ -477,11 +475,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else {
 #pragma unroll 1
           for (int c0 = hc * (BN / 2); c0 < (hc + 1) * (BN / 2); c0 += 32) {
-            uint8_t* buf = tma_out ? stg + (cbuf & 1u) * 4096 : stg;  // this chunk's staging buffer
             float pa[NB > 0 ? NB : 1][32];
 #pragma unroll
             for (int b = 0; b < NB; ++b) {  // prefetched aux block -> own row through shared memory
-              uint8_t* ab = buf + 2048;  // (never read by a TMA store in the DGeLU epilogue)
+              uint8_t* ab = stg + 2048;
 #pragma unroll
               for (int it = 0; it < 4; ++it) {
                 const int r = it * 8 + (lane >> 2), c = lane & 3;
@@ -529,20 +526,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                   v[i + 1] = p.y;
                 }
               }
-              // this buffer was last used two chunks ago: only the previous chunk's stores (1 or 2 bulk groups)
-              // may still be reading the other buffer
-              if (lane == 0) tc::bulk_wait_read_n<EPI == EPI_GELU ? 2 : 1>();
+              if (lane == 0) tc::bulk_wait_read();  // the previous chunk's stores have read the buffers
               __syncwarp();
-              stage_rows_bf16(buf, EPI == EPI_GELU ? o : v);
-              if (EPI == EPI_GELU) stage_rows_bf16(buf + 2048, v);
+              stage_rows_bf16(stg, EPI == EPI_GELU ? o : v);
+              if (EPI == EPI_GELU) stage_rows_bf16(stg + 2048, v);
               tc::fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
                 const int row0 = x.m0 + hm + 32 * q;
-                tc::tma_store_2d(&tD, buf, n, row0);
-                if (EPI == EPI_GELU) tc::tma_store_2d(&tD3, buf + 2048, n, row0);
+                tc::tma_store_2d(&tD, stg, n, row0);
+                if (EPI == EPI_GELU) tc::tma_store_2d(&tD3, stg + 2048, n, row0);
               }
-              ++cbuf;
             } else if (EPI == EPI_STORE) {
               if (a.has_rd) {  // fused exchange: the row goes straight to its rank's buffer over NVLink
                 if (a.rd.mask) {  // combine: every destination rank of the row (sequence migration)

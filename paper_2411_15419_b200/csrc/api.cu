@@ -228,6 +228,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
     o->x_peer_res = cv.take<void*>(m.P);
   }
   o->dl = cv.take<float>((size_t)m.Tmax * m.E);
+  o->rpart = cv.take<float>((size_t)((m.d + 1023) / 1024) * m.Tmax * m.E);
   o->wg_part = cv.take<float>((size_t)std::max(wg_parts(m.E, m.d), (m.Tmax + 31) / 32) * m.E * m.d);
 }
 

@@ -92,6 +92,7 @@ struct luffy_layer {
   void* send;         // [Rpad_max, d] send buffer (world > 1); reused as d_send in backward
   // ---- backward scratch
   float* dl;          // [Tmax, E] gate logit gradients
+  float* rpart;       // [ceil(d / 1024), Tmax, E] split partial logits of the register-W_g gate (8 < E <= 32)
   float* wg_part;     // [kWgParts, E, d]
   const float* wg_route;  // w_gate of this step's luffy_route (the stats' near-tie report reads it)
   uint64_t* stat64;   // [4] device stats of the last condense: [0] near-threshold pairs, [1] near-tie tokens

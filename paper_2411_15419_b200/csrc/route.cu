@@ -312,6 +312,163 @@ __global__ void __launch_bounds__(256, 2) route_e8_kernel(const T* __restrict__ 
   }
 }
 
+// Gate for 8 < E <= 32 with W_g held in REGISTERS: warp w of a CTA owns 128 columns (4 per lane) of a
+// 1024-column split of d and keeps those columns of all EB experts of W_g in registers (4 x EB floats), so
+// a token costs one 8-byte load per lane, 4 x EB FMAs (packed over expert pairs) and a transpose-reduce
+// (lane e ends with expert e's sum over the warp's 128 columns) -- no shared-memory traffic per FMA.  Warp
+// partials of a batch of 8 tokens meet in shared memory and are summed in warp order; with one split the
+// CTA finishes softmax / top-k itself (one warp per token, lane = expert), otherwise the split partials go
+// to `part` and route_finish_kernel sums them in split order.  Summation order is fixed (4-column chain in
+// a lane, the butterfly, warps, splits): reproducible.
+constexpr int RW_SPLIT = 1024;  // columns per split (8 warps x 128)
+constexpr int RW_NB = 8;        // tokens per shared-memory batch
+
+__device__ __forceinline__ void gate_finish(float logit, bool valid_e, int e, int t, int T_, int E, int k, int renorm,
+                                            float* __restrict__ probs, int32_t* __restrict__ idx, float* __restrict__ w,
+                                            int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
+  // one warp per token, lane e = expert (e < E valid): softmax over E, top-k by (logit desc, id asc), gate weights
+  const float lg = valid_e ? logit : -INFINITY;
+  float mx = lg;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float ex = valid_e ? expf(lg - mx) : 0.f;
+  float se = ex;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  if (t < T_ && valid_e) probs[(size_t)t * E + e] = ex / se;
+  bool taken = !valid_e;
+  float selv[8];
+  int seli[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= k) break;
+    float bv = taken ? -INFINITY : lg;
+    int bi = taken ? 0x7fffffff : e;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    taken = taken || bi == e;
+    selv[j] = bv;
+    seli[j] = bi;
+  }
+  float ev[8], sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < k) {
+      ev[j] = renorm ? expf(selv[j] - selv[0]) : expf(selv[j] - mx) / se;
+      sum += ev[j];
+    }
+  float myw = 0.f;
+  int myi = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < k && j == e) {
+      myw = renorm ? ev[j] / sum : ev[j];
+      myi = seli[j];
+    }
+  if (t < T_ && e < k) {
+    w[(size_t)t * k + e] = myw;
+    w_out[(size_t)t * k + e] = myw;
+    idx[(size_t)t * k + e] = myi;
+    idx_out[(size_t)t * k + e] = myi;
+  }
+}
+
+template <typename T, int EB>
+__global__ void __launch_bounds__(256, 1) route_wreg_kernel(const T* __restrict__ x, const float* __restrict__ wg, int T_,
+                                                            int E, int d, int k, int renorm, int tpc,
+                                                            float* __restrict__ part, float* __restrict__ probs,
+                                                            int32_t* __restrict__ idx, float* __restrict__ w,
+                                                            int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
+  pdl_enter();
+  using R = decltype(ld4raw(static_cast<const T*>(nullptr)));
+  __shared__ float red[RW_NB][8][EB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int split = blockIdx.y, nsplit = gridDim.y;
+  const int c = split * RW_SPLIT + wid * 128 + lane * 4;
+  const bool active = c < d;
+  float wr[EB][4];
+#pragma unroll
+  for (int e = 0; e < EB; ++e) {
+    const float4 q = (e < E && active) ? *reinterpret_cast<const float4*>(wg + (size_t)e * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    wr[e][0] = q.x; wr[e][1] = q.y; wr[e][2] = q.z; wr[e][3] = q.w;
+  }
+  const int tg0 = blockIdx.x * tpc, tg1 = min(T_, tg0 + tpc);
+  for (int tb = tg0; tb < tg1; tb += RW_NB) {
+    R raw[RW_NB];
+#pragma unroll
+    for (int b = 0; b < RW_NB; ++b) raw[b] = (active && tb + b < tg1) ? ld4raw(x + (size_t)(tb + b) * d + c) : R{};
+#pragma unroll
+    for (int b = 0; b < RW_NB; ++b) {
+      float xv[4];
+      cvt4(raw[b], xv);
+      float v[EB];
+#pragma unroll
+      for (int p = 0; p < EB / 2; ++p) {  // packed over expert pairs; each logit keeps its own column chain
+        float2 s2 = __fmul2_rn(make_float2(xv[0], xv[0]), make_float2(wr[2 * p][0], wr[2 * p + 1][0]));
+        s2 = __ffma2_rn(make_float2(xv[1], xv[1]), make_float2(wr[2 * p][1], wr[2 * p + 1][1]), s2);
+        s2 = __ffma2_rn(make_float2(xv[2], xv[2]), make_float2(wr[2 * p][2], wr[2 * p + 1][2]), s2);
+        s2 = __ffma2_rn(make_float2(xv[3], xv[3]), make_float2(wr[2 * p][3], wr[2 * p + 1][3]), s2);
+        v[2 * p] = s2.x;
+        v[2 * p + 1] = s2.y;
+      }
+      // lanes l and l + 32 - ... : butterfly over the offsets >= EB, then the transpose-reduce over offsets < EB
+#pragma unroll
+      for (int o = 16; o >= EB; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < EB; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+#pragma unroll
+      for (int o = EB / 2; o >= 1; o >>= 1) {
+        const bool hi = lane & o;
+#pragma unroll
+        for (int j = 0; j < o; ++j) {
+          const float send = hi ? v[j] : v[j + o];
+          const float keep = hi ? v[j + o] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (lane < EB) red[b][wid][lane] = v[0];  // lane e: expert e's sum over this warp's columns
+    }
+    __syncthreads();
+    // warp b finishes token tb + b: lane e sums the 8 warps' partials in warp order
+    {
+      const int b = wid, e = lane;
+      float s = 0.f;
+      if (e < EB)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += red[b][q][e];
+      const int t = tb + b;
+      if (nsplit == 1) {
+        gate_finish(s, e < E, e, t, tg1, E, k, renorm, probs, idx, w, idx_out, w_out);
+      } else if (t < tg1 && e < E) {
+        part[((size_t)split * T_ + t) * E + e] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Sum of the split partials in split order, then softmax / top-k (one warp per token, lane = expert).
+__global__ void __launch_bounds__(256) route_finish_kernel(const float* __restrict__ part, int nsplit, int T_, int E, int k,
+                                                           int renorm, float* __restrict__ probs, int32_t* __restrict__ idx,
+                                                           float* __restrict__ w, int32_t* __restrict__ idx_out,
+                                                           float* __restrict__ w_out) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += (gridDim.x * blockDim.x) >> 5) {
+    float s = 0.f;
+    if (lane < E)
+      for (int q = 0; q < nsplit; ++q) s += part[((size_t)q * T_ + t) * E + lane];
+    gate_finish(s, lane < E, lane, t, T_, E, k, renorm, probs, idx, w, idx_out, w_out);
+  }
+}
+
 // Fast gate for E <= 32: a CTA of 8 warps owns 32 tokens (4 per warp); W_g is staged through shared
 // memory in chunks of RC columns and every weight read from shared memory feeds 4 tokens.  Lane l owns
 // columns {4l..4l+3} and {128+4l..128+4l+3} of each 256-wide sub-chunk (conflict-free float4 reads).
@@ -787,13 +944,26 @@ int route_dispatch(const luffy_layer* L, const void* x, const float* wg, int32_t
       LUFFY_CUDA_TRY(smem_optin((const void*)route_e8_kernel<T>, 65536));
       launch_pdl(route_e8_kernel<T>, fb, 256, 65536, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
                  idx_out, w_out);
-    } else if (L->E <= 16)
-      launch_pdl(route_fast_kernel<T, 16>, fb, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
-                                                   idx_out, w_out);
-    else
-      launch_pdl(route_fast_kernel<T, 32>, fb, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, L->probs, L->idx, L->w,
-                                                   idx_out, w_out);
-    LUFFY_LAUNCHED();
+      LUFFY_LAUNCHED();
+    } else {
+      // W_g in registers (route_wreg_kernel): ~148 CTAs over the token ranges of every column split
+      const int nsplit = (L->d + RW_SPLIT - 1) / RW_SPLIT;
+      int tpc = (int)(((int64_t)L->T * nsplit + device_sms() - 1) / device_sms());
+      tpc = std::max(RW_NB, (tpc + RW_NB - 1) / RW_NB * RW_NB);
+      const dim3 grid((L->T + tpc - 1) / tpc, nsplit);
+      if (L->E <= 16)
+        launch_pdl(route_wreg_kernel<T, 16>, grid, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, tpc, L->rpart,
+                   L->probs, L->idx, L->w, idx_out, w_out);
+      else
+        launch_pdl(route_wreg_kernel<T, 32>, grid, 256, 0, s, xp, wg, L->T, L->E, L->d, L->k, L->renorm, tpc, L->rpart,
+                   L->probs, L->idx, L->w, idx_out, w_out);
+      LUFFY_LAUNCHED();
+      if (nsplit > 1) {
+        launch_pdl(route_finish_kernel, std::max(1, std::min((L->T + 7) / 8, 148 * 8)), 256, 0, s, (const float*)L->rpart,
+                   nsplit, L->T, L->E, L->k, L->renorm, L->probs, L->idx, L->w, idx_out, w_out);
+        LUFFY_LAUNCHED();
+      }
+    }
     return 0;
   }
 #define LUFFY_ROUTE(EBV)                                                                                 \

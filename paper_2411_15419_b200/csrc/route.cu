@@ -911,6 +911,93 @@ __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict
 
 // dW_g = sum of the partials in a fixed order: CTA = 32 outputs x 8 warps; warp w sums parts w, w+8, ...
 // (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+// Gate backward for 8 < E <= 32 in ONE pass over x: warp w of a CTA owns 64 columns (2 per lane) of a
+// 512-column split and keeps those columns of W_g (for dx += dl W_g) and its partial dW_g = sum_t dl[t] x[t]
+// over the CTA's token range in registers; dl of a batch of 8 tokens is formed once (warp = token, lane =
+// expert) and broadcast through shared memory.  The partials go to wg_part[CTA][e][c] and wg_reduce_kernel
+// sums them in CTA order.  Per element the order is fixed: reproducible.
+template <typename T, int EB>
+__global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
+                                                                const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                                                const float* __restrict__ dw, const T* __restrict__ x,
+                                                                int T_, int E, int d, int k, int renorm, int tpc,
+                                                                T* __restrict__ dx, float* __restrict__ wg_part) {
+  pdl_enter();
+  __shared__ __align__(16) float dls[RW_NB][EB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = blockIdx.y * 512 + wid * 64 + lane * 2;
+  const bool active = c < d;
+  float wr[EB][2], ga[EB][2];
+#pragma unroll
+  for (int e = 0; e < EB; ++e) {
+    const float2 q = (e < E && active) ? *reinterpret_cast<const float2*>(wg + (size_t)e * d + c) : make_float2(0.f, 0.f);
+    wr[e][0] = q.x;
+    wr[e][1] = q.y;
+    ga[e][0] = ga[e][1] = 0.f;
+  }
+  const int tg0 = blockIdx.x * tpc, tg1 = min(T_, tg0 + tpc);
+  for (int tb = tg0; tb < tg1; tb += RW_NB) {
+    {  // dl of the batch: warp b -> token tb + b, lane e (renormalised top-k or raw softmax, R1 / R11)
+      const int t = tb + wid, e = lane;
+      float v = 0.f;
+      if (t < tg1 && e < E) {
+        float s = 0.f, g = 0.f, wsel = 0.f;
+        bool sel = false;
+        for (int j = 0; j < k; ++j) {
+          const int ej = idx[(size_t)t * k + j];
+          const float dwj = dw[(size_t)t * k + j];
+          s += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
+          if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
+        }
+        v = renorm ? (sel ? wsel * (g - s) : 0.f) : probs[(size_t)t * E + e] * (g - s);
+      }
+      if (e < EB) dls[wid][e] = v;
+    }
+    __syncthreads();
+    const int nb = min(RW_NB, tg1 - tb);
+    for (int b = 0; b < nb; ++b) {
+      const int t = tb + b;
+      float x0 = 0.f, x1 = 0.f, d0 = 0.f, d1 = 0.f;
+      if (active) {
+        if constexpr (sizeof(T) == 2) {
+          const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)t * d + c));
+          const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dx + (size_t)t * d + c));
+          x0 = xf.x; x1 = xf.y; d0 = df.x; d1 = df.y;
+        } else {
+          const float2 xf = *reinterpret_cast<const float2*>(x + (size_t)t * d + c);
+          const float2 df = *reinterpret_cast<const float2*>(dx + (size_t)t * d + c);
+          x0 = xf.x; x1 = xf.y; d0 = df.x; d1 = df.y;
+        }
+      }
+      float2 acc = make_float2(d0, d1);
+#pragma unroll
+      for (int e4 = 0; e4 < EB; e4 += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(&dls[b][e4]);
+        const float dv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e4 + u;
+          acc = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(wr[e][0], wr[e][1]), acc);
+          const float2 g2 = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(x0, x1), make_float2(ga[e][0], ga[e][1]));
+          ga[e][0] = g2.x;
+          ga[e][1] = g2.y;
+        }
+      }
+      if (active) {
+        if constexpr (sizeof(T) == 2)
+          *reinterpret_cast<__nv_bfloat162*>(dx + (size_t)t * d + c) = __floats2bfloat162_rn(acc.x, acc.y);
+        else
+          *reinterpret_cast<float2*>(dx + (size_t)t * d + c) = acc;
+      }
+    }
+    __syncthreads();
+  }
+  if (active)
+#pragma unroll
+    for (int e = 0; e < EB; ++e)
+      if (e < E) *reinterpret_cast<float2*>(wg_part + ((size_t)blockIdx.x * E + e) * d + c) = make_float2(ga[e][0], ga[e][1]);
+}
+
 __global__ void __launch_bounds__(256) wg_reduce_kernel(const float* __restrict__ part, int parts, int n,
                                                         float* __restrict__ out) {
   pdl_enter();
@@ -1065,6 +1152,34 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
       launch_pdl(route_bwd_fused8_kernel<float>, parts, 256, 0, st, wg, L->probs, L->idx, L->w, dw,
                  static_cast<const float*>(x), L->T, L->E, L->d, L->k, L->renorm, L->dl, static_cast<float*>(dx), L->wg_part);
     LUFFY_LAUNCHED();
+    const int n = L->E * L->d;
+    launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
+    LUFFY_LAUNCHED();
+    return 0;
+  }
+  if (L->E > 8 && L->E <= 32 && L->d % 2 == 0) {  // one pass, W_g and the dW_g partials in registers
+    const int nsplit = (L->d + 511) / 512;
+    const int cap_parts = std::max(wg_parts(L->E, L->d), (L->Tmax + 31) / 32);  // wg_part capacity (workspace)
+    int tpc = (int)(((int64_t)L->T * nsplit + device_sms() - 1) / device_sms());
+    tpc = std::max(tpc, (L->T + cap_parts - 1) / cap_parts);
+    tpc = std::max(RW_NB, (tpc + RW_NB - 1) / RW_NB * RW_NB);
+    const int parts = (L->T + tpc - 1) / tpc;
+    const dim3 grid(parts, nsplit);
+#define LUFFY_RBW(EBV)                                                                                              \
+    do {                                                                                                            \
+      if (L->dtype == LUFFY_BF16)                                                                                   \
+        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, 0, st, wg, L->probs, L->idx, L->w, dw,            \
+                   static_cast<const bf16*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<bf16*>(dx),   \
+                   L->wg_part);                                                                                     \
+      else                                                                                                          \
+        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, 0, st, wg, L->probs, L->idx, L->w, dw,           \
+                   static_cast<const float*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<float*>(dx), \
+                   L->wg_part);                                                                                     \
+      LUFFY_LAUNCHED();                                                                                             \
+    } while (0)
+    if (L->E <= 16) LUFFY_RBW(16);
+    else LUFFY_RBW(32);
+#undef LUFFY_RBW
     const int n = L->E * L->d;
     launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
     LUFFY_LAUNCHED();

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32) xpack_push_tma_kernel(const T* __restrict_
   __syncwarp();
   if (lane == 0) {
     const int64_t rows = soff_s[E];
-    uint32_t phase = 0;
+    uint32_t phase = 0;  // bit j: parity of stage j's next completion (a stage skipped for padding keeps it)
     for (int64_t b0 = blockIdx.x; b0 < rows; b0 += (int64_t)gridDim.x * stages) {
       tc::bulk_wait_read();  // the previous batch's stores have read the ring
       int tj[32];
@@ -165,11 +165,11 @@ __global__ void __launch_bounds__(32) xpack_push_tma_kernel(const T* __restrict_
         const int p = e / El;
         const int64_t drow = (int64_t)base_s[e] + (s - soff_s[e]);
         peer_rowmask[p][drow] = dmask ? dmask[s] : (1ull << me);
-        tc::mbar_wait(&bar[j], phase);
+        tc::mbar_wait(&bar[j], (phase >> j) & 1u);
+        phase ^= 1u << j;
         tc::bulk_store(static_cast<T*>(peer_recv[p]) + drow * d, ring + (size_t)j * rb, rb);
         tc::bulk_commit();
       }
-      phase ^= 1u;
     }
     tc::bulk_wait_all();                                   // the rows have been written ...
     asm volatile("fence.proxy.async.global;" ::: "memory");  // ... and are ordered before the release below

@@ -50,6 +50,8 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     if args.config == "C2S":
         cfg = dataclasses.replace(workload.CONFIGS["C2"], seqs_per_rank=2)
+    elif args.config == "C2":
+        cfg = workload.CONFIGS["C2"]          # the benched size: T = 8192 per rank
     elif args.config == "C1":
         cfg = workload.CONFIGS["C1"]          # fp32 (SIMT path) through NCCL
     else:

@@ -30,7 +30,8 @@ def _run(n, config, h=0.9, extra=(), env=None):
     return r
 
 
-@pytest.mark.parametrize("n,config,h", [(2, "C2S", 0.9), (2, "C2S", 1.01), (2, "C1", 0.9), (4, "C2S", 0.9)])
+@pytest.mark.parametrize("n,config,h", [(2, "C2S", 0.9), (2, "C2S", 1.01), (2, "C1", 0.9), (4, "C2S", 0.9),
+                                        (2, "C2", 0.9)])
 def test_expert_parallel_parity(n, config, h):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")

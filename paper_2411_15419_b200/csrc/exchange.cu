@@ -221,11 +221,13 @@ int launch_xdispatch(luffy_layer* L, const void* x, void* s) {
                                          L->x_rank_of, L->x_slot_of, static_cast<bf16*>(L->x_recv[par]),
                                          static_cast<bf16*>(L->x_dexp), L->dtype == LUFFY_BF16 ? 2 : 4, L->x_rowmask);
   LUFFY_LAUNCHED();
+  // LUFFY_PUSH_TMA=1 selects the bulk-copy push.  Measured at C2, N=2 (CUPTI, warm): 36.1 us (240 GB/s over
+  // NVLink) against 23.7 us (365 GB/s) for the warp-store push, which therefore stays the default.
   static const bool tma_push = [] {
     const char* v = std::getenv("LUFFY_PUSH_TMA");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
-  if (tma_push) {  // bulk-copy push (default); LUFFY_PUSH_TMA=0 selects the warp-store push (A/B)
+  if (tma_push) {
     const size_t rb = (size_t)L->d * (L->dtype == LUFFY_BF16 ? 2 : 4);
     const int stages = (int)std::max<size_t>(2, std::min<size_t>(16, (96 * 1024) / rb));
     const int smem = (int)(stages * rb);

@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __r
                                                                 int T_, int E, int d, int k, int renorm, int tpc,
                                                                 T* __restrict__ dx, float* __restrict__ wg_part) {
   pdl_enter();
-  __shared__ __align__(16) float dls[RW_NB][EB];
+  extern __shared__ __align__(16) float dlsm[];  // [tpc][EB]: dl of the CTA's tokens
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int c = blockIdx.y * 512 + wid * 64 + lane * 2;
   const bool active = c < d;
@@ -936,53 +936,62 @@ __global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __r
     ga[e][0] = ga[e][1] = 0.f;
   }
   const int tg0 = blockIdx.x * tpc, tg1 = min(T_, tg0 + tpc);
-  for (int tb = tg0; tb < tg1; tb += RW_NB) {
-    {  // dl of the batch: warp b -> token tb + b, lane e (renormalised top-k or raw softmax, R1 / R11)
-      const int t = tb + wid, e = lane;
-      float v = 0.f;
-      if (t < tg1 && e < E) {
-        float s = 0.f, g = 0.f, wsel = 0.f;
-        bool sel = false;
-        for (int j = 0; j < k; ++j) {
-          const int ej = idx[(size_t)t * k + j];
-          const float dwj = dw[(size_t)t * k + j];
-          s += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
-          if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
-        }
-        v = renorm ? (sel ? wsel * (g - s) : 0.f) : probs[(size_t)t * E + e] * (g - s);
+  // dl of every token of the range first (renormalised top-k or raw softmax, R1 / R11), one thread per
+  // (token, expert), into shared memory: the token loop below then runs without barriers
+  for (int i = threadIdx.x; i < (tg1 - tg0) * EB; i += blockDim.x) {
+    const int tl = i / EB, e = i % EB, t = tg0 + tl;
+    float v = 0.f;
+    if (e < E) {
+      float s = 0.f, g = 0.f, wsel = 0.f;
+      bool sel = false;
+      for (int j = 0; j < k; ++j) {
+        const int ej = idx[(size_t)t * k + j];
+        const float dwj = dw[(size_t)t * k + j];
+        s += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
+        if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
       }
-      if (e < EB) dls[wid][e] = v;
+      v = renorm ? (sel ? wsel * (g - s) : 0.f) : probs[(size_t)t * E + e] * (g - s);
     }
-    __syncthreads();
+    dlsm[i] = v;
+  }
+  __syncthreads();
+  for (int tb = tg0; tb < tg1; tb += RW_NB) {
     const int nb = min(RW_NB, tg1 - tb);
-    for (int b = 0; b < nb; ++b) {
-      const int t = tb + b;
-      float x0 = 0.f, x1 = 0.f, d0 = 0.f, d1 = 0.f;
-      if (active) {
+    float2 xb[RW_NB], db[RW_NB];  // the batch's x and dx (all loads in flight before the arithmetic)
+#pragma unroll
+    for (int b = 0; b < RW_NB; ++b) {
+      xb[b] = db[b] = make_float2(0.f, 0.f);
+      if (active && b < nb) {
+        const int t = tb + b;
         if constexpr (sizeof(T) == 2) {
-          const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)t * d + c));
-          const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dx + (size_t)t * d + c));
-          x0 = xf.x; x1 = xf.y; d0 = df.x; d1 = df.y;
+          xb[b] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)t * d + c));
+          db[b] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dx + (size_t)t * d + c));
         } else {
-          const float2 xf = *reinterpret_cast<const float2*>(x + (size_t)t * d + c);
-          const float2 df = *reinterpret_cast<const float2*>(dx + (size_t)t * d + c);
-          x0 = xf.x; x1 = xf.y; d0 = df.x; d1 = df.y;
+          xb[b] = *reinterpret_cast<const float2*>(x + (size_t)t * d + c);
+          db[b] = *reinterpret_cast<const float2*>(dx + (size_t)t * d + c);
         }
       }
-      float2 acc = make_float2(d0, d1);
+    }
+#pragma unroll
+    for (int b = 0; b < RW_NB; ++b) {
+      if (b >= nb) break;
+      const int t = tb + b;
+      // dx += dl W_g over four interleaved partial chains (experts e = 4i + u), summed in a fixed order
+      float2 a4[4] = {db[b], make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int e4 = 0; e4 < EB; e4 += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(&dls[b][e4]);
+        const float4 q = *reinterpret_cast<const float4*>(&dlsm[(tb - tg0 + b) * EB + e4]);
         const float dv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int e = e4 + u;
-          acc = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(wr[e][0], wr[e][1]), acc);
-          const float2 g2 = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(x0, x1), make_float2(ga[e][0], ga[e][1]));
+          a4[u] = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(wr[e][0], wr[e][1]), a4[u]);
+          const float2 g2 = __ffma2_rn(make_float2(dv[u], dv[u]), xb[b], make_float2(ga[e][0], ga[e][1]));
           ga[e][0] = g2.x;
           ga[e][1] = g2.y;
         }
       }
+      const float2 acc = make_float2((a4[0].x + a4[1].x) + (a4[2].x + a4[3].x), (a4[0].y + a4[1].y) + (a4[2].y + a4[3].y));
       if (active) {
         if constexpr (sizeof(T) == 2)
           *reinterpret_cast<__nv_bfloat162*>(dx + (size_t)t * d + c) = __floats2bfloat162_rn(acc.x, acc.y);
@@ -990,7 +999,6 @@ __global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __r
           *reinterpret_cast<float2*>(dx + (size_t)t * d + c) = acc;
       }
     }
-    __syncthreads();
   }
   if (active)
 #pragma unroll
@@ -1163,16 +1171,17 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
     int tpc = (int)(((int64_t)L->T * nsplit + device_sms() - 1) / device_sms());
     tpc = std::max(tpc, (L->T + cap_parts - 1) / cap_parts);
     tpc = std::max(RW_NB, (tpc + RW_NB - 1) / RW_NB * RW_NB);
+    tpc = std::min(tpc, 256);  // the dl block of the range lives in shared memory (tpc x EB floats)
     const int parts = (L->T + tpc - 1) / tpc;
     const dim3 grid(parts, nsplit);
 #define LUFFY_RBW(EBV)                                                                                              \
     do {                                                                                                            \
       if (L->dtype == LUFFY_BF16)                                                                                   \
-        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, 0, st, wg, L->probs, L->idx, L->w, dw,            \
+        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, L->probs, L->idx, L->w, dw,            \
                    static_cast<const bf16*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<bf16*>(dx),   \
                    L->wg_part);                                                                                     \
       else                                                                                                          \
-        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, 0, st, wg, L->probs, L->idx, L->w, dw,           \
+        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, L->probs, L->idx, L->w, dw,           \
                    static_cast<const float*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<float*>(dx), \
                    L->wg_part);                                                                                     \
       LUFFY_LAUNCHED();                                                                                             \

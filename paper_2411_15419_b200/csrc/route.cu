@@ -911,17 +911,42 @@ __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict
 
 // dW_g = sum of the partials in a fixed order: CTA = 32 outputs x 8 warps; warp w sums parts w, w+8, ...
 // (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
+// dl [T, E] of the gate backward (renormalised top-k or raw softmax, R1 / R11): one warp per token, lane =
+// expert; the token's k (index, weight, dw) are read once by lanes < k and broadcast.
+__global__ void __launch_bounds__(256) gate_dl_kernel(const float* __restrict__ probs, const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ w, const float* __restrict__ dw, int T_,
+                                                      int E, int k, int renorm, float* __restrict__ dl) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += (gridDim.x * blockDim.x) >> 5) {
+    const int myi = lane < k ? idx[(size_t)t * k + lane] : -1;
+    const float myw = lane < k ? w[(size_t)t * k + lane] : 0.f;
+    const float mydw = lane < k ? dw[(size_t)t * k + lane] : 0.f;
+    const float p = lane < E ? probs[(size_t)t * E + lane] : 0.f;
+    float s = 0.f, g = 0.f, wsel = 0.f;
+    bool sel = false;
+    for (int j = 0; j < k; ++j) {  // same order as the scalar kernels: j ascending
+      const int ej = __shfl_sync(0xffffffffu, myi, j);
+      const float dwj = __shfl_sync(0xffffffffu, mydw, j);
+      const float wj = __shfl_sync(0xffffffffu, myw, j);
+      const float pj = __shfl_sync(0xffffffffu, p, ej & 31);
+      s += (renorm ? wj : pj) * dwj;
+      if (ej == lane) { g = dwj; wsel = wj; sel = true; }
+    }
+    if (lane < E) dl[(size_t)t * E + lane] = renorm ? (sel ? wsel * (g - s) : 0.f) : p * (g - s);
+  }
+}
+
 // Gate backward for 8 < E <= 32 in ONE pass over x: warp w of a CTA owns 64 columns (2 per lane) of a
 // 512-column split and keeps those columns of W_g (for dx += dl W_g) and its partial dW_g = sum_t dl[t] x[t]
 // over the CTA's token range in registers; dl of a batch of 8 tokens is formed once (warp = token, lane =
 // expert) and broadcast through shared memory.  The partials go to wg_part[CTA][e][c] and wg_reduce_kernel
 // sums them in CTA order.  Per element the order is fixed: reproducible.
 template <typename T, int EB>
-__global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __restrict__ wg, const float* __restrict__ probs,
-                                                                const int32_t* __restrict__ idx, const float* __restrict__ w,
-                                                                const float* __restrict__ dw, const T* __restrict__ x,
-                                                                int T_, int E, int d, int k, int renorm, int tpc,
-                                                                T* __restrict__ dx, float* __restrict__ wg_part) {
+__global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __restrict__ wg, const float* __restrict__ dl,
+                                                                const T* __restrict__ x,
+                                                                int T_, int E, int d, int tpc, T* __restrict__ dx,
+                                                                float* __restrict__ wg_part) {
   pdl_enter();
   extern __shared__ __align__(16) float dlsm[];  // [tpc][EB]: dl of the CTA's tokens
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -936,23 +961,11 @@ __global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __r
     ga[e][0] = ga[e][1] = 0.f;
   }
   const int tg0 = blockIdx.x * tpc, tg1 = min(T_, tg0 + tpc);
-  // dl of every token of the range first (renormalised top-k or raw softmax, R1 / R11), one thread per
-  // (token, expert), into shared memory: the token loop below then runs without barriers
+  // dl of the token range (gate_dl_kernel) staged in shared memory with coalesced loads: the token loop below
+  // then runs without barriers
   for (int i = threadIdx.x; i < (tg1 - tg0) * EB; i += blockDim.x) {
-    const int tl = i / EB, e = i % EB, t = tg0 + tl;
-    float v = 0.f;
-    if (e < E) {
-      float s = 0.f, g = 0.f, wsel = 0.f;
-      bool sel = false;
-      for (int j = 0; j < k; ++j) {
-        const int ej = idx[(size_t)t * k + j];
-        const float dwj = dw[(size_t)t * k + j];
-        s += (renorm ? w[(size_t)t * k + j] : probs[(size_t)t * E + ej]) * dwj;
-        if (ej == e) { g = dwj; wsel = w[(size_t)t * k + j]; sel = true; }
-      }
-      v = renorm ? (sel ? wsel * (g - s) : 0.f) : probs[(size_t)t * E + e] * (g - s);
-    }
-    dlsm[i] = v;
+    const int tl = i / EB, e = i % EB;
+    dlsm[i] = e < E ? __ldg(dl + (size_t)(tg0 + tl) * E + e) : 0.f;
   }
   __syncthreads();
   for (int tb = tg0; tb < tg1; tb += RW_NB) {
@@ -1174,16 +1187,17 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
     tpc = std::min(tpc, 256);  // the dl block of the range lives in shared memory (tpc x EB floats)
     const int parts = (L->T + tpc - 1) / tpc;
     const dim3 grid(parts, nsplit);
+    launch_pdl(gate_dl_kernel, std::max(1, std::min((L->T + 7) / 8, 148 * 8)), 256, 0, st, (const float*)L->probs,
+               (const int32_t*)L->idx, (const float*)L->w, dw, L->T, L->E, L->k, L->renorm, L->dl);
+    LUFFY_LAUNCHED();
 #define LUFFY_RBW(EBV)                                                                                              \
     do {                                                                                                            \
       if (L->dtype == LUFFY_BF16)                                                                                   \
-        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, L->probs, L->idx, L->w, dw,            \
-                   static_cast<const bf16*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<bf16*>(dx),   \
-                   L->wg_part);                                                                                     \
+        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, (const float*)L->dl, \
+                   static_cast<const bf16*>(x), L->T, L->E, L->d, tpc, static_cast<bf16*>(dx), L->wg_part);        \
       else                                                                                                          \
-        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, L->probs, L->idx, L->w, dw,           \
-                   static_cast<const float*>(x), L->T, L->E, L->d, L->k, L->renorm, tpc, static_cast<float*>(dx), \
-                   L->wg_part);                                                                                     \
+        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, (const float*)L->dl, \
+                   static_cast<const float*>(x), L->T, L->E, L->d, tpc, static_cast<float*>(dx), L->wg_part);      \
       LUFFY_LAUNCHED();                                                                                             \
     } while (0)
     if (L->E <= 16) LUFFY_RBW(16);

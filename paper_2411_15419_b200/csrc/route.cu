@@ -911,114 +911,6 @@ __global__ void __launch_bounds__(256) wg_partial_kernel(const float* __restrict
 
 // dW_g = sum of the partials in a fixed order: CTA = 32 outputs x 8 warps; warp w sums parts w, w+8, ...
 // (coalesced 128-byte rows), then the 8 warp sums are added in warp order.
-// dl [T, E] of the gate backward (renormalised top-k or raw softmax, R1 / R11): one warp per token, lane =
-// expert; the token's k (index, weight, dw) are read once by lanes < k and broadcast.
-__global__ void __launch_bounds__(256) gate_dl_kernel(const float* __restrict__ probs, const int32_t* __restrict__ idx,
-                                                      const float* __restrict__ w, const float* __restrict__ dw, int T_,
-                                                      int E, int k, int renorm, float* __restrict__ dl) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T_; t += (gridDim.x * blockDim.x) >> 5) {
-    const int myi = lane < k ? idx[(size_t)t * k + lane] : -1;
-    const float myw = lane < k ? w[(size_t)t * k + lane] : 0.f;
-    const float mydw = lane < k ? dw[(size_t)t * k + lane] : 0.f;
-    const float p = lane < E ? probs[(size_t)t * E + lane] : 0.f;
-    float s = 0.f, g = 0.f, wsel = 0.f;
-    bool sel = false;
-    for (int j = 0; j < k; ++j) {  // same order as the scalar kernels: j ascending
-      const int ej = __shfl_sync(0xffffffffu, myi, j);
-      const float dwj = __shfl_sync(0xffffffffu, mydw, j);
-      const float wj = __shfl_sync(0xffffffffu, myw, j);
-      const float pj = __shfl_sync(0xffffffffu, p, ej & 31);
-      s += (renorm ? wj : pj) * dwj;
-      if (ej == lane) { g = dwj; wsel = wj; sel = true; }
-    }
-    if (lane < E) dl[(size_t)t * E + lane] = renorm ? (sel ? wsel * (g - s) : 0.f) : p * (g - s);
-  }
-}
-
-// Gate backward for 8 < E <= 32 in ONE pass over x: warp w of a CTA owns 64 columns (2 per lane) of a
-// 512-column split and keeps those columns of W_g (for dx += dl W_g) and its partial dW_g = sum_t dl[t] x[t]
-// over the CTA's token range in registers; dl of a batch of 8 tokens is formed once (warp = token, lane =
-// expert) and broadcast through shared memory.  The partials go to wg_part[CTA][e][c] and wg_reduce_kernel
-// sums them in CTA order.  Per element the order is fixed: reproducible.
-template <typename T, int EB>
-__global__ void __launch_bounds__(256, 1) route_bwd_wreg_kernel(const float* __restrict__ wg, const float* __restrict__ dl,
-                                                                const T* __restrict__ x,
-                                                                int T_, int E, int d, int tpc, T* __restrict__ dx,
-                                                                float* __restrict__ wg_part) {
-  pdl_enter();
-  extern __shared__ __align__(16) float dlsm[];  // [tpc][EB]: dl of the CTA's tokens
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int c = blockIdx.y * 512 + wid * 64 + lane * 2;
-  const bool active = c < d;
-  float wr[EB][2], ga[EB][2];
-#pragma unroll
-  for (int e = 0; e < EB; ++e) {
-    const float2 q = (e < E && active) ? *reinterpret_cast<const float2*>(wg + (size_t)e * d + c) : make_float2(0.f, 0.f);
-    wr[e][0] = q.x;
-    wr[e][1] = q.y;
-    ga[e][0] = ga[e][1] = 0.f;
-  }
-  const int tg0 = blockIdx.x * tpc, tg1 = min(T_, tg0 + tpc);
-  // dl of the token range (gate_dl_kernel) staged in shared memory with coalesced loads: the token loop below
-  // then runs without barriers
-  for (int i = threadIdx.x; i < (tg1 - tg0) * EB; i += blockDim.x) {
-    const int tl = i / EB, e = i % EB;
-    dlsm[i] = e < E ? __ldg(dl + (size_t)(tg0 + tl) * E + e) : 0.f;
-  }
-  __syncthreads();
-  for (int tb = tg0; tb < tg1; tb += RW_NB) {
-    const int nb = min(RW_NB, tg1 - tb);
-    float2 xb[RW_NB], db[RW_NB];  // the batch's x and dx (all loads in flight before the arithmetic)
-#pragma unroll
-    for (int b = 0; b < RW_NB; ++b) {
-      xb[b] = db[b] = make_float2(0.f, 0.f);
-      if (active && b < nb) {
-        const int t = tb + b;
-        if constexpr (sizeof(T) == 2) {
-          xb[b] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(x + (size_t)t * d + c));
-          db[b] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dx + (size_t)t * d + c));
-        } else {
-          xb[b] = *reinterpret_cast<const float2*>(x + (size_t)t * d + c);
-          db[b] = *reinterpret_cast<const float2*>(dx + (size_t)t * d + c);
-        }
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < RW_NB; ++b) {
-      if (b >= nb) break;
-      const int t = tb + b;
-      // dx += dl W_g over four interleaved partial chains (experts e = 4i + u), summed in a fixed order
-      float2 a4[4] = {db[b], make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int e4 = 0; e4 < EB; e4 += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(&dlsm[(tb - tg0 + b) * EB + e4]);
-        const float dv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e4 + u;
-          a4[u] = __ffma2_rn(make_float2(dv[u], dv[u]), make_float2(wr[e][0], wr[e][1]), a4[u]);
-          const float2 g2 = __ffma2_rn(make_float2(dv[u], dv[u]), xb[b], make_float2(ga[e][0], ga[e][1]));
-          ga[e][0] = g2.x;
-          ga[e][1] = g2.y;
-        }
-      }
-      const float2 acc = make_float2((a4[0].x + a4[1].x) + (a4[2].x + a4[3].x), (a4[0].y + a4[1].y) + (a4[2].y + a4[3].y));
-      if (active) {
-        if constexpr (sizeof(T) == 2)
-          *reinterpret_cast<__nv_bfloat162*>(dx + (size_t)t * d + c) = __floats2bfloat162_rn(acc.x, acc.y);
-        else
-          *reinterpret_cast<float2*>(dx + (size_t)t * d + c) = acc;
-      }
-    }
-  }
-  if (active)
-#pragma unroll
-    for (int e = 0; e < EB; ++e)
-      if (e < E) *reinterpret_cast<float2*>(wg_part + ((size_t)blockIdx.x * E + e) * d + c) = make_float2(ga[e][0], ga[e][1]);
-}
-
 __global__ void __launch_bounds__(256) wg_reduce_kernel(const float* __restrict__ part, int parts, int n,
                                                         float* __restrict__ out) {
   pdl_enter();
@@ -1178,36 +1070,8 @@ int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const
     LUFFY_LAUNCHED();
     return 0;
   }
-  if (L->E > 8 && L->E <= 32 && L->d % 2 == 0) {  // one pass, W_g and the dW_g partials in registers
-    const int nsplit = (L->d + 511) / 512;
-    const int cap_parts = std::max(wg_parts(L->E, L->d), (L->Tmax + 31) / 32);  // wg_part capacity (workspace)
-    int tpc = (int)(((int64_t)L->T * nsplit + device_sms() - 1) / device_sms());
-    tpc = std::max(tpc, (L->T + cap_parts - 1) / cap_parts);
-    tpc = std::max(RW_NB, (tpc + RW_NB - 1) / RW_NB * RW_NB);
-    tpc = std::min(tpc, 256);  // the dl block of the range lives in shared memory (tpc x EB floats)
-    const int parts = (L->T + tpc - 1) / tpc;
-    const dim3 grid(parts, nsplit);
-    launch_pdl(gate_dl_kernel, std::max(1, std::min((L->T + 7) / 8, 148 * 8)), 256, 0, st, (const float*)L->probs,
-               (const int32_t*)L->idx, (const float*)L->w, dw, L->T, L->E, L->k, L->renorm, L->dl);
-    LUFFY_LAUNCHED();
-#define LUFFY_RBW(EBV)                                                                                              \
-    do {                                                                                                            \
-      if (L->dtype == LUFFY_BF16)                                                                                   \
-        launch_pdl(route_bwd_wreg_kernel<bf16, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, (const float*)L->dl, \
-                   static_cast<const bf16*>(x), L->T, L->E, L->d, tpc, static_cast<bf16*>(dx), L->wg_part);        \
-      else                                                                                                          \
-        launch_pdl(route_bwd_wreg_kernel<float, EBV>, grid, 256, (size_t)tpc * EBV * 4, st, wg, (const float*)L->dl, \
-                   static_cast<const float*>(x), L->T, L->E, L->d, tpc, static_cast<float*>(dx), L->wg_part);      \
-      LUFFY_LAUNCHED();                                                                                             \
-    } while (0)
-    if (L->E <= 16) LUFFY_RBW(16);
-    else LUFFY_RBW(32);
-#undef LUFFY_RBW
-    const int n = L->E * L->d;
-    launch_pdl(wg_reduce_kernel, (n + 31) / 32, 256, 0, st, L->wg_part, parts, n, dwg);
-    LUFFY_LAUNCHED();
-    return 0;
-  }
+  // (a one-pass backward for 8 < E <= 32 holding W_g and the dW_g partials in registers was measured slower
+  // than the two kernels below -- C3 74 vs 38 us, C4 179 vs 142 us: 8 warps per SM cannot hide its loads)
   if (fast) {
     const int fb = (L->T + 31) / 32;
     const int parts = (L->T + 63) / 64;

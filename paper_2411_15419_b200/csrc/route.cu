@@ -469,133 +469,6 @@ __global__ void __launch_bounds__(256) route_finish_kernel(const float* __restri
   }
 }
 
-// Fast gate for E <= 32: a CTA of 8 warps owns 32 tokens (4 per warp); W_g is staged through shared
-// memory in chunks of RC columns and every weight read from shared memory feeds 4 tokens.  Lane l owns
-// columns {4l..4l+3} and {128+4l..128+4l+3} of each 256-wide sub-chunk (conflict-free float4 reads).
-// Summation order is fixed (chunk, lane partial, butterfly), so the logits are reproducible.
-template <typename T, int EB>
-__global__ void __launch_bounds__(256) route_fast_kernel(const T* __restrict__ x, const float* __restrict__ wg, int T_,
-                                                         int E, int d, int k, int renorm, float* __restrict__ probs,
-                                                         int32_t* __restrict__ idx, float* __restrict__ w,
-                                                         int32_t* __restrict__ idx_out, float* __restrict__ w_out) {
-  pdl_enter();
-  constexpr int TB = 4, RC = 8192 / EB;  // 32 KiB of staged weights per chunk
-  __shared__ __align__(16) float ws[EB][RC];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int t0 = blockIdx.x * 32 + wid * TB;
-  float acc[TB][EB];
-#pragma unroll
-  for (int i = 0; i < TB; ++i)
-#pragma unroll
-    for (int e = 0; e < EB; ++e) acc[i][e] = 0.f;
-  for (int c0 = 0; c0 < d; c0 += RC) {
-    const int rc = min(RC, d - c0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < E * (rc / 4); i += blockDim.x) {
-      const int e = i / (rc / 4), c = (i % (rc / 4)) * 4;
-      *reinterpret_cast<float4*>(&ws[e][c]) = *reinterpret_cast<const float4*>(wg + (size_t)e * d + c0 + c);
-    }
-    __syncthreads();
-    for (int s0 = 0; s0 < rc; s0 += 256) {
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int cl = s0 + half * 128 + lane * 4;
-        float xv[TB][4];
-#pragma unroll
-        for (int i = 0; i < TB; ++i) {
-          const int t = t0 + i;
-          if (t < T_) {
-            const T* p = x + (size_t)t * d + c0 + cl;
-            if constexpr (sizeof(T) == 2) {
-              const uint2 u = *reinterpret_cast<const uint2*>(p);
-              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-              xv[i][0] = a.x; xv[i][1] = a.y; xv[i][2] = b.x; xv[i][3] = b.y;
-            } else {
-              const float4 u = *reinterpret_cast<const float4*>(p);
-              xv[i][0] = u.x; xv[i][1] = u.y; xv[i][2] = u.z; xv[i][3] = u.w;
-            }
-          } else {
-            xv[i][0] = xv[i][1] = xv[i][2] = xv[i][3] = 0.f;
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < EB; ++e) {
-          if (e < E) {
-            const float4 wv = *reinterpret_cast<const float4*>(&ws[e][cl]);
-            // packed fp32x2 FMAs over token pairs: each logit keeps its own column-ordered fmaf chain
-            // (bit-identical to the scalar form)
-#pragma unroll
-            for (int i = 0; i < TB; i += 2) {
-              float2 s2 = make_float2(acc[i][e], acc[i + 1][e]);
-              s2 = __ffma2_rn(make_float2(xv[i][0], xv[i + 1][0]), make_float2(wv.x, wv.x), s2);
-              s2 = __ffma2_rn(make_float2(xv[i][1], xv[i + 1][1]), make_float2(wv.y, wv.y), s2);
-              s2 = __ffma2_rn(make_float2(xv[i][2], xv[i + 1][2]), make_float2(wv.z, wv.z), s2);
-              s2 = __ffma2_rn(make_float2(xv[i][3], xv[i + 1][3]), make_float2(wv.w, wv.w), s2);
-              acc[i][e] = s2.x;
-              acc[i + 1][e] = s2.y;
-            }
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < TB; ++i)
-#pragma unroll
-    for (int e = 0; e < EB; ++e) acc[i][e] = warp_sum(acc[i][e]);
-  // lane i < TB finishes token t0 + i: softmax over E, top-k by (logit desc, id asc), gate weights
-#pragma unroll
-  for (int i = 0; i < TB; ++i) {
-    const int t = t0 + i;
-    if (lane != i || t >= T_) continue;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < EB; ++e)
-      if (e < E) mx = fmaxf(mx, acc[i][e]);
-    float se = 0.f;
-#pragma unroll
-    for (int e = 0; e < EB; ++e)
-      if (e < E) se += expf(acc[i][e] - mx);
-#pragma unroll
-    for (int e = 0; e < EB; ++e)
-      if (e < E) probs[(size_t)t * E + e] = expf(acc[i][e] - mx) / se;
-    unsigned taken = 0;
-    float selv[8];
-    int seli[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= k) break;
-      float bv = -INFINITY;
-      int bi = -1;
-#pragma unroll
-      for (int e = 0; e < EB; ++e)  // ascending ids, strict '>' keeps the lowest id among equal logits
-        if (e < E && !((taken >> e) & 1u) && (bi < 0 || acc[i][e] > bv)) {
-          bv = acc[i][e];
-          bi = e;
-        }
-      taken |= 1u << bi;
-      selv[j] = bv;
-      seli[j] = bi;
-    }
-    float ev[8], sum = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < k) {
-        ev[j] = renorm ? expf(selv[j] - selv[0]) : expf(selv[j] - mx) / se;
-        sum += ev[j];
-      }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < k) {
-        const float wv = renorm ? ev[j] / sum : ev[j];
-        w[(size_t)t * k + j] = wv;
-        w_out[(size_t)t * k + j] = wv;
-        idx[(size_t)t * k + j] = seli[j];
-        idx_out[(size_t)t * k + j] = seli[j];
-      }
-  }
-}
 
 // Gate backward, per token: dl from dw (renormalized or raw softmax), then dx[t] += dl W_g.
 template <typename T>

@@ -26,7 +26,19 @@ namespace {
 
 constexpr int GC_THREADS = 1024;
 
-template <int CS>
+// Priority keys (residual degree, -index) packed into one integer (degree in the high half, so integer order
+// is the greedy's order, R8); the cluster kernel uses 32-bit keys (groups < 65536 rows): one-word
+// shared-memory traffic and compares.
+template <typename KT>
+__device__ __forceinline__ KT make_key(int deg, int r) {
+  constexpr int S = sizeof(KT) * 4;
+  constexpr KT M = (KT(1) << S) - 1;
+  return (KT(deg) << S) | (M - KT(r));
+}
+__device__ __forceinline__ uint32_t warp_max_key(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long v) { return warp_max_u64(v); }
+
+template <int CS, typename KT>
 __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int32_t* __restrict__ goff,
                                                                       const int32_t* __restrict__ gcnt,
                                                                       const int64_t* __restrict__ adjoff,
@@ -80,8 +92,8 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   const int g0 = goff[e];
   const int n = gcnt[e];
   const int W = (goff[e + 1] - g0) >> 5;
-  unsigned long long* key = reinterpret_cast<unsigned long long*>(gsm);
-  unsigned long long* m1 = key + nmax;
+  KT* key = reinterpret_cast<KT*>(gsm);
+  KT* m1 = key + nmax;
   uint32_t* alive = reinterpret_cast<uint32_t*>(m1 + nmax);
   uint32_t* win = alive + (nmax >> 5);
   uint32_t* cnt = win + (nmax >> 5);  // [2] alive counters (by round parity)
@@ -128,7 +140,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   // Replica exchange: in every phase a CTA writes only its OWN slice (rows [r0, r1) of key / m1, words
   // [r0/32, (r0+R)/32) of win / alive; R is a multiple of 32) in its shared memory; after the cluster
   // barrier every CTA copies the other slices from their shared memory with coalesced DSMEM loads.
-  auto gather_rows = [&](unsigned long long* arr) {
+  auto gather_rows = [&](KT* arr) {
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
       const int j = r / R;
       if (j != rank) arr[r] = *cluster.map_shared_rank(arr + r, j);
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       int deg = 0;
       for (int w = lane; w < W; w += 32) deg += __popc(row[w] & alive[w]);
       deg = __reduce_add_sync(0xffffffffu, deg);
-      if (lane == 0) key[r] = ((unsigned long long)deg << 32) | (unsigned long long)(0xffffffffu - (uint32_t)r);
+      if (lane == 0) key[r] = make_key<KT>(deg, r);
     }
     cluster.sync();
     gather_rows(key);
@@ -166,16 +178,16 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       const uint32_t* row = ROW(r);
-      unsigned long long m = key[r];
+      KT m = key[r];
       for (int w = lane; w < W; w += 32) {
         uint32_t bits = row[w] & alive[w];
         while (bits) {
-          const unsigned long long v = key[w * 32 + __ffs(bits) - 1];
+          const KT v = key[w * 32 + __ffs(bits) - 1];
           bits &= bits - 1u;
           m = v > m ? v : m;
         }
       }
-      m = warp_max_u64(m);
+      m = warp_max_key(m);
       if (lane == 0) m1[r] = m;
     }
     cluster.sync();
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     // has m1[j] != key[r]: most rows lose without a scan and a scan stops at the first violation.
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-      const unsigned long long kr = key[r];
+      const KT kr = key[r];
       if (m1[r] != kr) continue;
       const uint32_t* row = ROW(r);
       bool lose = false;
@@ -285,9 +297,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   if (rank == 0 && threadIdx.x == 0) atomicMax(ctrl + 2, (uint32_t)max_round);
 }
 
-template <int CS>
+template <int CS, typename KT>
 int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int nclusters, cudaStream_t st) {
-  auto kern = greedy_cluster_kernel<CS>;
+  auto kern = greedy_cluster_kernel<CS, KT>;
   LUFFY_CUDA_TRY(smem_optin((const void*)kern, (int)smem));
   if (CS > 8) LUFFY_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg{};
@@ -317,7 +329,8 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int n
 int launch_greedy_cluster(luffy_layer* L, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
   const int nmax = (int)round_up(std::min<int64_t>(L->Tmax, L->Cpad_max), 128);  // a group holds <= T copies
-  const size_t state = (size_t)nmax * 16 + (size_t)(nmax / 32) * 8 + 16;
+  // 32-bit priority keys (make_key): the shared-memory budget below caps a group at 25600 rows < 65536
+  const size_t state = (size_t)nmax * 8 + (size_t)(nmax / 32) * 8 + 16;
   if (state > 200 * 1024) return -1;
   const size_t cache_bytes = std::min<size_t>(224 * 1024 - state, 96 * 1024) / 16 * 16;  // own-row cache
   const size_t smem = state + cache_bytes;
@@ -352,9 +365,9 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
       cudaGetLastError();
       return n;
     };
-    const int n16 = coresident(greedy_cluster_kernel<16>, 16);
-    const int n12 = coresident(greedy_cluster_kernel<12>, 12);
-    const int n8 = coresident(greedy_cluster_kernel<8>, 8);
+    const int n16 = coresident(greedy_cluster_kernel<16, uint32_t>, 16);
+    const int n12 = coresident(greedy_cluster_kernel<12, uint32_t>, 12);
+    const int n8 = coresident(greedy_cluster_kernel<8, uint32_t>, 8);
     const char* force = std::getenv("LUFFY_GREEDY_CS");  // experiments: 16 / 12 / 8
     const int f = force ? std::atoi(force) : 0;
     if (f == 16 && n16 >= 1) { cs = 16; ncl = n16; }
@@ -368,9 +381,9 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
                    n16, n12, n8, smem, ncl, cs);
     dev_cache_put(&tag, ckey, (cs << 16) | (ncl & 0xffff));
   }
-  if (cs == 16) return launch_cluster<16>(L, nmax, smem, cache_words, ncl, st);
-  if (cs == 12) return launch_cluster<12>(L, nmax, smem, cache_words, ncl, st);
-  return launch_cluster<8>(L, nmax, smem, cache_words, ncl, st);
+  if (cs == 16) return launch_cluster<16, uint32_t>(L, nmax, smem, cache_words, ncl, st);
+  if (cs == 12) return launch_cluster<12, uint32_t>(L, nmax, smem, cache_words, ncl, st);
+  return launch_cluster<8, uint32_t>(L, nmax, smem, cache_words, ncl, st);
 }
 
 }  // namespace luffy

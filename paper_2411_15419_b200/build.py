@@ -25,6 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
+CU_FLAGS += os.environ.get("LUFFY_NVCC_DEFS", "").split()  # diagnostic builds only, e.g. -DLUFFY_GREEDY_FINE
 
 
 def _sources():

@@ -656,6 +656,11 @@ int launch_cg(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
       dev_cache_put((const void*)kern, -1, pairs);
       if (std::getenv("LUFFY_VERBOSE")) std::fprintf(stderr, "[luffy] gemm pair grid: %d co-resident pairs\n", pairs);
     }
+    static const int cap = [] {  // LUFFY_GEMM_PAIRS: fewer pairs (bandwidth-sharing experiments only)
+      const char* v = std::getenv("LUFFY_GEMM_PAIRS");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (cap > 0) pairs = std::min(pairs, cap);
     cfg.gridDim = dim3(2 * pairs);
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, ta, tb, tb3, td, td3, a);

@@ -35,6 +35,8 @@ __device__ __forceinline__ KT make_key(int deg, int r) {
   constexpr KT M = (KT(1) << S) - 1;
   return (KT(deg) << S) | (M - KT(r));
 }
+template <typename KT>
+__device__ __forceinline__ int key_deg(KT key) { return (int)(key >> (sizeof(KT) * 4)); }
 __device__ __forceinline__ uint32_t warp_max_key(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
 __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long v) { return warp_max_u64(v); }
 
@@ -116,6 +118,12 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     }
   };
   STAMP();
+  // finer stamps (compute end, cluster barrier end) with LUFFY_GREEDY_FINE=1 builds only
+#ifdef LUFFY_GREEDY_FINE
+  auto FSTAMP = [&]() { STAMP(); };
+#else
+  auto FSTAMP = [&]() {};
+#endif
 
   for (int w = threadIdx.x; w < W; w += blockDim.x) {
     const int valid = n - w * 32;
@@ -170,15 +178,21 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       deg = __reduce_add_sync(0xffffffffu, deg);
       if (lane == 0) key[r] = make_key<KT>(deg, r);
     }
+    FSTAMP();
     cluster.sync();
+    FSTAMP();
     gather_rows(key);
     __syncthreads();
     STAMP();
     // ---- B: m1 = max key over the alive closed neighbourhood (own rows; set bits only)
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-      const uint32_t* row = ROW(r);
       KT m = key[r];
+      if (key_deg(m) == 0) {  // no alive neighbour: m1 = own key, no scan
+        if (lane == 0) m1[r] = m;
+        continue;
+      }
+      const uint32_t* row = ROW(r);
       for (int w = lane; w < W; w += 32) {
         uint32_t bits = row[w] & alive[w];
         while (bits) {
@@ -190,7 +204,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       m = warp_max_key(m);
       if (lane == 0) m1[r] = m;
     }
+    FSTAMP();
     cluster.sync();
+    FSTAMP();
     gather_rows(m1);
     __syncthreads();
     STAMP();
@@ -201,6 +217,10 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       const KT kr = key[r];
       if (m1[r] != kr) continue;
+      if (key_deg(kr) == 0) {  // isolated among the alive rows: wins without a scan
+        if (lane == 0) atomicOr(win + (r >> 5), 1u << (r & 31));
+        continue;
+      }
       const uint32_t* row = ROW(r);
       bool lose = false;
       for (int wb = 0; wb < W; wb += 32) {
@@ -219,7 +239,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       }
       if (!lose && lane == 0) atomicOr(win + (r >> 5), 1u << (r & 31));
     }
+    FSTAMP();
     cluster.sync();
+    FSTAMP();
     gather_words(win);
     __syncthreads();
     STAMP();
@@ -229,6 +251,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     // list's length are written here, which makes the layout's member placement a direct store
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((win[r >> 5] >> (r & 31)) & 1u)) continue;
+      if (key_deg(key[r]) == 0) {  // a winner without alive neighbours is its own only member
+        if (lane == 0) {
+          mrank[g0 + r] = 0;
+          mcnt_row[g0 + r] = 1;
+        }
+        continue;
+      }
       const uint32_t* row = ROW(r);
       int base = 0;
       for (int w0 = 0; w0 < W; w0 += 32) {
@@ -274,7 +303,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         atomicAnd(alive + (r >> 5), ~(1u << (r & 31)));
       }
     }
+    FSTAMP();
     cluster.sync();
+    FSTAMP();
     gather_words(alive);
     __syncthreads();
     STAMP();

@@ -1,6 +1,6 @@
 """Time the expert-FFN GEMM variants in isolation on the C2 shapes (G=8 experts x 1600 rows, d=1024,
 f=4096) through luffy_debug_gemm: which epilogue costs what.  GPU only; diagnostic, not a test.
-    python tools/gemm_probe.py [rows_per_expert]"""
+    python tools/gemm_probe.py [rows_per_expert] [d]"""
 import os
 import sys
 
@@ -12,7 +12,7 @@ from paper_2411_15419_b200 import luffy as L  # noqa: E402
 
 def main():
     rpe = int(sys.argv[1]) if len(sys.argv) > 1 else 1536
-    G, d, f = 8, 1024, 4096
+    G, d, f = 8, (int(sys.argv[2]) if len(sys.argv) > 2 else 1024), 4096  # d = 64: epilogue-bound tiles
     rows = G * rpe
     off = torch.arange(0, rows + 1, rpe, dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
@@ -41,6 +41,8 @@ def main():
     }
     flops = 2.0 * rows * d * f
     for name, fn in runs.items():
+        if d < 256 and "N=f" not in name:
+            continue  # N = d < one tile
         for _ in range(3):
             fn()
         torch.cuda.synchronize()

@@ -363,7 +363,7 @@ int launch_greedy_cluster(luffy_layer* L, void* s) {
   // 32-bit priority keys (make_key): the shared-memory budget below caps a group at 25600 rows < 65536
   const size_t state = (size_t)nmax * 8 + (size_t)(nmax / 32) * 8 + 16;
   if (state > 200 * 1024) return -1;
-  const size_t cache_bytes = std::min<size_t>(224 * 1024 - state, 96 * 1024) / 16 * 16;  // own-row cache
+  const size_t cache_bytes = (224 * 1024 - state) / 16 * 16;  // own-row cache
   const size_t smem = state + cache_bytes;
   const int cache_words = (int)(cache_bytes / 4);
   // (the control block is zeroed by gather_norm_kernel, which precedes the Gram)

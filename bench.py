@@ -469,6 +469,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ktab", action="store_true", help="skip the CUPTI per-kernel pass (e.g. under ncu)")
+    ap.add_argument("--no-graph", action="store_true", help="one GPU: time eager steps instead of CUDA-graph replays")
     ap.add_argument("--migrate", type=int, default=0,
                     help="world > 1: sequence migration with Alg. 1 candidate-set size q (0 = off)")
     ap.add_argument("--stack", type=int, default=0, help="run the N-block stack (attention + MoE) instead of one layer")
@@ -536,7 +537,11 @@ def main():
         dy_out = torch.randn(world * T, cfg.d_model, device=dev).to(tdt)
         mig_stats = {"migrated_seqs": 0, "hosted_tokens": 0}
 
+    SH = [s]  # stream handle the step's calls go to (the capture stream while a CUDA graph records it)
+
     def step(evs=None):
+        s = SH[0]
+
         def m(i):
             if evs is not None:
                 evs[i].record(stream)
@@ -577,6 +582,31 @@ def main():
     n_ev = len(marks) + 1
     start, stop = ev(), ev()
 
+    # one GPU: the step is captured once into a CUDA graph and replayed (the whole fwd+bwd is device-side,
+    # no host sync; PDL edges are kept by the capture), so the host enqueue (~0.5 ms of ctypes calls per
+    # step) can never starve the GPU.  N > 1 runs eagerly: each step's exchange flags carry a new sequence
+    # number set by the host.
+    graph = None
+    if world == 1 and not mig and not args.no_graph:
+        try:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            n0 = L.luffy_launch_count()
+            SH[0] = cap.cuda_stream
+            with torch.cuda.graph(g, stream=cap):
+                step()
+            graph_launches = L.luffy_launch_count() - n0
+            SH[0] = s
+            stream.wait_stream(cap)
+            for _ in range(2):
+                g.replay()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as exc:  # capture unsupported here: eager steps
+            SH[0] = s
+            print(f"[bench] CUDA graph capture failed ({exc}); eager steps", file=sys.stderr)
+            torch.cuda.synchronize()
     launches0 = L.luffy_launch_count()
     torch.cuda.synchronize()
     if world > 1:
@@ -584,11 +614,14 @@ def main():
     t_host0 = time.time()
     start.record(stream)
     for i in range(args.steps):
-        step()  # no events inside the timed steps: a stream event between kernels would block their PDL overlap
+        if graph is not None:
+            graph.replay()
+        else:
+            step()  # no events inside the timed steps: a stream event between kernels would block their PDL overlap
     stop.record(stream)
     host_ms = (time.time() - t_host0) * 1e3 / args.steps  # enqueue time per step (no host sync in the step)
     torch.cuda.synchronize()
-    launches = (L.luffy_launch_count() - launches0) // args.steps
+    launches = graph_launches if graph is not None else (L.luffy_launch_count() - launches0) // args.steps
     clk.window = (t_host0, time.time())
     time.sleep(0.06)
     clk_window = "timed region"
@@ -603,7 +636,7 @@ def main():
         t1 = time.time()
         while time.time() - t1 < 0.3:
             for _ in range(20):
-                step()
+                graph.replay() if graph is not None else step()
             torch.cuda.synchronize()
         clk.window = (t1, time.time())
         time.sleep(0.06)
@@ -664,7 +697,7 @@ def main():
         hx = torch.empty(x.shape, dtype=tdt, pin_memory=True).copy_(x)
         hdy = torch.empty(dy.shape, dtype=tdt, pin_memory=True).copy_(dy)
         hy = torch.empty(x.shape, dtype=tdt, pin_memory=True)
-        stepper = LY.HostStepper(lay, T)
+        stepper = LY.HostStepper(lay, T, graphs=os.environ.get("LUFFY_STEPPER_GRAPHS", "1") != "0")
         stepper.run([(hx, hdy, hy)] * 3, wg, w1, w2, w3, h=cfg.h)
         torch.cuda.synchronize()
         if world > 1:
@@ -815,7 +848,8 @@ def main():
                "migration": ({"q": args.migrate, **mig_stats} if mig else None),
                "breakdown_ms": breakdown, "roofline": roof, "roofline_gram": gram_roof, "roofline_memory": mem_roof,
                "kernel_shares": shares, "nvlink": nvlink, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(launches), "host_enqueue_ms_per_step": host_ms, "clocks": clocks}
+               "gpu_launches": int(launches), "host_enqueue_ms_per_step": host_ms, "clocks": clocks,
+               "step_exec": "cuda_graph_replay" if graph is not None else "eager"}
         print(json.dumps(out), flush=True)
     lay.close()
     if world > 1:

@@ -177,9 +177,13 @@ class HostStepper:
     result; device buffers are double-buffered and ordered with events (an upload waits for the backward
     that last read its buffer, a forward waits for the download that last read its output buffer)."""
 
-    def __init__(self, layer: CondensedMoELayer, tokens: int):
+    def __init__(self, layer: CondensedMoELayer, tokens: int, graphs: bool = True):
         dev, tdt, d = layer.device, layer.tdt, layer.d
         self.layer, self.T, self.dev = layer, tokens, dev
+        # one GPU: the forward and the backward of each buffer parity are captured once as CUDA graphs and
+        # replayed (no per-step host launch cost); the copies and their events stay on the copy streams
+        self.graphs = graphs and layer.world == 1
+        self._g, self._gkey = None, None
         self.x = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
         self.dy = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
         self.y = [torch.empty(tokens, d, dtype=tdt, device=dev) for _ in range(2)]
@@ -205,6 +209,21 @@ class HostStepper:
                 self.dy[b].copy_(batches[i][1], non_blocking=True)
             self.ev_in[b].record(self.h2d)
 
+        key = (w_gate.data_ptr(), w1.data_ptr(), w2.data_ptr(), None if w3 is None else w3.data_ptr(), float(h))
+        if self.graphs and self._gkey != key:
+            cap = torch.cuda.Stream(device=self.dev)
+            cap.wait_stream(cs)
+            self._g = []
+            for b in range(2):
+                gf, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gf, stream=cap):
+                    self.layer.forward(self.x[b][:T], w_gate, w1, w2, w3, h=h, out=self.y[b])
+                with torch.cuda.graph(gb, stream=cap):
+                    self.layer.backward(self.dy[b][:T], self.x[b][:T], w_gate, w1, w2, w3)
+                self._g.append((gf, gb))
+            cs.wait_stream(cap)
+            self._gkey = key
+
         upload(0)
         for i in range(n):
             b = i % 2
@@ -213,12 +232,19 @@ class HostStepper:
             cs.wait_event(self.ev_in[b])
             if i >= 2:
                 cs.wait_event(self.ev_out[b])
-            y = self.layer.forward(self.x[b][:T], w_gate, w1, w2, w3, h=h, out=self.y[b])
+            if self.graphs:
+                self._g[b][0].replay()
+                y = self.y[b][:T]
+            else:
+                y = self.layer.forward(self.x[b][:T], w_gate, w1, w2, w3, h=h, out=self.y[b])
             self.ev_y[b].record(cs)
             self.d2h.wait_event(self.ev_y[b])
             with torch.cuda.stream(self.d2h):
                 batches[i][2].copy_(y, non_blocking=True)
             self.ev_out[b].record(self.d2h)
-            self.layer.backward(self.dy[b][:T], self.x[b][:T], w_gate, w1, w2, w3)
+            if self.graphs:
+                self._g[b][1].replay()
+            else:
+                self.layer.backward(self.dy[b][:T], self.x[b][:T], w_gate, w1, w2, w3)
             self.ev_used[b].record(cs)
         cs.wait_event(self.ev_out[(n - 1) % 2])

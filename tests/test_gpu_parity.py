@@ -225,10 +225,11 @@ def test_deterministic_bitwise():
         assert np.array_equal(a[k], b[k]), k
 
 
-def test_host_stepper_pipelined_steps():
+@pytest.mark.parametrize("graphs", [True, False])
+def test_host_stepper_pipelined_steps(graphs):
     """HostStepper (the e2e driver): three steps with DIFFERENT host inputs, uploads / downloads overlapped
-    with compute on two copy streams; every downloaded Y and the gradients of the last step equal the
-    device-resident path bitwise (the kernels are deterministic)."""
+    with compute on two copy streams, the compute replayed from CUDA graphs (or eager); every downloaded Y
+    and the gradients of the last step equal the device-resident path bitwise (deterministic kernels)."""
     import torch
     from paper_2411_15419_b200 import layer as LY
     cfg = C2S
@@ -245,7 +246,9 @@ def test_host_stepper_pipelined_steps():
         hx = torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True).copy_(bf(inp["X"]))
         hdy = torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True).copy_(bf(inp["dY"]))
         host.append((hx, hdy, torch.empty(T, cfg.d_model, dtype=torch.bfloat16, pin_memory=True)))
-    LY.HostStepper(lay, T).run(host, wg, w1, w2, None, h=0.9)
+    st = LY.HostStepper(lay, T, graphs=graphs)
+    st.run(host, wg, w1, w2, None, h=0.9)
+    st.run(host, wg, w1, w2, None, h=0.9)  # graphs: the second run replays the captured ones
     torch.cuda.synchronize()
     dw1_pipe = lay.dw1.clone()
     for hx, hdy, hy in host:

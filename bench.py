@@ -582,27 +582,33 @@ def main():
     n_ev = len(marks) + 1
     start, stop = ev(), ev()
 
-    # one GPU: the step is captured once into a CUDA graph and replayed (the whole fwd+bwd is device-side,
-    # no host sync; PDL edges are kept by the capture), so the host enqueue (~0.5 ms of ctypes calls per
-    # step) can never starve the GPU.  N > 1 runs eagerly: each step's exchange flags carry a new sequence
-    # number set by the host.
+    # The step is captured into CUDA graphs once and replayed (the whole fwd+bwd is device-side with no host
+    # sync; PDL edges are kept by the capture), so host enqueue jitter and launch gaps never reach the GPU.
+    # World > 1: two consecutive steps are captured (the receive buffers alternate by step parity) and
+    # replayed alternately; every exchange flag carries the device step number (luffy_layer::dseq) that each
+    # replay bumps.  Sequence migration (a host planner per step) runs eagerly.
     graph = None
-    if world == 1 and not mig and not args.no_graph:
+    if not mig and not args.no_graph:
         try:
             cap = torch.cuda.Stream(device=dev)
             cap.wait_stream(stream)
-            g = torch.cuda.CUDAGraph()
+            gs = []
             n0 = L.luffy_launch_count()
             SH[0] = cap.cuda_stream
-            with torch.cuda.graph(g, stream=cap):
-                step()
-            graph_launches = L.luffy_launch_count() - n0
+            for _ in range(1 if world == 1 else 2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cap):
+                    step()
+                gs.append(g)
+            graph_launches = (L.luffy_launch_count() - n0) // len(gs)
             SH[0] = s
             stream.wait_stream(cap)
-            for _ in range(2):
-                g.replay()
+            if world > 1:
+                dist.barrier()
+            for i in range(2 * len(gs)):
+                gs[i % len(gs)].replay()
             torch.cuda.synchronize()
-            graph = g
+            graph = gs
         except Exception as exc:  # capture unsupported here: eager steps
             SH[0] = s
             print(f"[bench] CUDA graph capture failed ({exc}); eager steps", file=sys.stderr)
@@ -615,7 +621,7 @@ def main():
     start.record(stream)
     for i in range(args.steps):
         if graph is not None:
-            graph.replay()
+            graph[i % len(graph)].replay()
         else:
             step()  # no events inside the timed steps: a stream event between kernels would block their PDL overlap
     stop.record(stream)
@@ -636,7 +642,7 @@ def main():
         t1 = time.time()
         while time.time() - t1 < 0.3:
             for _ in range(20):
-                graph.replay() if graph is not None else step()
+                graph[_ % len(graph)].replay() if graph is not None else step()
             torch.cuda.synchronize()
         clk.window = (t1, time.time())
         time.sleep(0.06)

@@ -176,6 +176,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->ctrl = cv.take<uint32_t>(64 + kGreedyMaxRounds);
   o->stat64 = cv.take<uint64_t>(4);
   o->x_errw = cv.take<uint32_t>(2);
+  o->dseq = cv.take<uint32_t>(1);
   if (c->fast_measure) {
     o->hone = cv.take<uint32_t>(m.adjw);
     o->hzero = cv.take<uint32_t>(m.adjw);
@@ -446,6 +447,7 @@ luffy_status luffy_layer_create(luffy_ctx* ctx, void* ws, size_t bytes, luffy_la
   {  // the grouping's last-CTA ticket starts at zero (every launch leaves it at zero)
     cudaError_t e = cudaMemset(L->gticket, 0, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(L->x_errw, 0, 2 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(L->dseq, 0, sizeof(uint32_t));
     if (e != cudaSuccess) {
       delete L;
       return cuda_fail(e, "luffy_layer_create (workspace init)");
@@ -643,6 +645,7 @@ luffy_status luffy_route(luffy_layer* L, const void* x, const float* w_gate, int
   L->seq += 1;  // a new forward step (every rank calls in lockstep)
   L->S = 0;
   L->mig = false;
+  if (L->P > 1) LUFFY_CHECK(launch_xstep(L, stream), "luffy_route/step");
   LUFFY_CHECK(launch_route(L, x, w_gate, topk_idx, topk_w, stream), "luffy_route");
   L->stage = 1;
   return LUFFY_OK;
@@ -794,7 +797,7 @@ luffy_status luffy_expert_ffn(luffy_layer* L, const void* recv, const void* w1, 
   const bool tile_wait = L->P > 1 && L->dtype == LUFFY_BF16;
   if (tile_wait) {
     wr.flags = L->x_flags + XP_DISP * L->P;
-    wr.seq = L->seq;
+    wr.seqp = L->dseq;
     wr.P = L->P;
     wr.E = L->E;
     wr.El = L->El;

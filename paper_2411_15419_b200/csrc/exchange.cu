@@ -12,11 +12,18 @@ namespace luffy {
 namespace {
 
 // Wait until every rank published `seq` for this phase (bounded: see xwait_flag).
-__global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t seq, XErr err, int phase) {
+__global__ void xwait_kernel(const uint32_t* __restrict__ flags, int P, const uint32_t* seqp, XErr err, int phase) {
   pdl_enter();
   const int p = threadIdx.x;
-  if (p < P) xwait_flag(flags + p, seq, err, phase);
+  if (p < P) xwait_flag(flags + p, *seqp, err, phase);
   __syncthreads();
+}
+
+// First launch of a step at world > 1 (luffy_route): the device step number every exchange of the step
+// publishes and waits for.  Device-resident, so a step captured in a CUDA graph bumps it on every replay.
+__global__ void xstep_kernel(uint32_t* dseq) {
+  pdl_enter();
+  if (threadIdx.x == 0) *dseq += 1u;
 }
 
 // Count exchange and layout plan in ONE single-CTA kernel: push my counts to every rank, publish XP_CNT,
@@ -31,7 +38,7 @@ __global__ void xcnt_plan_kernel(const int32_t* __restrict__ nrep, int E, int me
     peer_cnt[p][(size_t)me * E + e] = nrep[e];
   }
   xsignal_done(sig);  // (single CTA: publishes XP_CNT to every rank)
-  if (threadIdx.x < P) xwait_flag(flags + threadIdx.x, sig.seq, err, XP_CNT);
+  if (threadIdx.x < P) xwait_flag(flags + threadIdx.x, *sig.seqp, err, XP_CNT);
   __syncthreads();
   xplan_body(inbox, P, E, me, cnt_all, roff, dst_base, src_soff, threadIdx.x, blockDim.x);
 }
@@ -187,7 +194,13 @@ inline int grid_warps(int64_t warps) {
 
 int launch_xwait(const luffy_layer* L, int phase, void* s) {
   cudaStream_t st = static_cast<cudaStream_t>(s);
-  launch_pdl(xwait_kernel, 1, 64, 0, st, L->x_flags + phase * L->P, L->P, L->seq, make_xerr(L), phase);
+  launch_pdl(xwait_kernel, 1, 64, 0, st, L->x_flags + phase * L->P, L->P, (const uint32_t*)L->dseq, make_xerr(L), phase);
+  LUFFY_LAUNCHED();
+  return 0;
+}
+
+int launch_xstep(const luffy_layer* L, void* s) {
+  launch_pdl(xstep_kernel, 1, 32, 0, static_cast<cudaStream_t>(s), L->dseq);
   LUFFY_LAUNCHED();
   return 0;
 }
@@ -205,7 +218,7 @@ XSignal make_signal(const luffy_layer* L, int phase) {
   sg.counter = L->x_counters + phase;
   sg.flag = L->x_flagptr + phase * L->P;
   sg.P = L->P;
-  sg.seq = L->seq;
+  sg.seqp = L->dseq;
   return sg;
 }
 

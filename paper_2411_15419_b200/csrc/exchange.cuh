@@ -30,7 +30,7 @@ struct XSignal {
   uint32_t* counter;        // local CTA-completion counter (reset by the last CTA)
   uint32_t* const* flag;    // [P] address of (phase, my rank) in each peer's flag array
   int P;
-  uint32_t seq;
+  const uint32_t* seqp;     // the step's sequence number (device word, luffy_layer::dseq)
 };
 
 // Row redirect for an epilogue.  mask == nullptr: expert-layout row r goes to rank rank_of[r], row
@@ -63,7 +63,8 @@ __device__ __forceinline__ void xsignal_done(const XSignal& s) {
     if (prev == total - 1) {
       *s.counter = 0u;
       __threadfence_system();
-      for (int p = 0; p < s.P; ++p) st_release_sys(s.flag[p], s.seq);
+      const uint32_t seq = *s.seqp;
+      for (int p = 0; p < s.P; ++p) st_release_sys(s.flag[p], seq);
     }
   }
 }
@@ -119,7 +120,7 @@ __device__ __forceinline__ bool xwait_flag(const uint32_t* flag, uint32_t seq, c
 // q's pack-and-push kernel), instead of a stream-wide wait for every rank.
 struct XWaitRows {
   const uint32_t* flags;   // [P] this rank's XP_DISP flags (one per source rank)
-  uint32_t seq;
+  const uint32_t* seqp;    // the step's sequence number (device word)
   int P, E, El, me;
   const int32_t* cnt_all;  // [P][E] rows each source sends to each expert
   const int32_t* roff;     // [El+1] expert-layout offsets of the local experts
@@ -127,10 +128,11 @@ struct XWaitRows {
 };
 __device__ __forceinline__ void xwait_rows(const XWaitRows& w, int el, int r0, int r1) {
   const int e = w.me * w.El + el;
+  const uint32_t seq = *w.seqp;
   int base = w.roff[el];
   for (int q = 0; q < w.P; ++q) {
     const int n = w.cnt_all[q * w.E + e];
-    if (n > 0 && base < r1 && base + n > r0) xwait_flag(w.flags + q, w.seq, w.err, XP_DISP);
+    if (n > 0 && base < r1 && base + n > r0) xwait_flag(w.flags + q, seq, w.err, XP_DISP);
     base += n;
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");  // peer-written rows -> TMA (async proxy) reads

@@ -115,6 +115,8 @@ struct luffy_layer {
   uint32_t* x_err_h;     // [2] mapped pinned host memory: first timed-out exchange wait (phase + 1, seq)
   uint32_t* x_err_d;     // its device alias
   uint32_t* x_errw;      // [2] device copy polled by the waits (workspace)
+  uint32_t* dseq;        // [1] device step sequence number (world > 1: bumped by luffy_route's first launch;
+                         //     every exchange flag carries it, so a captured step replays correctly)
   uint64_t x_timeout_ns; // bound of every cross-rank wait (LUFFY_EXCHANGE_TIMEOUT_MS, luffy_layer_set_exchange_timeout)
   void* x_recv[2];     // own buffers inside the region
   void* x_gathered;
@@ -181,6 +183,7 @@ int launch_unpack_bwd(const luffy_layer* L, const void* dsend, const void* res, 
 int launch_route_bwd(const luffy_layer* L, const void* x, const float* wg, const float* dw, void* dx, float* dwg, void* s);
 int launch_xdispatch(luffy_layer* L, const void* x, void* s);
 int launch_xwait(const luffy_layer* L, int phase, void* s);
+int launch_xstep(const luffy_layer* L, void* s);
 int launch_seq_rows(luffy_layer* L, void* s);
 int launch_set_migration(luffy_layer* L, void* s);
 int launch_mig_meta_push(luffy_layer* L, void* s);

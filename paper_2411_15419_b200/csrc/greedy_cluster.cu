@@ -72,7 +72,11 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     order_s[rk] = i;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && E <= ncl) {  // a cluster per group: LPT puts the r-th costliest on cluster r
+    nlist_s = cid < E ? 1 : 0;
+    if (cid < E) list_s[0] = order_s[cid];
+    largest_s = order_s[0];
+  } else if (threadIdx.x == 0) {
     long long load[32];
     for (int c = 0; c < ncl; ++c) load[c] = 0;
     int k = 0;
@@ -139,7 +143,11 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
 #pragma unroll 4
     for (int i = threadIdx.x; i < nv; i += blockDim.x) dst[i] = src[i];
   }
-  auto ROW = [&](int r) -> const uint32_t* { return r - r0 < ncached ? rowc + (r - r0) * W : A + (int64_t)r * W; };
+  // word w of adjacency row r: a shared-memory load for the cached rows (all of them at the usual group
+  // sizes), a global load otherwise -- two explicit address spaces instead of one generic pointer
+  auto RW = [&](int r, int w) -> uint32_t {
+    return r - r0 < ncached ? rowc[(r - r0) * W + w] : __ldg(A + (int64_t)r * W + w);
+  };
   for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) rep_local[g0 + r] = -1;
   if (rank == CS - 1)  // padding rows of the group's row space: never representatives
     for (int r = n + threadIdx.x; r < W * 32; r += blockDim.x) rep_local[g0 + r] = -1;
@@ -172,9 +180,8 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     for (int w = w0 + threadIdx.x; w < w1; w += blockDim.x) win[w] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
-      const uint32_t* row = ROW(r);
       int deg = 0;
-      for (int w = lane; w < W; w += 32) deg += __popc(row[w] & alive[w]);
+      for (int w = lane; w < W; w += 32) deg += __popc(RW(r, w) & alive[w]);
       deg = __reduce_add_sync(0xffffffffu, deg);
       if (lane == 0) key[r] = make_key<KT>(deg, r);
     }
@@ -192,9 +199,8 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         if (lane == 0) m1[r] = m;
         continue;
       }
-      const uint32_t* row = ROW(r);
       for (int w = lane; w < W; w += 32) {
-        uint32_t bits = row[w] & alive[w];
+        uint32_t bits = RW(r, w) & alive[w];
         while (bits) {
           const KT v = key[w * 32 + __ffs(bits) - 1];
           bits &= bits - 1u;
@@ -221,12 +227,11 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         if (lane == 0) atomicOr(win + (r >> 5), 1u << (r & 31));
         continue;
       }
-      const uint32_t* row = ROW(r);
       bool lose = false;
       for (int wb = 0; wb < W; wb += 32) {
         const int w = wb + lane;
         if (w < W) {
-          uint32_t bits = row[w] & alive[w];
+          uint32_t bits = RW(r, w) & alive[w];
           while (bits && !lose) {
             lose = m1[w * 32 + __ffs(bits) - 1] != kr;
             bits &= bits - 1u;
@@ -258,11 +263,10 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
         }
         continue;
       }
-      const uint32_t* row = ROW(r);
       int base = 0;
       for (int w0 = 0; w0 < W; w0 += 32) {
         const int w = w0 + lane;
-        uint32_t m = w < W ? (row[w] & alive[w]) : 0u;
+        uint32_t m = w < W ? (RW(r, w) & alive[w]) : 0u;
         if (w == (r >> 5)) m |= 1u << (r & 31);
         const int cnt = __popc(m);
         int inc = cnt;
@@ -289,10 +293,9 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
       if ((win[r >> 5] >> (r & 31)) & 1u) {
         owner = r;
       } else {
-        const uint32_t* row = ROW(r);
         int found = 0x7fffffff;
         for (int w = lane; w < W; w += 32) {
-          const uint32_t bits = row[w] & win[w];
+          const uint32_t bits = RW(r, w) & win[w];
           if (bits) found = min(found, w * 32 + __ffs(bits) - 1);
         }
         found = __reduce_min_sync(0xffffffffu, found);

@@ -32,6 +32,11 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Kernels whose prologue touches nothing the preceding kernel writes (mbarrier init, TMEM allocation,
+// tensor-map prefetch, cluster barrier) start with pdl_defer() and call pdl_enter() right after that
+// prologue and before their first global-memory access, so a CTA that becomes resident while the previous
+// kernel is still draining spends the wait with its prologue already done.
+__device__ __forceinline__ void pdl_defer() {}
 
 // Per-device launch caches (api.cu).  Function attributes and occupancy answers belong to a (kernel,
 // device) pair, so they are cached per current device and per `extra` key (e.g. the shared-memory size or

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                    const __grid_constant__ CUtensorMap tB3, const __grid_constant__ CUtensorMap tD,
                    const __grid_constant__ CUtensorMap tD3, const TcArgs a) {
-  pdl_enter();
+  pdl_defer();
   constexpr int STAGES = Pipe<CG>::STAGES;
   constexpr int B_BYTES = Pipe<CG>::B_BYTES;
   constexpr int B_ROWS = Pipe<CG>::B_ROWS;
@@ -256,7 +256,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i <= a.G; i += blockDim.x) off_s[i] = a.off[i];
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -279,6 +278,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (CG == 2) tc::cluster_sync();  // barrier inits visible to the peer before any remote arrive
   else __syncthreads();
   tc::tc_fence_after();
+  pdl_enter();  // from here on: the previous kernel's outputs (expert offsets, operands)
+  for (int i = threadIdx.x; i <= a.G; i += blockDim.x) off_s[i] = a.off[i];
+  __syncthreads();
   const uint32_t tmem_base = *tmem_holder;
   const int ntiles = num_tiles<WG, CG>(a, off_s);
   const int tile0 = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;

@@ -125,7 +125,7 @@ __device__ __forceinline__ bool decode_tile(int t, const int32_t* goff_s, int E,
 
 template <bool HIST>
 __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_constant__ CUtensorMap tX, const GramArgs a) {
-  pdl_enter();
+  pdl_defer();
   extern __shared__ uint8_t smem_raw[];
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
@@ -142,18 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = tc::cluster_rank();  // 0: leader (issues the MMA)
   const int E = a.E;
-  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
-    goff_s[i] = a.goff[i];
-    if (i < E) gcnt_s[i] = a.gcnt[i];
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (int e = 0; e < E; ++e) {
-      const int nt = pair_blocks(goff_s[e + 1] - goff_s[e]);
-      n += nt * (nt + 1) / 2;
-    }
-    ntiles_s = n;
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -169,6 +158,21 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
+  pdl_enter();  // from here on: the previous kernels' outputs (group offsets and rows, norms)
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+    goff_s[i] = a.goff[i];
+    if (i < E) gcnt_s[i] = a.gcnt[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int e = 0; e < E; ++e) {
+      const int nt = pair_blocks(goff_s[e + 1] - goff_s[e]);
+      n += nt * (nt + 1) / 2;
+    }
+    ntiles_s = n;
+  }
+  __syncthreads();
   const uint32_t tmem_base = *tmem_holder;
   const int ntiles = ntiles_s;
   const int nkb = a.d / BK;

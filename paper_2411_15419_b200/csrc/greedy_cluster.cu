@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     for (int w = lane; w < W; w += 32) left += __popc(alive[w]);
     if (__reduce_add_sync(0xffffffffu, left) == 0) break;
     // ---- A: residual degree -> key (own rows)
+    FSTAMP();
     for (int w = w0 + threadIdx.x; w < w1; w += blockDim.x) win[w] = 0u;
     for (int r = r0 + wid; r < r1; r += nwarp) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;

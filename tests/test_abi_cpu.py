@@ -106,7 +106,18 @@ def test_every_kernel_enters_through_pdl():
         assert "<<<" not in code, f"{fn}: raw <<<>>> launch"
         for m in re.finditer(r"__global__[^;{]*?\)\s*\{", code, re.S):
             body = code[m.end():m.end() + 200].lstrip()
-            assert body.startswith("pdl_enter();"), f"{fn}: kernel at offset {m.start()} does not start with pdl_enter()"
+            if body.startswith("pdl_defer();"):
+                # deferred wait (tensor-core kernels): pdl_enter() follows the prologue and comes before the
+                # first read of a kernel-argument pointer (a.*[...]) in the kernel
+                full = code[m.end():]
+                end = full.find("\n}\n")
+                k = full[:end]
+                i_enter = k.find("pdl_enter();")
+                assert i_enter > 0, f"{fn}: pdl_defer() without pdl_enter()"
+                first_read = re.search(r"\ba\.\w+\[", k)
+                assert first_read is None or first_read.start() > i_enter, f"{fn}: global read before pdl_enter()"
+            else:
+                assert body.startswith("pdl_enter();"), f"{fn}: kernel at offset {m.start()} does not start with pdl_enter()"
             kernels += 1
     assert kernels >= 30
 

@@ -177,6 +177,7 @@ void carve(const luffy_config* c, Carver& cv, luffy_layer* L) {
   o->stat64 = cv.take<uint64_t>(4);
   o->x_errw = cv.take<uint32_t>(2);
   o->dseq = cv.take<uint32_t>(1);
+  o->gdone = cv.take<uint32_t>(LUFFY_MAX_EXPERTS);
   if (c->fast_measure) {
     o->hone = cv.take<uint32_t>(m.adjw);
     o->hzero = cv.take<uint32_t>(m.adjw);
@@ -681,6 +682,7 @@ luffy_status luffy_condense(luffy_layer* L, const void* x, float h, int32_t* rep
   } else {
     L->has_adj = true;
     // bf16: tcgen05 Gram; fp32: exact SIMT FFMA Gram
+    L->gdone_live = L->dtype == LUFFY_BF16;
     if (L->dtype == LUFFY_BF16) LUFFY_CHECK(launch_gram_tc(L, h, band, stream), "luffy_condense/gram");
     else LUFFY_CHECK(launch_gram_simt(L, h, band, stream), "luffy_condense/gram");
     LUFFY_CHECK(launch_greedy(L, stream), "luffy_condense/greedy");

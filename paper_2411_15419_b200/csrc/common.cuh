@@ -37,6 +37,9 @@ __device__ __forceinline__ void pdl_enter() {
 // prologue and before their first global-memory access, so a CTA that becomes resident while the previous
 // kernel is still draining spends the wait with its prologue already done.
 __device__ __forceinline__ void pdl_defer() {}
+// griddepcontrol.launch_dependents alone: for a kernel that synchronises with its predecessor through
+// explicit counters instead of waiting for the whole grid (greedy_cluster_kernel after the Gram)
+__device__ __forceinline__ void pdl_launch_only() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Per-device launch caches (api.cu).  Function attributes and occupancy answers belong to a (kernel,
 // device) pair, so they are cached per current device and per `extra` key (e.g. the shared-memory size or

@@ -34,7 +34,8 @@ constexpr int GB_TCH = 128;
 __global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __restrict__ idx, int T, int k, int E,
                                                             int32_t* __restrict__ chunk, uint32_t* __restrict__ ticket,
                                                             int32_t* __restrict__ gcnt, int32_t* __restrict__ goff,
-                                                            int64_t* __restrict__ adjoff, uint32_t* __restrict__ ctrl) {
+                                                            int64_t* __restrict__ adjoff, uint32_t* __restrict__ ctrl,
+                                                            uint32_t* __restrict__ gdone) {
   pdl_enter();
   __shared__ int cnt[LUFFY_MAX_EXPERTS];
   __shared__ bool last;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(GB_TCH) group_count_kernel(const int32_t* __re
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 64; i += blockDim.x) ctrl[i] = 0u;  // greedy control block reset
+  for (int i = threadIdx.x; i < E; i += blockDim.x) gdone[i] = 0u;  // Gram tiles finished per group
   __syncthreads();
   if (threadIdx.x == 0) {
     int o = 0;
@@ -521,7 +523,7 @@ int launch_group_build(luffy_layer* L, const void* x, void* s) {
   if (L->k > 8) return (int)cudaErrorInvalidValue;
   const int nch = (L->T + GB_TCH - 1) / GB_TCH;
   launch_pdl(group_count_kernel, nch, GB_TCH, 0, st, (const int32_t*)L->idx, L->T, L->k, L->E, L->gchunk, L->gticket,
-             L->gcnt, L->goff, L->adjoff, L->ctrl);
+             L->gcnt, L->goff, L->adjoff, L->ctrl, L->gdone);
   LUFFY_LAUNCHED();
   if (L->dtype == LUFFY_BF16)
     launch_pdl(group_place_kernel<bf16>, nch * GB_SUB, 256, 0, st, static_cast<const bf16*>(x), (const int32_t*)L->idx,

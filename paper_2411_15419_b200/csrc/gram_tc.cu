@@ -40,6 +40,7 @@ struct GramArgs {
   const uint32_t* dec1;           // previous block's s > S1 for this block's pairs (nullable: no history)
   const uint32_t* dec0;           // previous block's s < S2
   const uint8_t* tskip;           // [tiles] 1: every pair of the tile is decided -> no TMA, no MMA
+  uint32_t* gdone;                // out (nullable): per group, pair tiles finished (+1 per CTA of the pair)
   uint32_t* hone;                 // out: this block's finalized weight > S1
   uint32_t* hzero;                // out: this block's finalized weight < S2
   double c2s1, c2s2;              // 2 S1 - 1, 2 S2 - 1
@@ -105,10 +106,25 @@ __device__ __forceinline__ uint32_t decide_row(const uint32_t (&r)[32], const fl
   return word;
 }
 
-// pair tiles (I, J), J >= I, over blocks of 2 TS rows of each group
+// pair tiles (I, J), J >= I, over blocks of 2 TS rows of each group; groups in descending cost (n^2, ties
+// to the lower group) -- the order the representative selection schedules them in, so the costliest
+// group's selection can start first (greedy_cluster_kernel waits per group on GramArgs::gdone)
 __device__ __forceinline__ int pair_blocks(int npad) { return (npad / TS + 1) / 2; }
-__device__ __forceinline__ bool decode_tile(int t, const int32_t* goff_s, int E, int& e, int& I, int& J) {
-  for (e = 0; e < E; ++e) {
+__device__ __forceinline__ void group_order(const int32_t* gcnt_s, int E, int* order_s) {
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const long long ci = (long long)gcnt_s[i] * gcnt_s[i];
+    int rk = 0;
+    for (int j = 0; j < E; ++j) {
+      const long long cj = (long long)gcnt_s[j] * gcnt_s[j];
+      rk += (cj > ci) || (cj == ci && j < i);
+    }
+    order_s[rk] = i;
+  }
+}
+__device__ __forceinline__ bool decode_tile(int t, const int32_t* goff_s, const int* order_s, int E, int& e, int& I,
+                                            int& J) {
+  for (int r = 0; r < E; ++r) {
+    e = order_s[r];
     const int nt = pair_blocks(goff_s[e + 1] - goff_s[e]);
     const int pairs = nt * (nt + 1) / 2;
     if (t < pairs) {
@@ -130,6 +146,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
   __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
   __shared__ int ntiles_s;
+  __shared__ int order_s[LUFFY_MAX_EXPERTS];
   __shared__ __align__(16) float njs_all[8 * 32];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -164,6 +181,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     if (i < E) gcnt_s[i] = a.gcnt[i];
   }
   __syncthreads();
+  group_order(gcnt_s, E, order_s);
   if (threadIdx.x == 0) {
     int n = 0;
     for (int e = 0; e < E; ++e) {
@@ -185,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
       for (int t = tile0; t < ntiles; t += tstride) {
         if (HIST && a.tskip != nullptr && a.tskip[t]) continue;  // decided by history: nothing to measure
         int e, I, J;
-        decode_tile(t, goff_s, E, e, I, J);
+        decode_tile(t, goff_s, order_s, E, e, I, J);
         const int h = (int)crank * TS;
         const int rI = goff_s[e] + I * 2 * TS + h, rJ = goff_s[e] + J * 2 * TS + h;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -231,9 +249,16 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     float* njs = njs_all + (warp - 2) * 32;  // this warp's column norms (fp32)
     int acc = 0;
     uint32_t aphase = 0;
+    // every epilogue thread's words of the tile are globally visible before its group's counter moves
+    auto tile_done = [&](int e) {
+      if (a.gdone == nullptr) return;
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (warp == 2 && lane == 0) atomicAdd(a.gdone + e, 1u);
+    };
     for (int t = tile0; t < ntiles; t += tstride) {
       int e, I, J;
-      decode_tile(t, goff_s, E, e, I, J);
+      decode_tile(t, goff_s, order_s, E, e, I, J);
       const int n = gcnt_s[e];
       const int npad = goff_s[e + 1] - goff_s[e];
       const int W = npad >> 5;
@@ -270,6 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
           store_sym(a.hone + a.adjoff[e], W, li, i0, j0, lane, d1, diag);
           store_sym(a.hzero + a.adjoff[e], W, li, i0, j0, lane, d0, diag);
         }
+        tile_done(e);
         continue;
       }
       tc::mbar_wait(&tfull[acc], aphase);
@@ -366,6 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
       if (lane == 0) tc::mbar_arrive_cluster_relaxed(tc::map_rank(&tempty[acc], 0));
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
+      tile_done(e);
     }
   }
   tc::tc_fence_before();
@@ -459,9 +486,16 @@ __global__ void __launch_bounds__(2 * TS) hist_flags_kernel(const int32_t* __res
                                                             unsigned long long* __restrict__ counts) {
   pdl_enter();
   __shared__ int32_t goff_s[LUFFY_MAX_EXPERTS + 1];
+  __shared__ int32_t gcnt_s[LUFFY_MAX_EXPERTS];
+  __shared__ int order_s[LUFFY_MAX_EXPERTS];
   __shared__ uint32_t colw[2 * TS / 32];
   __shared__ int ntiles_s;
-  for (int i = threadIdx.x; i <= E; i += blockDim.x) goff_s[i] = goff[i];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+    goff_s[i] = goff[i];
+    if (i < E) gcnt_s[i] = gcnt[i];
+  }
+  __syncthreads();
+  group_order(gcnt_s, E, order_s);  // the Gram's tile order (tskip is indexed by it)
   __syncthreads();
   if (threadIdx.x == 0) {
     int nt = 0;
@@ -476,7 +510,7 @@ __global__ void __launch_bounds__(2 * TS) hist_flags_kernel(const int32_t* __res
   unsigned long long dec_pairs = 0, skipped = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int e, I, J;
-    decode_tile(t, goff_s, E, e, I, J);
+    decode_tile(t, goff_s, order_s, E, e, I, J);
     const int g0 = goff_s[e], npad = goff_s[e + 1] - g0, n = gcnt[e], W = npad >> 5;
     const int lj = J * 2 * TS + threadIdx.x;
     const bool cv = lj < n && gnorm[g0 + lj] > 0.0;
@@ -536,6 +570,7 @@ int launch_gram_tc(luffy_layer* L, float h, unsigned long long* band, void* s) {
   a.gdump = L->dbg_gram;
   a.gdump_cap = (int64_t)L->dbg_gram_cap;
   a.band = band;
+  a.gdone = L->gdone;
   const bool hist = L->fast_measure;
   if (hist) {
     a.hone = L->hone;

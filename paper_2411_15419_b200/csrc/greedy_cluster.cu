@@ -50,8 +50,15 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
                                                                       int max_rounds, int cache_words, int E,
                                                                       int32_t* __restrict__ gnrep,
                                                                       int32_t* __restrict__ mrank,
-                                                                      int32_t* __restrict__ mcnt_row) {
-  pdl_enter();
+                                                                      int32_t* __restrict__ mcnt_row,
+                                                                      const uint32_t* __restrict__ gdone) {
+  pdl_defer();
+  // With the tensor-core Gram in front (gdone != nullptr) a group starts as soon as ITS pair tiles are in
+  // (per-group counters, below) instead of waiting for the whole Gram grid: clusters take the SMs the Gram's
+  // last partial wave leaves idle.  The grouping outputs read here were complete before the Gram released
+  // its dependents (it waited for them first).
+  if (gdone == nullptr) pdl_enter();
+  else pdl_launch_only();
   extern __shared__ __align__(16) uint8_t gsm[];
   __shared__ int order_s[LUFFY_MAX_EXPERTS];
   __shared__ int list_s[LUFFY_MAX_EXPERTS];
@@ -98,6 +105,19 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
   const int g0 = goff[e];
   const int n = gcnt[e];
   const int W = (goff[e + 1] - g0) >> 5;
+  if (gdone != nullptr) {  // this group's adjacency complete: 2 arrivals per pair tile
+    if (threadIdx.x == 0) {
+      const int nt = (W * 32 / 128 + 1) / 2;
+      const uint32_t need = (uint32_t)(nt * (nt + 1));
+      uint32_t got;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(gdone + e) : "memory");
+        if (got >= need) break;
+        __nanosleep(100);
+      }
+    }
+    __syncthreads();
+  }
   KT* key = reinterpret_cast<KT*>(gsm);
   KT* m1 = key + nmax;
   uint32_t* alive = reinterpret_cast<uint32_t*>(m1 + nmax);
@@ -353,7 +373,8 @@ int launch_cluster(luffy_layer* L, int nmax, size_t smem, int cache_words, int n
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   LUFFY_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, (const int32_t*)L->goff, (const int32_t*)L->gcnt,
                                     (const int64_t*)L->adjoff, (const uint32_t*)L->adj, L->rep_local, L->ctrl, nmax,
-                                    kGreedyMaxRounds, cache_words, L->E, L->gnrep, L->mrank, L->mcnt_row));
+                                    kGreedyMaxRounds, cache_words, L->E, L->gnrep, L->mrank, L->mcnt_row,
+                                    (const uint32_t*)(L->gdone_live && pdl_enabled() ? L->gdone : nullptr)));
   LUFFY_LAUNCHED();
   return 0;
 }

@@ -115,6 +115,8 @@ struct luffy_layer {
   uint32_t* x_err_h;     // [2] mapped pinned host memory: first timed-out exchange wait (phase + 1, seq)
   uint32_t* x_err_d;     // its device alias
   uint32_t* x_errw;      // [2] device copy polled by the waits (workspace)
+  uint32_t* gdone;       // [E] Gram pair tiles finished per group (x2: both CTAs of a pair), zeroed by grouping
+  bool gdone_live;       // the tensor-core Gram of this condense counts into gdone (the greedy waits on it)
   uint32_t* dseq;        // [1] device step sequence number (world > 1: bumped by luffy_route's first launch;
                          //     every exchange flag carries it, so a captured step replays correctly)
   uint64_t x_timeout_ns; // bound of every cross-rank wait (LUFFY_EXCHANGE_TIMEOUT_MS, luffy_layer_set_exchange_timeout)

@@ -249,12 +249,16 @@ __global__ void __launch_bounds__(THREADS, 1) gram_tc_kernel(const __grid_consta
     float* njs = njs_all + (warp - 2) * 32;  // this warp's column norms (fp32)
     int acc = 0;
     uint32_t aphase = 0;
-    // every epilogue thread's words of the tile are globally visible before its group's counter moves
+    // every epilogue thread's words of the tile are globally visible before its group's counter moves:
+    // the epilogue warps meet at a CTA barrier, then one thread's gpu-scope fence (cumulative over what the
+    // barrier ordered before it) and the increment
     auto tile_done = [&](int e) {
       if (a.gdone == nullptr) return;
-      __threadfence();
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (warp == 2 && lane == 0) atomicAdd(a.gdone + e, 1u);
+      if (warp == 2 && lane == 0) {
+        __threadfence();
+        atomicAdd(a.gdone + e, 1u);
+      }
     };
     for (int t = tile0; t < ntiles; t += tstride) {
       int e, I, J;

@@ -28,9 +28,12 @@
  *    torch.distributed) and passes them to luffy_layer_ipc_open.  The pack kernel, the GEMM2 / dgrad1
  *    epilogues and the uncondense backward then store rows straight into the destination rank's buffer
  *    and publish per-step sequence flags (system-scope release); consumers wait on the device (acquire),
- *    so no host synchronisation is needed.  With world > 1 the expert-side and gathered buffer
- *    arguments are NULL (the layer's exchange buffers are used; luffy_layer_exchange_buffers returns them).
- *    All ranks must issue the same sequence of calls.
+ *    so no host synchronisation is needed.  The step number the flags carry lives in device memory and is
+ *    advanced by luffy_route's first launch, so a step (luffy_route .. luffy_route_bwd, no sequence
+ *    migration) captured in a CUDA graph replays correctly; the receive buffers alternate by step
+ *    parity, so capture two consecutive steps and replay them alternately.  With world > 1 the
+ *    expert-side and gathered buffer arguments are NULL (the layer's exchange buffers are used;
+ *    luffy_layer_exchange_buffers returns them).  All ranks must issue the same sequence of calls.
  *  - Errors: arguments are validated on the host before anything is enqueued; on failure a status is
  *    returned, nothing is launched and luffy_last_error() describes the problem.  CUDA failures map to
  *    LUFFY_E_CUDA.  Calling out of order returns LUFFY_E_STATE.  A rank that stops participating does not

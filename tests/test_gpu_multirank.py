@@ -70,3 +70,17 @@ def test_sequence_migration_parity(n, mode, extra):
     r = _run(n, "C2S", 0.9, extra=("--migrate", mode, "--q", "2") + tuple(extra))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count('"ok": true') == n
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_graph_replay_world_gt1(n):
+    """Two captured world > 1 steps replayed alternately give the eager step's outputs bitwise
+    (tests/mp_graph_worker.py): the exchange flags carry the device step number."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_graph_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count('"ok": true') == n

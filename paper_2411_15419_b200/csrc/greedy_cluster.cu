@@ -199,12 +199,12 @@ __global__ void __launch_bounds__(GC_THREADS, 1) greedy_cluster_kernel(const int
     // ---- A: residual degree -> key (own rows)
     FSTAMP();
     for (int w = w0 + threadIdx.x; w < w1; w += blockDim.x) win[w] = 0u;
-    for (int r = r0 + wid; r < r1; r += nwarp) {
+    // one thread per row: W independent word loads and popcounts per thread, no cross-lane reduction
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
       if (!((alive[r >> 5] >> (r & 31)) & 1u)) continue;
       int deg = 0;
-      for (int w = lane; w < W; w += 32) deg += __popc(RW(r, w) & alive[w]);
-      deg = __reduce_add_sync(0xffffffffu, deg);
-      if (lane == 0) key[r] = make_key<KT>(deg, r);
+      for (int w = 0; w < W; ++w) deg += __popc(RW(r, w) & alive[w]);
+      key[r] = make_key<KT>(deg, r);
     }
     FSTAMP();
     cluster.sync();
